@@ -1,0 +1,183 @@
+/*
+ * tinfer_sm100.h — C ABI of the B200 (sm_100a) Ernie generation path.
+ *
+ * The reference (`tinfer`, pure Python + numba) has no FFI layer; its hot path
+ * sits behind two Python APIs:
+ *   - the operator API `tinfer.kernels` (kernels.py:96-109 gemm_f32,
+ *     kernels.py:216-233 attend_f32, kernels.py:112-126 bias_add/gelu), called
+ *     only from model._gemm/_attend (model.py:407-437), and
+ *   - the model API `tinfer.model` (_forward_tokens model.py:440-504, and the
+ *     generate loop model.py:613-667) that the north star keeps.
+ * This header is the C boundary that replaces both: the tf_gemm / tf_attention /
+ * tf_embed_ln / tf_layernorm operators replace the numba kernels, and the
+ * model/session runtime replaces _forward_tokens plus the decode loop. The
+ * Python package `paper_2407_04991_b200` binds it with ctypes.
+ *
+ * Conventions
+ *   - Every entry point returns an int status (tf_status); it never throws.
+ *     tf_last_error() returns a thread-local message for the last failure.
+ *   - All tensor arguments are DEVICE pointers owned by the caller. Streams are
+ *     cudaStream_t passed as void*. One device per process.
+ *   - Activations and weights are f16 (IEEE binary16) with f32 accumulation;
+ *     every f32->f16 conversion is the reference's saturating RNE
+ *     (tensor.py:95-100).
+ *   - GEMM operands are K-major: activations [rows, ld] row-major, weights packed
+ *     as W^T [out_features, ld] (the reference stores W as [in, out],
+ *     model.py:190-207). K is zero-padded to a multiple of 64 (ld >= pad64(K)).
+ *   - The ctypes call releases the GIL, preserving the reference kernels'
+ *     nogil=True threading contract (kernels.py:42-233).
+ */
+#ifndef TINFER_SM100_H
+#define TINFER_SM100_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TF_ABI_VERSION 1
+
+enum tf_status {
+  TF_OK = 0,
+  TF_ERR_ARG = 1,         /* -> ParameterError */
+  TF_ERR_SHAPE = 2,       /* -> DimensionError */
+  TF_ERR_CUDA = 3,        /* -> DeviceError    */
+  TF_ERR_UNSUPPORTED = 4, /* -> DeviceError    */
+  TF_ERR_CAPACITY = 5     /* -> CapacityError  */
+};
+
+/* GEMM epilogues (fused; replaces the fused/unfused bias + GELU launches of
+ * model._gemm, model.py:407-426, and the residual adds model.py:481/493). */
+enum tf_epilogue {
+  TF_EPI_F32 = 0,        /* out_f32 = acc                                   */
+  TF_EPI_BIAS = 1,       /* out = q16(acc + bias)                           */
+  TF_EPI_BIAS_GELU = 2,  /* out = q16(gelu_tanh(acc + bias))                */
+  TF_EPI_BIAS_RESID = 3, /* out = q16(resid + q16(acc + bias))              */
+  TF_EPI_QKV = 4,        /* q16(acc + bias) -> q buffer / K cache / V cache */
+  TF_EPI_LOGITS = 5      /* q16(acc) -> logits and/or argmax keys           */
+};
+
+int tf_abi_version(void);
+const char* tf_last_error(void);
+/* SM count and compute capability of the current device. */
+int tf_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ------------------------------------------------------------------ operators */
+
+/* out[m_tok, n_feat] = epilogue(act[m_tok, k] . wt[n_feat, k]^T).
+ * Replaces kernels.gemm_f32 (kernels.py:96-109) + bias_add/gelu (112-126). */
+typedef struct tf_gemm_desc {
+  int m_tok, n_feat, k;
+  const void* act; int lda;      /* f16 [m_tok, lda]                              */
+  const void* wt; int ldw;       /* f16 [n_feat, ldw]                             */
+  int epilogue;                  /* tf_epilogue                                   */
+  const float* bias;             /* [n_feat] or NULL (EPI_F32 / EPI_LOGITS)       */
+  void* out; int ldo;            /* f16 (or f32 for TF_EPI_F32) [m_tok, ldo]      */
+  const void* resid; int ldr;    /* TF_EPI_BIAS_RESID: f16 [m_tok, ldr]           */
+  /* TF_EPI_QKV: features [0,H) -> q_out[tok, ldq]; [H,2H) / [2H,3H) -> cache
+   * [B, heads, cap, head_dim] at slot (*qbase_dev + tok % seq_len), B = tok / seq_len */
+  void* q_out; int ldq;
+  void* k_cache; void* v_cache;
+  int hidden, heads, head_dim, cap, seq_len;
+  const int* qbase_dev;
+  unsigned long long* argmax_keys; /* TF_EPI_LOGITS: [m_tok] packed keys (zeroed) or NULL */
+  float* workspace; size_t workspace_bytes; /* split-K partial tiles                 */
+  int* counters; int n_counters;            /* zero-initialised split-K tile counters */
+  int force_swap;                /* -1 auto (swap-AB when m_tok <= 256), 0, 1      */
+  int splits;                    /* 0 auto; else must divide ceil(k/64)             */
+  int pdl;                       /* launch with programmatic dependent launch       */
+} tf_gemm_desc;
+int tf_gemm(const tf_gemm_desc* d, void* stream);
+
+/* x = q16(tok_emb[id] + pos_emb[p] (+ type_emb[t])); h = q16(LN(x)) (h optional).
+ * Replaces the gather-sum of model.py:453-455 / embed (model.py:521-534) and the
+ * first layer_norm_f32 (tensor.py:153-160). `remap` (optional) maps original ids
+ * to pruned ids (pruning.py:50-52); ids outside the map go to unk_id
+ * (SPEC.md:306). */
+typedef struct tf_embed_desc {
+  int n_tok, hidden, vocab, max_pos;
+  const int* ids; const int* pos; const int* type_ids;
+  const int* remap; int remap_n; int unk_id;
+  const void* tok_emb; const void* pos_emb; const void* type_emb; int ldw;
+  const float* ln_gamma; const float* ln_beta;
+  void* x; void* h; int ldx;
+  int* ids_out;
+} tf_embed_desc;
+int tf_embed_ln(const tf_embed_desc* d, void* stream);
+
+/* h[r] = q16(LN(x[r * src_stride + src_off])) (tensor.py:153-160). */
+int tf_layernorm(int n_rows, int hidden, const void* x, int ldx, int src_stride, int src_off,
+                 const float* gamma, const float* beta, void* h, int ldh, void* stream);
+
+/* Masked attention over the KV cache (kernels.attend_f32, kernels.py:216-233).
+ * q: [batch*seq_len, ldq] (head h at columns h*head_dim); caches [batch, heads,
+ * cap, head_dim]; row t of sequence b attends slots [start[b], *qbase_dev + t].
+ * seq_len == 1 selects the decode kernel. */
+int tf_attention(int batch, int heads, int head_dim, int cap, int seq_len, const void* q, int ldq,
+                 const void* k_cache, const void* v_cache, const int* start, const int* qbase_dev,
+                 float scale, void* out, int ldo, void* stream);
+
+/* ------------------------------------------------------------------ model runtime */
+
+typedef struct tf_layer_weights {
+  const float* ln1_gamma; const float* ln1_beta;
+  const void* wqkv_t; const float* bqkv; /* [3H, ldk_h] f16, [3H] f32 */
+  const void* wo_t; const float* bo;     /* [H, ldk_h], [H]            */
+  const float* ln2_gamma; const float* ln2_beta;
+  const void* w1_t; const float* b1;     /* [F, ldk_h], [F]            */
+  const void* w2_t; const float* b2;     /* [H, ldk_f], [H]            */
+} tf_layer_weights;
+
+typedef struct tf_model_desc {
+  int vocab, hidden, layers, heads, head_dim, ffn, max_pos;
+  int ldk_h, ldk_f;                      /* padded K strides for H and F inputs */
+  const void* tok_emb; const void* pos_emb; const void* type_emb; int n_types; int ldw;
+  const tf_layer_weights* layer;         /* [layers] */
+  const float* final_gamma; const float* final_beta;
+  const void* lm_head_t;                 /* [vocab, ldk_h] f16 */
+} tf_model_desc;
+int tf_model_create(const tf_model_desc* d, void** model);
+int tf_model_destroy(void* model);
+
+/* A generation session: one batch, its KV cache and scratch (all caller-owned). */
+typedef struct tf_session_desc {
+  int batch, capacity, max_tokens, max_new;
+  void* k_cache; void* v_cache;          /* [layers, batch, heads, capacity, head_dim] f16 */
+  void* x; void* h; void* q; void* attn; /* [batch*max_tokens, ldk_h] f16 */
+  void* ffn;                             /* [batch*max_tokens, ldk_f] f16 */
+  void* logits;                          /* optional [batch*max_tokens, vocab] f16 */
+  float* workspace; size_t workspace_bytes;
+  int* counters; int n_counters;
+  unsigned long long* keys;              /* [batch] argmax keys (zeroed) */
+  int* len_dev; int* step_dev;           /* device scalars */
+  int* out_tokens;                       /* [batch, max_new] */
+  const int* pads;                       /* [batch] left-pad offsets = first valid slot */
+  const int* remap; int remap_n; int unk_id;  /* optional prompt-id remap */
+} tf_session_desc;
+int tf_session_create(void* model, const tf_session_desc* d, void** session);
+int tf_session_destroy(void* session);
+
+enum tf_forward_mode {
+  TF_FWD_ARGMAX = 0,      /* last-row logits -> argmax -> out_tokens[:, step]; step++ */
+  TF_FWD_LOGITS_LAST = 1, /* last-row f16 logits -> logits[batch, vocab]              */
+  TF_FWD_LOGITS_ALL = 2   /* every row's f16 logits -> logits[batch*T, vocab]        */
+};
+/* Run T new tokens per sequence through every layer (model._forward_tokens,
+ * model.py:440-504): K/V appended at slots [len, len+T), len += T afterwards.
+ * ids/pos: device [batch*T] (pos may be NULL -> len - pads). ids may be NULL
+ * (T == 1): feed the previous argmax. */
+int tf_forward(void* session, const int* ids, const int* pos, int T, int mode, int pdl,
+               void* stream);
+/* n greedy decode steps (model.py:651-666), each a T=1 TF_FWD_ARGMAX forward fed
+ * by the previous argmax; with use_graph the step is captured once into a CUDA
+ * graph and replayed. */
+int tf_decode(void* session, int n_steps, int use_graph, void* stream);
+/* Kernels launched by one decode step (for the bench's gpu_launches count). */
+int tf_session_launches_per_step(void* session);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TINFER_SM100_H */

@@ -1,0 +1,308 @@
+// tcgen05 GEMM with fused generation-path epilogues (sm_100a).
+//
+// Computes C[i][j] = sum_k P[i][k] * Q[j][k] for two K-major f16 operands:
+//   prefill (SWAP=false): P = activations [tokens, K], Q = W^T [features, K]
+//   decode  (SWAP=true) : P = W^T [features, K],     Q = activations [tokens, K]
+// Swap-AB puts the (large) output-feature dimension on MMA-M = 128 and the
+// (small) decode batch on MMA-N = 16..256, so one CTA streams a 128-row weight
+// slab while the batch rides along in the N dimension.
+//
+// Structure (one output tile per CTA, 128 threads):
+//   warp 0 / lane 0 : TMA producer over a `stages`-deep smem ring (128B swizzle)
+//   warp 1 / lane 0 : tcgen05.mma issuer, f32 accumulator in TMEM
+//   warp 2          : TMEM allocation owner
+//   warps 0-3       : epilogue, tcgen05.ld 32 lanes x 16 columns at a time
+// Split-K (grid.z) is deterministic: every split writes its f32 partial tile to
+// a workspace, the last split to arrive (per-tile counter) sums the partials in
+// split order 0..S-1 and runs the epilogue. The split count depends only on
+// (features, K), never on the batch, so a row's result is batch-invariant.
+//
+// Epilogues implement the reference's f16 quantisation points exactly
+// (model.py:465-504): bias is added to the f32
+// accumulator, GELU (tanh form) in f32, then saturating RNE to f16; the residual
+// add is f32(x) + f32(o) rounded again.
+#pragma once
+
+#include "common.cuh"
+
+namespace tf {
+
+enum EpiMode : int {
+  EPI_F32 = 0,         // raw f32 accumulator store (operator API / tests)
+  EPI_BIAS = 1,        // out = q16(acc + b)
+  EPI_BIAS_GELU = 2,   // out = q16(gelu(acc + b))
+  EPI_BIAS_RESID = 3,  // out = q16(x + q16(acc + b))
+  EPI_QKV = 4,         // q16(acc + b) routed to q buffer / K cache / V cache
+  EPI_LOGITS = 5,      // q16(acc) stored and/or folded into a per-token argmax key
+};
+
+struct GemmArgs {
+  int rows_a, rows_b;  // rows of operand P and Q
+  int k_blocks;        // number of 64-wide K blocks
+  int kb_per_split;    // K blocks per split (grid.z = splits)
+  int splits;
+  int bn;              // Q rows per tile == MMA N (multiple of 16, <= 256)
+  int stages;
+  int m_tok, n_feat;   // logical output shape tokens x features
+  const float* bias;   // [n_feat] f32 (f16-representable values)
+  __half* out;         // [m_tok, ldo] f16
+  int ldo;
+  float* out_f32;      // EPI_F32 target [m_tok, ldo]
+  const __half* resid; // EPI_BIAS_RESID residual [m_tok, ldr] (may alias out)
+  int ldr;
+  // EPI_QKV routing: features [0,H) -> q_out, [H,2H) -> K cache, [2H,3H) -> V cache
+  __half* q_out;
+  int ldq;
+  __half* kc;  // layer base of [B, NH, cap, D]
+  __half* vc;
+  int H, NH, D, cap, T;
+  const int* qbase_dev;  // cache slot of token t = 0 (device scalar; graph-replayable)
+  // EPI_LOGITS
+  unsigned long long* keys;  // [m_tok] packed (value, ~id) argmax keys, or null
+  // split-K scratch
+  float* ws;
+  int* counters;
+};
+
+constexpr int kTileA = 128;          // MMA M
+constexpr int kBK = 64;              // K elements per stage (one 128-B swizzle row)
+constexpr int kABytes = kTileA * kBK * 2;
+
+__host__ __device__ inline int gemm_tmem_cols(int bn) {
+  return bn <= 32 ? 32 : (bn <= 64 ? 64 : (bn <= 128 ? 128 : 256));
+}
+__host__ __device__ inline int gemm_stage_bytes(int bn) { return kABytes + bn * kBK * 2; }
+__host__ inline size_t gemm_smem_bytes(int bn, int stages) {
+  return 1024 + (size_t)stages * gemm_stage_bytes(bn) + (2 * stages + 1) * 8 + 16;
+}
+
+template <int MODE, bool SWAP>
+__device__ __forceinline__ void epi_store(const GemmArgs& p, int tok, int f, float acc) {
+  if constexpr (MODE == EPI_F32) {
+    p.out_f32[(size_t)tok * p.ldo + f] = acc;
+  } else if constexpr (MODE == EPI_BIAS) {
+    p.out[(size_t)tok * p.ldo + f] = f16_sat(__fadd_rn(acc, p.bias[f]));
+  } else if constexpr (MODE == EPI_BIAS_GELU) {
+    p.out[(size_t)tok * p.ldo + f] = f16_sat(gelu_ref(__fadd_rn(acc, p.bias[f])));
+  } else if constexpr (MODE == EPI_BIAS_RESID) {
+    float o = q16(__fadd_rn(acc, p.bias[f]));
+    float x = __half2float(p.resid[(size_t)tok * p.ldr + f]);
+    p.out[(size_t)tok * p.ldo + f] = f16_sat(__fadd_rn(x, o));
+  } else if constexpr (MODE == EPI_QKV) {
+    __half val = f16_sat(__fadd_rn(acc, p.bias[f]));
+    int which = f / p.H;
+    int r = f - which * p.H;
+    if (which == 0) {
+      p.q_out[(size_t)tok * p.ldq + r] = val;
+    } else {
+      int b = tok / p.T, t = tok - b * p.T;
+      int head = r / p.D, d = r - head * p.D;
+      int slot = *p.qbase_dev + t;
+      size_t idx = (((size_t)b * p.NH + head) * p.cap + slot) * p.D + d;
+      (which == 1 ? p.kc : p.vc)[idx] = val;
+    }
+  } else if constexpr (MODE == EPI_LOGITS) {
+    if (p.out) p.out[(size_t)tok * p.ldo + f] = f16_sat(acc);
+  }
+}
+
+// Epilogue for one 16-column chunk held by this thread (A-tile row `ra`,
+// Q rows qb .. qb+15). For EPI_LOGITS with SWAP the argmax over the CTA's 128
+// features is reduced warp -> CTA -> one atomicMax per token.
+template <int MODE, bool SWAP>
+__device__ __forceinline__ void epi_chunk(const GemmArgs& p, int ra, int qb, const float (&v)[16],
+                                          unsigned long long* red) {
+  if constexpr (!SWAP) {
+    const int tok = ra;
+    if (tok < p.m_tok) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int f = qb + j;
+        if (f < p.n_feat) epi_store<MODE, SWAP>(p, tok, f, v[j]);
+      }
+    }
+    if constexpr (MODE == EPI_LOGITS) {
+      if (p.keys != nullptr && tok < p.m_tok) {
+        unsigned long long best = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int f = qb + j;
+          if (f < p.n_feat) {
+            unsigned long long k = argmax_key(q16(v[j]), (uint32_t)f);
+            best = k > best ? k : best;
+          }
+        }
+        atomicMax(&p.keys[tok], best);
+      }
+    }
+  } else {
+    const int f = ra;
+    const bool fok = f < p.n_feat;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int tok = qb + j;
+      if (fok && tok < p.m_tok) epi_store<MODE, SWAP>(p, tok, f, v[j]);
+    }
+    if constexpr (MODE == EPI_LOGITS) {
+      if (p.keys != nullptr) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          unsigned long long k = fok ? argmax_key(q16(v[j]), (uint32_t)f) : 0ull;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long other = __shfl_xor_sync(0xffffffffu, k, o);
+            k = other > k ? other : k;
+          }
+          if (lane == 0) red[warp * 16 + j] = k;
+        }
+        __syncthreads();
+        if (threadIdx.x < 16) {
+          const int tok = qb + threadIdx.x;
+          unsigned long long k = red[threadIdx.x];
+#pragma unroll
+          for (int w = 1; w < 4; ++w) k = red[w * 16 + threadIdx.x] > k ? red[w * 16 + threadIdx.x] : k;
+          if (tok < p.m_tok) atomicMax(&p.keys[tok], k);
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+template <int MODE, bool SWAP>
+__global__ void __launch_bounds__(128, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const GemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int bn = p.bn, stages = p.stages;
+  const int stage_bytes = gemm_stage_bytes(bn);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  __shared__ unsigned long long red[64];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile_a = blockIdx.x, tile_b = blockIdx.y, split = blockIdx.z;
+  const int kb0 = split * p.kb_per_split;
+  const int nkb = min(p.kb_per_split, p.k_blocks - kb0);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + stages),
+                 done_bar = smem_u32(bars + 2 * stages);
+  const uint32_t ncols = (uint32_t)gemm_tmem_cols(bn);
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(done_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), ncols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer. Weights do not depend on the previous
+    // kernel, so in decode (SWAP) mode the first ring's worth of weight tiles
+    // is requested before waiting on the programmatic launch dependency.
+    const uint32_t tx = (uint32_t)stage_bytes;
+    const int pre = SWAP ? min(stages, nkb) : 0;
+    for (int i = 0; i < pre; ++i) {
+      const uint32_t sa = smem_u32(smem + (size_t)i * stage_bytes);
+      mbar_expect_tx(full0 + 8 * i, tx);
+      tma_load_2d(sa, &tmA, (kb0 + i) * kBK, tile_a * kTileA, full0 + 8 * i);
+    }
+    pdl_wait();
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % stages;
+      const uint32_t ph = (uint32_t)(i / stages) & 1u;
+      const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
+      const uint32_t sb = sa + kABytes;
+      if (i >= pre) {
+        mbar_wait(empty0 + 8 * s, ph ^ 1u);
+        mbar_expect_tx(full0 + 8 * s, tx);
+        tma_load_2d(sa, &tmA, (kb0 + i) * kBK, tile_a * kTileA, full0 + 8 * s);
+      }
+      tma_load_2d(sb, &tmB, (kb0 + i) * kBK, tile_b * bn, full0 + 8 * s);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- single-thread MMA issuer
+    const uint32_t idesc = idesc_f16_m128((uint32_t)bn);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % stages;
+      const uint32_t ph = (uint32_t)(i / stages) & 1u;
+      mbar_wait(full0 + 8 * s, ph);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
+      const uint64_t da = umma_desc_sw128(sa);
+      const uint64_t db = umma_desc_sw128(sa + kABytes);
+#pragma unroll
+      for (int k = 0; k < kBK / 16; ++k) {
+        // advance 16 f16 = 32 B along K inside the swizzle atom (+2 in 16-B units)
+        tc_mma_f16(tmem, da + 2 * k, db + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+      }
+      tc_commit(empty0 + 8 * s);
+    }
+    tc_commit(done_bar);
+  }
+  __syncwarp();
+  pdl_trigger();
+
+  // ---------------- epilogue (all 4 warps)
+  pdl_wait();
+  mbar_wait(done_bar, 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;  // TMEM lane == row of the A tile
+  const int ra = tile_a * kTileA + row;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  float v[16];
+  if (p.splits == 1) {
+    for (int c = 0; c < bn; c += 16) {
+      tmem_ld16(trow + (uint32_t)c, v);
+      epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, red);
+    }
+  } else {
+    const int tile_id = tile_b * gridDim.x + tile_a;
+    const size_t tile_elems = (size_t)bn * kTileA;
+    float* base = p.ws + (size_t)tile_id * p.splits * tile_elems;
+    float* mine = base + (size_t)split * tile_elems;
+    for (int c = 0; c < bn; c += 16) {
+      tmem_ld16(trow + (uint32_t)c, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) __stcg(&mine[(size_t)(c + j) * kTileA + row], v[j]);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int prev = atomicAdd(&p.counters[tile_id], 1);
+      *last_flag = (prev == p.splits - 1);
+    }
+    __syncthreads();
+    if (*last_flag) {
+      __threadfence();
+      for (int c = 0; c < bn; c += 16) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+        for (int s = 0; s < p.splits; ++s) {
+          const float* part = base + (size_t)s * tile_elems;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], __ldcg(&part[(size_t)(c + j) * kTileA + row]));
+        }
+        epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, red);
+      }
+      if (threadIdx.x == 0) p.counters[tile_id] = 0;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem, ncols);
+}
+
+}  // namespace tf

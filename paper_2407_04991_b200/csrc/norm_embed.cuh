@@ -1,0 +1,166 @@
+// Embedding gather-sum (+ optional pruned-vocab remap and type row) fused with
+// the first LayerNorm, the stand-alone LayerNorm, and step bookkeeping.
+//
+// Numerics follow the reference exactly where it is integer/elementwise:
+//   x = q16(tok[id] + pos[p] (+ type[t]))      (model.py:453-455, bit-exact)
+//   LN: mean = sum/H; c = x - mean; var = sum(c*c)/H;
+//       y = q16(((c * (1/sqrt(var + 1e-5))) * g) + b)   (tensor.py:153-160)
+// Only the two reductions differ in summation order from numpy's pairwise sum.
+#pragma once
+
+#include "common.cuh"
+
+namespace tf {
+
+struct EmbedArgs {
+  int n_tok, H, V, P;
+  const int* ids;            // [n_tok] token ids (model vocab), or null -> keys
+  unsigned long long* keys;  // decode: argmax keys of the previous step (consumed + reset)
+  const int* remap;          // optional [remap_n] old->new id table (-1 = dropped)
+  int remap_n, unk_id;       // ids >= remap_n or unmapped -> unk_id
+  const int* pos;            // [n_tok] positions, or null -> (*len_dev - pads[row])
+  const int* len_dev;
+  const int* pads;
+  const int* type_ids;       // optional [n_tok]
+  const __half* tok_emb;     // [V, ldw]
+  const __half* pos_emb;     // [P, ldw]
+  const __half* type_emb;    // optional [n_types, ldw]
+  int ldw;
+  const float* ln_g;         // [H]
+  const float* ln_b;
+  __half* x;                 // [n_tok, ldx]
+  __half* h;                 // [n_tok, ldx] (may be null: no LN)
+  int ldx;
+  int* tok_out;              // optional: ids actually embedded
+};
+
+template <int VPL>
+__device__ __forceinline__ void ln_row_store(const float (&xv)[VPL], int H, const float* g,
+                                             const float* b, __half* hrow, int lane) {
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < H) s = __fadd_rn(s, xv[i]);
+  }
+  s = warp_sum(s);
+  const float mean = __fdiv_rn(s, (float)H);
+  float ss = 0.0f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < H) {
+      const float d = __fsub_rn(xv[i], mean);
+      ss = __fadd_rn(ss, __fmul_rn(d, d));
+    }
+  }
+  ss = warp_sum(ss);
+  const float var = __fdiv_rn(ss, (float)H);
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + 32 * i;
+    if (c < H) {
+      const float d = __fsub_rn(xv[i], mean);
+      hrow[c] = f16_sat(__fadd_rn(__fmul_rn(__fmul_rn(d, inv), g[c]), b[c]));
+    }
+  }
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256) embed_ln_kernel(const EmbedArgs a) {
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + warp;
+  if (row >= a.n_tok) return;
+  int id;
+  if (a.ids != nullptr) {
+    id = a.ids[row];
+  } else {
+    id = (int)argmax_id(a.keys[row]);
+  }
+  if (a.remap != nullptr) {
+    id = (id >= 0 && id < a.remap_n) ? a.remap[id] : -1;
+    if (id < 0) id = a.unk_id;
+  }
+  const int p = (a.pos != nullptr) ? a.pos[row] : (*a.len_dev - a.pads[row]);
+  const __half* tr = a.tok_emb + (size_t)id * a.ldw;
+  const __half* pr = a.pos_emb + (size_t)p * a.ldw;
+  const __half* yr = a.type_emb ? a.type_emb + (size_t)a.type_ids[row] * a.ldw : nullptr;
+  __half* xr = a.x + (size_t)row * a.ldx;
+  float xv[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + 32 * i;
+    float v = 0.0f;
+    if (c < a.H) {
+      v = __fadd_rn(__half2float(tr[c]), __half2float(pr[c]));
+      if (yr) v = __fadd_rn(v, __half2float(yr[c]));
+      const __half hv = f16_sat(v);
+      xr[c] = hv;
+      v = __half2float(hv);
+    }
+    xv[i] = v;
+  }
+  if (a.h != nullptr) ln_row_store<VPL>(xv, a.H, a.ln_g, a.ln_b, a.h + (size_t)row * a.ldx, lane);
+  if (lane == 0 && a.tok_out) a.tok_out[row] = id;
+  if (a.ids == nullptr && lane == 0) a.keys[row] = 0ull;  // consumed: reset for the next argmax
+  pdl_trigger();
+}
+
+struct LnArgs {
+  int n_rows, H;
+  const __half* x;  // source rows: x + (row * src_stride + src_off) * ldx
+  int ldx, src_stride, src_off;
+  const float* g;
+  const float* b;
+  __half* h;  // [n_rows, ldh]
+  int ldh;
+};
+
+template <int VPL>
+__global__ void __launch_bounds__(256) layernorm_kernel(const LnArgs a) {
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + warp;
+  if (row < a.n_rows) {
+    const __half* xr = a.x + ((size_t)row * a.src_stride + a.src_off) * a.ldx;
+    float xv[VPL];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = lane + 32 * i;
+      xv[i] = (c < a.H) ? __half2float(xr[c]) : 0.0f;
+    }
+    ln_row_store<VPL>(xv, a.H, a.g, a.b, a.h + (size_t)row * a.ldh, lane);
+  }
+  pdl_trigger();
+}
+
+// Step bookkeeping after the logits argmax: feed ids, append the generated
+// token, advance the device-side cache length (model.py:651-666).
+struct CollectArgs {
+  int B;
+  unsigned long long* keys;  // [B] consumed here only when consume != 0
+  int* out_tokens;           // [B, max_new]
+  int max_new;
+  int* step_dev;             // generated-token counter
+  int* len_dev;              // cache length
+  int advance;               // tokens appended to the cache by this forward
+};
+
+__global__ void collect_kernel(const CollectArgs a) {
+  pdl_wait();
+  const int step = *a.step_dev;
+  for (int b = threadIdx.x; b < a.B; b += blockDim.x) {
+    const int tok = (int)argmax_id(a.keys[b]);
+    if (step < a.max_new) a.out_tokens[(size_t)b * a.max_new + step] = tok;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *a.step_dev = step + 1;
+    *a.len_dev += a.advance;
+  }
+  pdl_trigger();
+}
+
+}  // namespace tf

@@ -1,0 +1,765 @@
+// C-ABI implementation: operator launchers + the native generation runtime
+// (model / session / forward / graph-captured decode loop). See
+// include/tinfer_sm100.h for the contract and the reference interfaces each
+// entry point replaces.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tinfer_sm100.h"
+#include "attention.cuh"
+#include "common.cuh"
+#include "gemm_tc.cuh"
+#include "norm_embed.cuh"
+
+using namespace tf;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+namespace {
+
+struct TfError {
+  int code;
+  std::string msg;
+};
+
+#define TF_CHECK_CUDA(expr)                                                             \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      throw TfError{TF_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)};   \
+  } while (0)
+
+#define TF_REQUIRE(cond, code, msg)                  \
+  do {                                               \
+    if (!(cond)) throw TfError{(code), (msg)};       \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TF_OK;
+  } catch (const TfError& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TF_ERR_CUDA;
+  }
+}
+
+int pad64(int k) { return (k + 63) / 64 * 64; }
+
+// ------------------------------------------------------------------ TMA maps
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+void load_encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  TF_REQUIRE(g_encode != nullptr, TF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+}
+
+// K-major f16 matrix [rows, ld]; box = 64 (K) x box_rows, 128-byte swizzle,
+// out-of-bounds rows/columns read as zero.
+CUtensorMap make_kmajor_map(const void* ptr, int rows, int k_extent, int ld, int box_rows) {
+  load_encoder();
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)k_extent, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TF_REQUIRE(r == CUDA_SUCCESS, TF_ERR_ARG,
+             "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + "): rows=" +
+                 std::to_string(rows) + " k=" + std::to_string(k_extent) +
+                 " ld=" + std::to_string(ld));
+  return m;
+}
+
+// ------------------------------------------------------------------ launch helper
+template <typename Kern, typename... Args>
+void launch(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  TF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    TF_CHECK_CUDA(cudaGetDevice(&dev));
+    TF_CHECK_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return g_num_sms;
+}
+
+// dynamic smem budget: 227 KB per CTA minus room for the kernels' static smem
+constexpr size_t kMaxSmem = 227 * 1024 - 1024;
+
+template <int MODE, bool SWAP>
+void ensure_gemm_attr() {
+  static bool done = false;
+  if (!done) {
+    TF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<MODE, SWAP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
+    done = true;
+  }
+}
+
+// ------------------------------------------------------------------ GEMM planning
+struct GemmPlan {
+  bool swap;
+  int bn, tiles_a, tiles_b, k_blocks, splits, stages;
+};
+
+// Deterministic split count: a function of (features, K) only, never of the
+// batch, so decode results are batch-invariant.
+int pick_splits(int tiles, int k_blocks) {
+  const int target = 128;
+  int best = 1;
+  for (int d = 1; d <= k_blocks && d <= 32; ++d) {
+    if (k_blocks % d) continue;
+    best = d;
+    if (tiles * d >= target) break;
+  }
+  return best;
+}
+
+GemmPlan plan_gemm(const tf_gemm_desc& d) {
+  GemmPlan p{};
+  p.k_blocks = (d.k + 63) / 64;
+  p.swap = d.force_swap >= 0 ? d.force_swap != 0 : d.m_tok <= 256;
+  if (p.swap) {
+    const int mt = d.m_tok < 256 ? d.m_tok : 256;
+    p.bn = ((mt + 15) / 16) * 16;
+    if (p.bn < 16) p.bn = 16;
+    p.tiles_a = (d.n_feat + 127) / 128;
+    p.tiles_b = (d.m_tok + p.bn - 1) / p.bn;
+  } else {
+    p.bn = d.n_feat >= 1024 ? 256 : 128;
+    if (d.n_feat < p.bn) p.bn = ((d.n_feat + 15) / 16) * 16;
+    if (p.bn < 16) p.bn = 16;
+    p.tiles_a = (d.m_tok + 127) / 128;
+    p.tiles_b = (d.n_feat + p.bn - 1) / p.bn;
+  }
+  if (d.splits > 0) {
+    TF_REQUIRE(p.k_blocks % d.splits == 0, TF_ERR_ARG, "splits must divide ceil(k/64)");
+    p.splits = d.splits;
+  } else {
+    p.splits = p.swap ? pick_splits(p.tiles_a * p.tiles_b, p.k_blocks) : 1;
+  }
+  const int kb_per = p.k_blocks / p.splits;
+  const int stage_bytes = gemm_stage_bytes(p.bn);
+  int st = (int)((kMaxSmem - 2048) / stage_bytes);
+  if (st > 8) st = 8;
+  if (st > kb_per) st = kb_per;
+  if (st < 1) st = 1;
+  p.stages = st;
+  return p;
+}
+
+template <int MODE, bool SWAP>
+void launch_gemm_t(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& ta,
+                   const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
+  ensure_gemm_attr<MODE, SWAP>();
+  dim3 grid(p.tiles_a, p.tiles_b, p.splits);
+  launch(gemm_tc_kernel<MODE, SWAP>, grid, dim3(128), gemm_smem_bytes(p.bn, p.stages), st,
+         d.pdl != 0, ta, tb, args);
+}
+
+template <int MODE>
+void launch_gemm_mode(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& ta,
+                      const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
+  if (p.swap)
+    launch_gemm_t<MODE, true>(d, p, ta, tb, args, st);
+  else
+    launch_gemm_t<MODE, false>(d, p, ta, tb, args, st);
+}
+
+void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
+  TF_REQUIRE(d.m_tok > 0 && d.n_feat > 0 && d.k > 0, TF_ERR_SHAPE, "gemm: empty shape");
+  TF_REQUIRE(d.act && d.wt, TF_ERR_ARG, "gemm: null operand");
+  const GemmPlan p = plan_gemm(d);
+  const int kext = p.k_blocks * 64;
+  TF_REQUIRE(d.lda >= kext && d.ldw >= kext, TF_ERR_SHAPE,
+             "gemm: leading dimensions must cover K padded to a multiple of 64");
+  TF_REQUIRE(d.lda % 8 == 0 && d.ldw % 8 == 0, TF_ERR_SHAPE, "gemm: ld must be a multiple of 8");
+  GemmArgs a{};
+  a.rows_a = p.swap ? d.n_feat : d.m_tok;
+  a.rows_b = p.swap ? d.m_tok : d.n_feat;
+  a.k_blocks = p.k_blocks;
+  a.splits = p.splits;
+  a.kb_per_split = p.k_blocks / p.splits;
+  a.bn = p.bn;
+  a.stages = p.stages;
+  a.m_tok = d.m_tok;
+  a.n_feat = d.n_feat;
+  a.bias = d.bias;
+  a.out = static_cast<__half*>(d.out);
+  a.out_f32 = static_cast<float*>(d.out);
+  a.ldo = d.ldo;
+  a.resid = static_cast<const __half*>(d.resid);
+  a.ldr = d.ldr;
+  a.q_out = static_cast<__half*>(d.q_out);
+  a.ldq = d.ldq;
+  a.kc = static_cast<__half*>(d.k_cache);
+  a.vc = static_cast<__half*>(d.v_cache);
+  a.H = d.hidden;
+  a.NH = d.heads;
+  a.D = d.head_dim;
+  a.cap = d.cap;
+  a.T = d.seq_len;
+  a.qbase_dev = d.qbase_dev;
+  a.keys = d.argmax_keys;
+  a.ws = d.workspace;
+  a.counters = d.counters;
+  switch (d.epilogue) {
+    case TF_EPI_BIAS:
+    case TF_EPI_BIAS_GELU:
+      TF_REQUIRE(d.bias && d.out, TF_ERR_ARG, "gemm: bias/out required");
+      break;
+    case TF_EPI_BIAS_RESID:
+      TF_REQUIRE(d.bias && d.out && d.resid, TF_ERR_ARG, "gemm: bias/out/resid required");
+      break;
+    case TF_EPI_QKV:
+      TF_REQUIRE(d.bias && d.q_out && d.k_cache && d.v_cache && d.qbase_dev, TF_ERR_ARG,
+                 "gemm: qkv routing pointers required");
+      TF_REQUIRE(d.n_feat == 3 * d.hidden && d.hidden == d.heads * d.head_dim && d.seq_len > 0,
+                 TF_ERR_SHAPE, "gemm: qkv shape");
+      break;
+    case TF_EPI_F32:
+      TF_REQUIRE(d.out, TF_ERR_ARG, "gemm: out required");
+      break;
+    case TF_EPI_LOGITS:
+      TF_REQUIRE(d.out || d.argmax_keys, TF_ERR_ARG, "gemm: logits need out or keys");
+      break;
+    default:
+      throw TfError{TF_ERR_ARG, "gemm: unknown epilogue"};
+  }
+  if (p.splits > 1) {
+    const size_t need = (size_t)p.tiles_a * p.tiles_b * p.splits * p.bn * kTileA * sizeof(float);
+    TF_REQUIRE(d.workspace && d.workspace_bytes >= need, TF_ERR_ARG,
+               "gemm: split-K workspace too small (" + std::to_string(need) + " bytes needed)");
+    TF_REQUIRE(d.counters && d.n_counters >= p.tiles_a * p.tiles_b, TF_ERR_ARG,
+               "gemm: split-K counters too small");
+  }
+  const void* P = p.swap ? d.wt : d.act;
+  const void* Q = p.swap ? d.act : d.wt;
+  const int ldp = p.swap ? d.ldw : d.lda, ldq = p.swap ? d.lda : d.ldw;
+  const CUtensorMap ta = make_kmajor_map(P, a.rows_a, kext, ldp, kTileA);
+  const CUtensorMap tb = make_kmajor_map(Q, a.rows_b, kext, ldq, p.bn);
+  switch (d.epilogue) {
+    case TF_EPI_F32: launch_gemm_mode<EPI_F32>(d, p, ta, tb, a, st); break;
+    case TF_EPI_BIAS: launch_gemm_mode<EPI_BIAS>(d, p, ta, tb, a, st); break;
+    case TF_EPI_BIAS_GELU: launch_gemm_mode<EPI_BIAS_GELU>(d, p, ta, tb, a, st); break;
+    case TF_EPI_BIAS_RESID: launch_gemm_mode<EPI_BIAS_RESID>(d, p, ta, tb, a, st); break;
+    case TF_EPI_QKV: launch_gemm_mode<EPI_QKV>(d, p, ta, tb, a, st); break;
+    case TF_EPI_LOGITS: launch_gemm_mode<EPI_LOGITS>(d, p, ta, tb, a, st); break;
+  }
+}
+
+// ------------------------------------------------------------------ LN / embed / attention
+int vpl_for(int H) {
+  const int v = (H + 31) / 32;
+  if (v <= 4) return 4;
+  if (v <= 8) return 8;
+  if (v <= 16) return 16;
+  if (v <= 24) return 24;
+  if (v <= 32) return 32;
+  if (v <= 48) return 48;
+  if (v <= 64) return 64;
+  return -1;
+}
+
+void run_embed(const EmbedArgs& a, cudaStream_t st, bool pdl) {
+  const dim3 grid((a.n_tok + 7) / 8);
+  switch (vpl_for(a.H)) {
+    case 4: launch(embed_ln_kernel<4>, grid, dim3(256), 0, st, pdl, a); break;
+    case 8: launch(embed_ln_kernel<8>, grid, dim3(256), 0, st, pdl, a); break;
+    case 16: launch(embed_ln_kernel<16>, grid, dim3(256), 0, st, pdl, a); break;
+    case 24: launch(embed_ln_kernel<24>, grid, dim3(256), 0, st, pdl, a); break;
+    case 32: launch(embed_ln_kernel<32>, grid, dim3(256), 0, st, pdl, a); break;
+    case 48: launch(embed_ln_kernel<48>, grid, dim3(256), 0, st, pdl, a); break;
+    case 64: launch(embed_ln_kernel<64>, grid, dim3(256), 0, st, pdl, a); break;
+    default: throw TfError{TF_ERR_UNSUPPORTED, "hidden size > 2048 unsupported"};
+  }
+}
+
+void run_ln(const LnArgs& a, cudaStream_t st, bool pdl) {
+  const dim3 grid((a.n_rows + 7) / 8);
+  switch (vpl_for(a.H)) {
+    case 4: launch(layernorm_kernel<4>, grid, dim3(256), 0, st, pdl, a); break;
+    case 8: launch(layernorm_kernel<8>, grid, dim3(256), 0, st, pdl, a); break;
+    case 16: launch(layernorm_kernel<16>, grid, dim3(256), 0, st, pdl, a); break;
+    case 24: launch(layernorm_kernel<24>, grid, dim3(256), 0, st, pdl, a); break;
+    case 32: launch(layernorm_kernel<32>, grid, dim3(256), 0, st, pdl, a); break;
+    case 48: launch(layernorm_kernel<48>, grid, dim3(256), 0, st, pdl, a); break;
+    case 64: launch(layernorm_kernel<64>, grid, dim3(256), 0, st, pdl, a); break;
+    default: throw TfError{TF_ERR_UNSUPPORTED, "hidden size > 2048 unsupported"};
+  }
+}
+
+void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
+  TF_REQUIRE(a.D >= 1 && a.D <= 128, TF_ERR_UNSUPPORTED, "head_dim must be in [1, 128]");
+  if (a.T == 1) {
+    const size_t smem = (size_t)(a.D + a.cap + 256) * sizeof(float);
+    TF_REQUIRE(smem <= kMaxSmem, TF_ERR_UNSUPPORTED, "cache capacity too large for decode kernel");
+    static bool attr = false;
+    if (!attr) {
+      TF_CHECK_CUDA(cudaFuncSetAttribute(attn_decode_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
+      attr = true;
+    }
+    launch(attn_decode_kernel, dim3(a.NH, a.B), dim3(128), smem, st, pdl, a);
+  } else {
+    const size_t smem = (size_t)kPfRows * a.D * sizeof(float) + (size_t)2 * kPfKeys * (a.D + 1) * 2;
+    launch(attn_prefill_kernel, dim3((a.T + kPfRows - 1) / kPfRows, a.NH, a.B), dim3(128), smem, st,
+           pdl, a);
+  }
+}
+
+// ------------------------------------------------------------------ runtime objects
+struct Model {
+  tf_model_desc d;
+  std::vector<tf_layer_weights> layers;
+};
+
+struct Session {
+  Model* m;
+  tf_session_desc d;
+  cudaGraphExec_t graph = nullptr;
+  int graph_launches = 0;
+  int launches_last = 0;
+};
+
+int* qbase_zero_ptr() {
+  // device scalar 0 for operator calls that start at slot 0
+  static int* p = nullptr;
+  if (!p) {
+    TF_CHECK_CUDA(cudaMalloc(&p, sizeof(int)));
+    TF_CHECK_CUDA(cudaMemset(p, 0, sizeof(int)));
+  }
+  return p;
+}
+
+// One forward of T tokens per sequence through every layer. Returns the number
+// of kernels launched.
+int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pdl,
+            cudaStream_t st) {
+  const tf_model_desc& m = s.m->d;
+  const tf_session_desc& sd = s.d;
+  const int B = sd.batch, M = B * T;
+  const int H = m.hidden, NH = m.heads, D = m.head_dim, F = m.ffn, L = m.layers;
+  TF_REQUIRE(T >= 1 && T <= sd.max_tokens, TF_ERR_SHAPE, "forward: T out of range");
+  TF_REQUIRE(ids != nullptr || T == 1, TF_ERR_ARG, "forward: ids required for T > 1");
+  TF_REQUIRE(mode != TF_FWD_ARGMAX || sd.out_tokens, TF_ERR_ARG, "forward: out_tokens required");
+  TF_REQUIRE(mode == TF_FWD_ARGMAX || sd.logits, TF_ERR_ARG, "forward: logits buffer required");
+  int launches = 0;
+  const size_t layer_cache = (size_t)B * NH * sd.capacity * D;
+  __half* x = static_cast<__half*>(sd.x);
+  __half* h = static_cast<__half*>(sd.h);
+
+  EmbedArgs e{};
+  e.n_tok = M;
+  e.H = H;
+  e.V = m.vocab;
+  e.P = m.max_pos;
+  e.ids = ids;
+  e.keys = sd.keys;
+  e.remap = ids ? sd.remap : nullptr;
+  e.remap_n = sd.remap_n;
+  e.unk_id = sd.unk_id;
+  e.pos = pos;
+  e.len_dev = sd.len_dev;
+  e.pads = sd.pads;
+  e.tok_emb = static_cast<const __half*>(m.tok_emb);
+  e.pos_emb = static_cast<const __half*>(m.pos_emb);
+  e.ldw = m.ldw;
+  e.ln_g = s.m->layers[0].ln1_gamma;
+  e.ln_b = s.m->layers[0].ln1_beta;
+  e.x = x;
+  e.h = h;
+  e.ldx = m.ldk_h;
+  run_embed(e, st, pdl);
+  ++launches;
+
+  tf_gemm_desc g{};
+  g.m_tok = M;
+  g.force_swap = -1;
+  g.workspace = sd.workspace;
+  g.workspace_bytes = sd.workspace_bytes;
+  g.counters = sd.counters;
+  g.n_counters = sd.n_counters;
+  g.pdl = pdl ? 1 : 0;
+
+  for (int l = 0; l < L; ++l) {
+    const tf_layer_weights& w = s.m->layers[l];
+    // fused QKV projection, K/V straight into the cache (model.py:464-474)
+    tf_gemm_desc q = g;
+    q.n_feat = 3 * H;
+    q.k = H;
+    q.act = h;
+    q.lda = m.ldk_h;
+    q.wt = w.wqkv_t;
+    q.ldw = m.ldk_h;
+    q.epilogue = TF_EPI_QKV;
+    q.bias = w.bqkv;
+    q.q_out = sd.q;
+    q.ldq = m.ldk_h;
+    q.k_cache = static_cast<__half*>(sd.k_cache) + l * layer_cache;
+    q.v_cache = static_cast<__half*>(sd.v_cache) + l * layer_cache;
+    q.hidden = H;
+    q.heads = NH;
+    q.head_dim = D;
+    q.cap = sd.capacity;
+    q.seq_len = T;
+    q.qbase_dev = sd.len_dev;
+    run_gemm(q, st);
+    ++launches;
+    // attention over slots [pad_b, len + t] (model.py:475-478)
+    AttnArgs at{};
+    at.B = B;
+    at.NH = NH;
+    at.D = D;
+    at.cap = sd.capacity;
+    at.T = T;
+    at.q = static_cast<const __half*>(sd.q);
+    at.ldq = m.ldk_h;
+    at.kc = static_cast<const __half*>(q.k_cache);
+    at.vc = static_cast<const __half*>(q.v_cache);
+    at.start = sd.pads;
+    at.qbase_dev = sd.len_dev;
+    at.scale = (float)(1.0 / std::sqrt((double)D));
+    at.out = static_cast<__half*>(sd.attn);
+    at.ldo = m.ldk_h;
+    run_attention(at, st, pdl);
+    ++launches;
+    // output projection + residual (model.py:478-482)
+    tf_gemm_desc o = g;
+    o.n_feat = H;
+    o.k = H;
+    o.act = sd.attn;
+    o.lda = m.ldk_h;
+    o.wt = w.wo_t;
+    o.ldw = m.ldk_h;
+    o.epilogue = TF_EPI_BIAS_RESID;
+    o.bias = w.bo;
+    o.out = x;
+    o.ldo = m.ldk_h;
+    o.resid = x;
+    o.ldr = m.ldk_h;
+    run_gemm(o, st);
+    ++launches;
+    // ffn_norm (model.py:484-486)
+    LnArgs ln{};
+    ln.n_rows = M;
+    ln.H = H;
+    ln.x = x;
+    ln.ldx = m.ldk_h;
+    ln.src_stride = 1;
+    ln.src_off = 0;
+    ln.g = w.ln2_gamma;
+    ln.b = w.ln2_beta;
+    ln.h = h;
+    ln.ldh = m.ldk_h;
+    run_ln(ln, st, pdl);
+    ++launches;
+    // FFN1 + GELU (model.py:488-490)
+    tf_gemm_desc f1 = g;
+    f1.n_feat = F;
+    f1.k = H;
+    f1.act = h;
+    f1.lda = m.ldk_h;
+    f1.wt = w.w1_t;
+    f1.ldw = m.ldk_h;
+    f1.epilogue = TF_EPI_BIAS_GELU;
+    f1.bias = w.b1;
+    f1.out = sd.ffn;
+    f1.ldo = m.ldk_f;
+    run_gemm(f1, st);
+    ++launches;
+    // FFN2 + residual (model.py:491-494)
+    tf_gemm_desc f2 = g;
+    f2.n_feat = H;
+    f2.k = F;
+    f2.act = sd.ffn;
+    f2.lda = m.ldk_f;
+    f2.wt = w.w2_t;
+    f2.ldw = m.ldk_f;
+    f2.epilogue = TF_EPI_BIAS_RESID;
+    f2.bias = w.b2;
+    f2.out = x;
+    f2.ldo = m.ldk_h;
+    f2.resid = x;
+    f2.ldr = m.ldk_h;
+    run_gemm(f2, st);
+    ++launches;
+    // next layer's attn_norm, or final_norm (model.py:460-462, 497-498)
+    LnArgs nl = ln;
+    if (l + 1 < L) {
+      nl.g = s.m->layers[l + 1].ln1_gamma;
+      nl.b = s.m->layers[l + 1].ln1_beta;
+    } else {
+      nl.g = m.final_gamma;
+      nl.b = m.final_beta;
+      if (mode != TF_FWD_LOGITS_ALL) {  // only the last position feeds the lm_head
+        nl.n_rows = B;
+        nl.src_stride = T;
+        nl.src_off = T - 1;
+      }
+    }
+    run_ln(nl, st, pdl);
+    ++launches;
+  }
+  // lm_head (+ argmax) (model.py:500-504, 594, 652)
+  tf_gemm_desc lg = g;
+  lg.m_tok = (mode == TF_FWD_LOGITS_ALL) ? M : B;
+  lg.n_feat = m.vocab;
+  lg.k = H;
+  lg.act = h;
+  lg.lda = m.ldk_h;
+  lg.wt = m.lm_head_t;
+  lg.ldw = m.ldk_h;
+  lg.epilogue = TF_EPI_LOGITS;
+  if (mode == TF_FWD_ARGMAX) {
+    lg.argmax_keys = sd.keys;
+  } else {
+    lg.out = sd.logits;
+    lg.ldo = m.vocab;
+  }
+  run_gemm(lg, st);
+  ++launches;
+  CollectArgs c{};
+  c.B = B;
+  c.keys = sd.keys;
+  c.out_tokens = mode == TF_FWD_ARGMAX ? sd.out_tokens : nullptr;
+  c.max_new = sd.max_new;
+  c.step_dev = sd.step_dev;
+  c.len_dev = sd.len_dev;
+  c.advance = T;
+  if (mode != TF_FWD_ARGMAX) {
+    // only advance the cache length: reuse collect with no token output
+    CollectArgs c2 = c;
+    c2.B = 0;
+    launch(collect_kernel, dim3(1), dim3(32), 0, st, pdl, c2);
+  } else {
+    launch(collect_kernel, dim3(1), dim3(256), 0, st, pdl, c);
+  }
+  ++launches;
+  return launches;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int tf_abi_version(void) { return TF_ABI_VERSION; }
+
+const char* tf_last_error(void) { return g_last_error.c_str(); }
+
+int tf_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  return guarded([&] {
+    int dev = 0;
+    TF_CHECK_CUDA(cudaGetDevice(&dev));
+    if (sm_count) TF_CHECK_CUDA(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev));
+    if (cc_major) TF_CHECK_CUDA(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (cc_minor) TF_CHECK_CUDA(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev));
+  });
+}
+
+int tf_gemm(const tf_gemm_desc* d, void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(d != nullptr, TF_ERR_ARG, "null desc");
+    run_gemm(*d, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tf_embed_ln(const tf_embed_desc* d, void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(d && d->ids && d->tok_emb && d->pos_emb && d->x, TF_ERR_ARG, "embed: null pointer");
+    TF_REQUIRE(d->pos != nullptr, TF_ERR_ARG, "embed: positions required");
+    TF_REQUIRE(!d->h || (d->ln_gamma && d->ln_beta), TF_ERR_ARG, "embed: LN params required");
+    EmbedArgs e{};
+    e.n_tok = d->n_tok;
+    e.H = d->hidden;
+    e.V = d->vocab;
+    e.P = d->max_pos;
+    e.ids = d->ids;
+    e.pos = d->pos;
+    e.type_ids = d->type_ids;
+    e.remap = d->remap;
+    e.remap_n = d->remap_n;
+    e.unk_id = d->unk_id;
+    e.tok_emb = static_cast<const __half*>(d->tok_emb);
+    e.pos_emb = static_cast<const __half*>(d->pos_emb);
+    e.type_emb = static_cast<const __half*>(d->type_emb);
+    e.ldw = d->ldw;
+    e.ln_g = d->ln_gamma;
+    e.ln_b = d->ln_beta;
+    e.x = static_cast<__half*>(d->x);
+    e.h = static_cast<__half*>(d->h);
+    e.ldx = d->ldx;
+    e.tok_out = d->ids_out;
+    if (d->n_tok > 0) run_embed(e, static_cast<cudaStream_t>(stream), false);
+  });
+}
+
+int tf_layernorm(int n_rows, int hidden, const void* x, int ldx, int src_stride, int src_off,
+                 const float* gamma, const float* beta, void* h, int ldh, void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(x && h && gamma && beta, TF_ERR_ARG, "layernorm: null pointer");
+    LnArgs a{n_rows, hidden, static_cast<const __half*>(x), ldx, src_stride, src_off,
+             gamma,  beta,   static_cast<__half*>(h),       ldh};
+    if (n_rows > 0) run_ln(a, static_cast<cudaStream_t>(stream), false);
+  });
+}
+
+int tf_attention(int batch, int heads, int head_dim, int cap, int seq_len, const void* q, int ldq,
+                 const void* k_cache, const void* v_cache, const int* start, const int* qbase_dev,
+                 float scale, void* out, int ldo, void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(q && k_cache && v_cache && start && out, TF_ERR_ARG, "attention: null pointer");
+    AttnArgs a{};
+    a.B = batch;
+    a.NH = heads;
+    a.D = head_dim;
+    a.cap = cap;
+    a.T = seq_len;
+    a.q = static_cast<const __half*>(q);
+    a.ldq = ldq;
+    a.kc = static_cast<const __half*>(k_cache);
+    a.vc = static_cast<const __half*>(v_cache);
+    a.start = start;
+    a.qbase_dev = qbase_dev ? qbase_dev : qbase_zero_ptr();
+    a.scale = scale;
+    a.out = static_cast<__half*>(out);
+    a.ldo = ldo;
+    if (batch > 0 && seq_len > 0) run_attention(a, static_cast<cudaStream_t>(stream), false);
+  });
+}
+
+int tf_model_create(const tf_model_desc* d, void** model) {
+  return guarded([&] {
+    TF_REQUIRE(d && model && d->layer, TF_ERR_ARG, "model: null desc");
+    TF_REQUIRE(d->hidden == d->heads * d->head_dim, TF_ERR_SHAPE, "model: hidden != heads*head_dim");
+    TF_REQUIRE(d->ldk_h >= pad64(d->hidden) && d->ldk_f >= pad64(d->ffn), TF_ERR_SHAPE,
+               "model: padded strides too small");
+    TF_REQUIRE(vpl_for(d->hidden) > 0, TF_ERR_UNSUPPORTED, "model: hidden > 2048");
+    TF_REQUIRE(d->head_dim <= 128, TF_ERR_UNSUPPORTED, "model: head_dim > 128");
+    Model* m = new Model();
+    m->d = *d;
+    m->layers.assign(d->layer, d->layer + d->layers);
+    m->d.layer = m->layers.data();
+    *model = m;
+  });
+}
+
+int tf_model_destroy(void* model) {
+  return guarded([&] { delete static_cast<Model*>(model); });
+}
+
+int tf_session_create(void* model, const tf_session_desc* d, void** session) {
+  return guarded([&] {
+    TF_REQUIRE(model && d && session, TF_ERR_ARG, "session: null argument");
+    TF_REQUIRE(d->batch >= 1 && d->capacity >= 1 && d->max_tokens >= 1, TF_ERR_SHAPE,
+               "session: bad sizes");
+    TF_REQUIRE(d->k_cache && d->v_cache && d->x && d->h && d->q && d->attn && d->ffn && d->keys &&
+                   d->len_dev && d->step_dev && d->pads,
+               TF_ERR_ARG, "session: missing buffer");
+    Session* s = new Session();
+    s->m = static_cast<Model*>(model);
+    s->d = *d;
+    *session = s;
+  });
+}
+
+int tf_session_destroy(void* session) {
+  return guarded([&] {
+    Session* s = static_cast<Session*>(session);
+    if (s && s->graph) cudaGraphExecDestroy(s->graph);
+    delete s;
+  });
+}
+
+int tf_forward(void* session, const int* ids, const int* pos, int T, int mode, int pdl,
+               void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(session, TF_ERR_ARG, "forward: null session");
+    Session& s = *static_cast<Session*>(session);
+    s.launches_last = forward(s, ids, pos, T, mode, pdl != 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tf_decode(void* session, int n_steps, int use_graph, void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(session, TF_ERR_ARG, "decode: null session");
+    Session& s = *static_cast<Session*>(session);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n_steps <= 0) return;
+    if (!use_graph) {
+      for (int i = 0; i < n_steps; ++i)
+        s.launches_last = forward(s, nullptr, nullptr, 1, TF_FWD_ARGMAX, true, st);
+      return;
+    }
+    if (!s.graph) {
+      // capture one decode step on a private stream; every per-step quantity
+      // (cache length, fed ids, output column) lives in device memory
+      cudaStream_t cs;
+      TF_CHECK_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      cudaGraph_t g;
+      TF_CHECK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      int launches = 0;
+      try {
+        launches = forward(s, nullptr, nullptr, 1, TF_FWD_ARGMAX, true, cs);
+      } catch (...) {
+        cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        throw;
+      }
+      TF_CHECK_CUDA(cudaStreamEndCapture(cs, &g));
+      TF_CHECK_CUDA(cudaGraphInstantiate(&s.graph, g, 0));
+      TF_CHECK_CUDA(cudaGraphDestroy(g));
+      TF_CHECK_CUDA(cudaStreamDestroy(cs));
+      s.graph_launches = launches;
+    }
+    for (int i = 0; i < n_steps; ++i) TF_CHECK_CUDA(cudaGraphLaunch(s.graph, st));
+    s.launches_last = s.graph_launches;
+  });
+}
+
+int tf_session_launches_per_step(void* session) {
+  if (!session) return -1;
+  return static_cast<Session*>(session)->launches_last;
+}
+
+}  // extern "C"
