@@ -1,0 +1,240 @@
+"""Device mirror of a host ``Model`` and per-batch generation sessions.
+
+``DeviceModel`` packs the reference weights (``[in, out]`` row-major, reference
+model.py:190-207) into the layout the sm_100a kernels stream:
+
+* every projection as f16 ``W^T [out, pad64(in)]`` (K-major, zero-padded K) so
+  TMA can fetch 64-wide K slabs with a 128-byte swizzle;
+* Q, K and V fused into one ``[3H, pad64(H)]`` matrix (one GEMM, K/V written
+  straight into the cache by the epilogue);
+* LayerNorm parameters and biases as f32 (they hold f16-representable values
+  for F16 models, and the epilogues add them in f32 like the reference);
+* the untied lm_head transposed to ``[V, pad64(H)]``.
+
+F32 models are rounded to f16 on upload (saturating RNE, tensor.py:95-100): the
+device path always stores f16 and accumulates in f32.
+
+``Session`` owns one batch's KV cache ``[L, B, NH, cap, D]`` (reference layout,
+model.py:316-317) and activation scratch, plus the native ``tf_session`` whose
+decode step is captured into a CUDA graph on first use and replayed.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .ops import pad64
+from .tensor import round_to, DType
+
+
+def _f16_kmajor(w_in_out: np.ndarray, ld: int) -> np.ndarray:
+    k, n = w_in_out.shape
+    buf = np.zeros((n, ld), dtype=np.float16)
+    buf[:, :k] = round_to(np.asarray(w_in_out, dtype=np.float32), DType.F16).T
+    return buf
+
+
+def _f32_vec(v: np.ndarray) -> np.ndarray:
+    return round_to(np.asarray(v, dtype=np.float32), DType.F16).astype(np.float32)
+
+
+class DeviceModel:
+    """Packed, device-resident weights + the native ``tf_model`` handle."""
+
+    def __init__(self, model, device: torch.device):
+        c = model.config
+        self.config = c
+        self.device = device
+        self.H, self.F, self.V = c.hidden_size, c.ffn_size, c.vocab_size
+        self.L, self.NH, self.D, self.P = c.num_layers, c.num_heads, c.head_dim, c.max_position
+        self.ldk_h, self.ldk_f = pad64(self.H), pad64(self.F)
+        self.lock = threading.Lock()
+        f32 = {name: t.array.astype(np.float32) for name, t in model.named_tensors()}
+        up16 = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+        self._keep = []
+
+        def keep(t):
+            self._keep.append(t)
+            return t
+
+        self.tok_emb = keep(up16(round_to(f32["token_embedding"], DType.F16)))
+        self.pos_emb = keep(up16(round_to(f32["position_embedding"], DType.F16)))
+        layers = (N.LayerWeights * self.L)()
+        self.layers = []
+        for i in range(self.L):
+            p = f"layers.{i}."
+            wqkv = np.concatenate([f32[p + "attn.wq"], f32[p + "attn.wk"], f32[p + "attn.wv"]], axis=1)
+            bqkv = np.concatenate([f32[p + "attn.bq"], f32[p + "attn.bk"], f32[p + "attn.bv"]])
+            lw = dict(
+                ln1_gamma=up16(_f32_vec(f32[p + "attn_norm.gamma"])),
+                ln1_beta=up16(_f32_vec(f32[p + "attn_norm.beta"])),
+                wqkv_t=up16(_f16_kmajor(wqkv, self.ldk_h)), bqkv=up16(_f32_vec(bqkv)),
+                wo_t=up16(_f16_kmajor(f32[p + "attn.wo"], self.ldk_h)), bo=up16(_f32_vec(f32[p + "attn.bo"])),
+                ln2_gamma=up16(_f32_vec(f32[p + "ffn_norm.gamma"])),
+                ln2_beta=up16(_f32_vec(f32[p + "ffn_norm.beta"])),
+                w1_t=up16(_f16_kmajor(f32[p + "ffn.w1"], self.ldk_h)), b1=up16(_f32_vec(f32[p + "ffn.b1"])),
+                w2_t=up16(_f16_kmajor(f32[p + "ffn.w2"], self.ldk_f)), b2=up16(_f32_vec(f32[p + "ffn.b2"])),
+            )
+            self.layers.append(lw)
+            for k, t in lw.items():
+                setattr(layers[i], k, t.data_ptr())
+        self.final_gamma = keep(up16(_f32_vec(f32["final_norm.gamma"])))
+        self.final_beta = keep(up16(_f32_vec(f32["final_norm.beta"])))
+        self.lm_head_t = keep(up16(_f16_kmajor(f32["lm_head"], self.ldk_h)))
+        self._layer_structs = layers
+        d = N.ModelDesc()
+        d.vocab, d.hidden, d.layers, d.heads = self.V, self.H, self.L, self.NH
+        d.head_dim, d.ffn, d.max_pos = self.D, self.F, self.P
+        d.ldk_h, d.ldk_f = self.ldk_h, self.ldk_f
+        d.tok_emb, d.pos_emb, d.type_emb, d.n_types = self.tok_emb.data_ptr(), self.pos_emb.data_ptr(), None, 0
+        d.ldw = self.tok_emb.stride(0)
+        d.layer = layers
+        d.final_gamma, d.final_beta = self.final_gamma.data_ptr(), self.final_beta.data_ptr()
+        d.lm_head_t = self.lm_head_t.data_ptr()
+        h = C.c_void_p()
+        N.check(N.lib().tf_model_create(C.byref(d), C.byref(h)), "tf_model_create")
+        self.handle = h
+        # shared split-K scratch (sessions of one model run sequentially under self.lock)
+        self.ws_bytes = 64 << 20
+        self.ws = torch.empty(self.ws_bytes // 4, dtype=torch.float32, device=device)
+        self.n_counters = 1 << 16
+        self.counters = torch.zeros(self.n_counters, dtype=torch.int32, device=device)
+        self._sessions: dict[tuple, Session] = {}
+
+    def weight_bytes(self) -> int:
+        """Bytes of weights one decode step streams (all layers + lm_head)."""
+        n = 0
+        for lw in self.layers:
+            for k in ("wqkv_t", "wo_t", "w1_t", "w2_t"):
+                n += lw[k].numel() * 2
+        return n + self.lm_head_t.numel() * 2
+
+    def session(self, batch: int, capacity: int, max_tokens: int, max_new: int,
+                logits: bool = False) -> "Session":
+        key = (batch, capacity, max_tokens, max_new, logits)
+        s = self._sessions.get(key)
+        if s is None:
+            if len(self._sessions) >= 8:  # bound the cache; drop the oldest
+                old = next(iter(self._sessions))
+                self._sessions.pop(old).close()
+            s = Session(self, batch, capacity, max_tokens, max_new, logits)
+            self._sessions[key] = s
+        return s
+
+    def close(self):
+        for s in self._sessions.values():
+            s.close()
+        self._sessions.clear()
+        if self.handle:
+            N.lib().tf_model_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Session:
+    """One batch shape: KV cache, activations, device step state, native handle."""
+
+    def __init__(self, dm: DeviceModel, batch: int, capacity: int, max_tokens: int, max_new: int,
+                 logits: bool, k_cache: torch.Tensor | None = None,
+                 v_cache: torch.Tensor | None = None):
+        dev = dm.device
+        self.dm, self.batch, self.capacity = dm, batch, capacity
+        self.max_tokens, self.max_new = max_tokens, max(1, max_new)
+        rows = batch * max_tokens
+        shape = (dm.L, batch, dm.NH, capacity, dm.D)
+        self.k_cache = k_cache if k_cache is not None else torch.zeros(shape, dtype=torch.float16, device=dev)
+        self.v_cache = v_cache if v_cache is not None else torch.zeros(shape, dtype=torch.float16, device=dev)
+        z16 = lambda n, ld: torch.zeros((n, ld), dtype=torch.float16, device=dev)  # noqa: E731
+        self.x, self.h = z16(rows, dm.ldk_h), z16(rows, dm.ldk_h)
+        self.q, self.attn = z16(rows, dm.ldk_h), z16(rows, dm.ldk_h)
+        self.ffn = z16(rows, dm.ldk_f)
+        self.logits = z16(rows, dm.V) if logits else None
+        self.keys = torch.zeros(batch, dtype=torch.int64, device=dev)
+        # int32 state: [len, step] + pads[B] + ids[rows] + pos[rows]
+        self.state = torch.zeros(2 + batch + 2 * rows, dtype=torch.int32, device=dev)
+        self.len_dev, self.step_dev = self.state[0:1], self.state[1:2]
+        self.pads = self.state[2:2 + batch]
+        self.ids = self.state[2 + batch:2 + batch + rows]
+        self.pos = self.state[2 + batch + rows:]
+        self.out_tokens = torch.zeros((batch, self.max_new), dtype=torch.int32, device=dev)
+        self.host_in = torch.zeros(self.state.numel(), dtype=torch.int32).pin_memory()
+        self.host_out = torch.zeros((batch, self.max_new), dtype=torch.int32).pin_memory()
+        self.remap = None
+        d = N.SessionDesc()
+        d.batch, d.capacity, d.max_tokens, d.max_new = batch, capacity, max_tokens, self.max_new
+        d.k_cache, d.v_cache = self.k_cache.data_ptr(), self.v_cache.data_ptr()
+        d.x, d.h, d.q, d.attn = self.x.data_ptr(), self.h.data_ptr(), self.q.data_ptr(), self.attn.data_ptr()
+        d.ffn = self.ffn.data_ptr()
+        d.logits = self.logits.data_ptr() if logits else None
+        d.workspace, d.workspace_bytes = dm.ws.data_ptr(), dm.ws_bytes
+        d.counters, d.n_counters = dm.counters.data_ptr(), dm.n_counters
+        d.keys = self.keys.data_ptr()
+        d.len_dev, d.step_dev = self.len_dev.data_ptr(), self.step_dev.data_ptr()
+        d.out_tokens = self.out_tokens.data_ptr()
+        d.pads = self.pads.data_ptr()
+        d.remap, d.remap_n, d.unk_id = None, 0, 0
+        self.desc = d
+        h = C.c_void_p()
+        N.check(N.lib().tf_session_create(dm.handle, C.byref(d), C.byref(h)), "tf_session_create")
+        self.handle = h
+        self.len = 0  # host mirror of the device cache length
+
+    # ------------------------------------------------------------------ steps
+    @staticmethod
+    def stream():
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def load_inputs(self, ids: np.ndarray, pos: np.ndarray, pads: np.ndarray, length: int = 0):
+        """One H2D copy of [len, step, pads, ids, pos] from pinned memory."""
+        B, rows = self.batch, ids.size
+        buf = self.host_in.numpy()
+        buf[0], buf[1] = length, 0
+        buf[2:2 + B] = pads
+        buf[2 + B:2 + B + rows] = ids.reshape(-1)
+        buf[2 + B + self.batch * self.max_tokens:2 + B + self.batch * self.max_tokens + rows] = pos.reshape(-1)
+        self.state.copy_(self.host_in, non_blocking=True)
+        self.keys.zero_()
+        self.len = length
+        return (2 + B + 2 * rows) * 4
+
+    def forward(self, T: int, mode: int, use_ids: bool = True, pdl: bool = True):
+        ids = C.c_void_p(self.ids.data_ptr()) if use_ids else None
+        pos = C.c_void_p(self.pos.data_ptr()) if use_ids else None
+        N.check(N.lib().tf_forward(self.handle, ids, pos, T, mode, 1 if pdl else 0, self.stream()),
+                "tf_forward")
+        self.len += T
+        return N.lib().tf_session_launches_per_step(self.handle)
+
+    def decode(self, n_steps: int, use_graph: bool = True) -> int:
+        if n_steps <= 0:
+            return 0
+        N.check(N.lib().tf_decode(self.handle, n_steps, 1 if use_graph else 0, self.stream()),
+                "tf_decode")
+        self.len += n_steps
+        return n_steps * N.lib().tf_session_launches_per_step(self.handle)
+
+    def fetch_tokens(self, n: int) -> np.ndarray:
+        self.host_out[:, :n].copy_(self.out_tokens[:, :n], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.host_out[:, :n].numpy().copy()
+
+    def close(self):
+        if getattr(self, "handle", None):
+            N.lib().tf_session_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
