@@ -83,10 +83,10 @@ typedef struct tf_gemm_desc {
   int hidden, heads, head_dim, cap, seq_len;
   const int* qbase_dev;
   unsigned long long* argmax_keys; /* TF_EPI_LOGITS: [m_tok] packed keys (zeroed) or NULL */
-  float* workspace; size_t workspace_bytes; /* split-K partial tiles                 */
-  int* counters; int n_counters;            /* zero-initialised split-K tile counters */
+  float* workspace; size_t workspace_bytes; /* reserved (split-K reduces via DSMEM)  */
+  int* counters; int n_counters;            /* reserved                              */
   int force_swap;                /* -1 auto (swap-AB when m_tok <= 256), 0, 1      */
-  int splits;                    /* 0 auto; else must divide ceil(k/64)             */
+  int splits;                    /* 0 auto; else divides ceil(k/64), <= 16 (cluster) */
   int pdl;                       /* launch with programmatic dependent launch       */
 } tf_gemm_desc;
 int tf_gemm(const tf_gemm_desc* d, void* stream);

@@ -12,10 +12,11 @@
 //   warp 1 / lane 0 : tcgen05.mma issuer, f32 accumulator in TMEM
 //   warp 2          : TMEM allocation owner
 //   warps 0-3       : epilogue, tcgen05.ld 32 lanes x 16 columns at a time
-// Split-K (grid.z) is deterministic: every split writes its f32 partial tile to
-// a workspace, the last split to arrive (per-tile counter) sums the partials in
-// split order 0..S-1 and runs the epilogue. The split count depends only on
-// (features, K), never on the batch, so a row's result is batch-invariant.
+// Split-K (grid.z) runs as one thread-block cluster per output tile: the S
+// K-slices reduce their f32 partial tiles through distributed shared memory in
+// split order 0..S-1 (deterministic, no global round trip). The split count
+// depends only on (features, K), never on the batch, so a row's result is
+// batch-invariant.
 //
 // Epilogues implement the reference's f16 quantisation points exactly
 // (model.py:465-504): bias is added to the f32
@@ -59,9 +60,6 @@ struct GemmArgs {
   const int* qbase_dev;  // cache slot of token t = 0 (device scalar; graph-replayable)
   // EPI_LOGITS
   unsigned long long* keys;  // [m_tok] packed (value, ~id) argmax keys, or null
-  // split-K scratch
-  float* ws;
-  int* counters;
 };
 
 constexpr int kTileA = 128;          // MMA M
@@ -72,8 +70,15 @@ __host__ __device__ inline int gemm_tmem_cols(int bn) {
   return bn <= 32 ? 32 : (bn <= 64 ? 64 : (bn <= 128 ? 128 : 256));
 }
 __host__ __device__ inline int gemm_stage_bytes(int bn) { return kABytes + bn * kBK * 2; }
-__host__ inline size_t gemm_smem_bytes(int bn, int stages) {
-  return 1024 + (size_t)stages * gemm_stage_bytes(bn) + (2 * stages + 1) * 8 + 16;
+// ring bytes: the pipeline stages, or the f32 partial tile of the cluster
+// split-K reduction if that is larger (it reuses the drained ring)
+__host__ __device__ inline size_t gemm_ring_bytes(int bn, int stages, int splits) {
+  size_t ring = (size_t)stages * gemm_stage_bytes(bn);
+  size_t part = splits > 1 ? (size_t)kTileA * bn * 4 : 0;
+  return ring > part ? ring : part;
+}
+__host__ inline size_t gemm_smem_bytes(int bn, int stages, int splits) {
+  return 1024 + gemm_ring_bytes(bn, stages, splits) + (2 * stages + 1) * 8 + 16;
 }
 
 template <int MODE, bool SWAP>
@@ -170,6 +175,14 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& p, int ra, int qb, con
   }
 }
 
+// single-element epilogue for the split-K reduction path (A-tile row ra, Q row qb)
+template <int MODE, bool SWAP>
+__device__ __forceinline__ void epi_elem(const GemmArgs& p, int ra, int qb, float acc) {
+  const int tok = SWAP ? qb : ra;
+  const int f = SWAP ? ra : qb;
+  if (tok < p.m_tok && f < p.n_feat) epi_store<MODE, SWAP>(p, tok, f, acc);
+}
+
 template <int MODE, bool SWAP>
 __global__ void __launch_bounds__(128, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -179,9 +192,8 @@ __global__ void __launch_bounds__(128, 1)
                                              ~static_cast<uintptr_t>(1023));
   const int bn = p.bn, stages = p.stages;
   const int stage_bytes = gemm_stage_bytes(bn);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)stages * stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + gemm_ring_bytes(bn, stages, p.splits));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 1);
-  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   __shared__ unsigned long long red[64];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -269,36 +281,32 @@ __global__ void __launch_bounds__(128, 1)
       epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, red);
     }
   } else {
-    const int tile_id = tile_b * gridDim.x + tile_a;
-    const size_t tile_elems = (size_t)bn * kTileA;
-    float* base = p.ws + (size_t)tile_id * p.splits * tile_elems;
-    float* mine = base + (size_t)split * tile_elems;
+    // Split-K across the CTAs of one thread-block cluster (grid.z == cluster.z
+    // == splits). Each CTA parks its f32 partial tile in its own (drained)
+    // pipeline smem as [column][128 rows]; after a cluster barrier every CTA
+    // reduces a contiguous 1/S slice of the tile by reading the S partials over
+    // DSMEM in split order 0..S-1 (deterministic), then runs the epilogue on it.
+    float* part = reinterpret_cast<float*>(smem);
     for (int c = 0; c < bn; c += 16) {
       tmem_ld16(trow + (uint32_t)c, v);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) __stcg(&mine[(size_t)(c + j) * kTileA + row], v[j]);
+      for (int j = 0; j < 16; ++j) part[(c + j) * kTileA + row] = v[j];
     }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const int prev = atomicAdd(&p.counters[tile_id], 1);
-      *last_flag = (prev == p.splits - 1);
+    cluster_sync();
+    const uint32_t rank = cluster_ctarank();
+    const int S = p.splits;
+    const int E = kTileA * bn;
+    const int per = (E + S - 1) / S;
+    const int e_lo = (int)rank * per, e_hi = min(E, e_lo + per);
+    const uint32_t local = smem_u32(part);
+    for (int e = e_lo + threadIdx.x; e < e_hi; e += 128) {
+      float acc = 0.0f;
+      for (int sp = 0; sp < S; ++sp)
+        acc = __fadd_rn(acc, ld_dsmem_f32(dsmem_addr(local + 4u * (uint32_t)e, (uint32_t)sp)));
+      const int col = e / kTileA, r = e - col * kTileA;
+      epi_elem<MODE, SWAP>(p, tile_a * kTileA + r, tile_b * bn + col, acc);
     }
-    __syncthreads();
-    if (*last_flag) {
-      __threadfence();
-      for (int c = 0; c < bn; c += 16) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.0f;
-        for (int s = 0; s < p.splits; ++s) {
-          const float* part = base + (size_t)s * tile_elems;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], __ldcg(&part[(size_t)(c + j) * kTileA + row]));
-        }
-        epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, red);
-      }
-      if (threadIdx.x == 0) p.counters[tile_id] = 0;
-    }
+    cluster_sync();  // partial tiles stay alive until every CTA has read them
   }
   tc_fence_before();
   __syncthreads();

@@ -67,6 +67,128 @@ __device__ __forceinline__ void ln_row_store(const float (&xv)[VPL], int H, cons
   }
 }
 
+// ---- 16-byte vectorised variants (H % 8 == 0): lane owns 8-element chunks
+// c8 = lane + 32*i; every load of the row (x, gamma, beta) is issued before the
+// first use so one row costs ~one memory round trip.
+__device__ __forceinline__ void unpack8(const uint4& r, float* f) {
+  const __half2* h = reinterpret_cast<const __half2*>(&r);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 t = __half22float2(h[e]);
+    f[2 * e] = t.x;
+    f[2 * e + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  uint4 r;
+  __half* h = reinterpret_cast<__half*>(&r);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) h[e] = f16_sat(f[e]);
+  return r;
+}
+
+template <int NC>
+__device__ __forceinline__ void ln_row_vec(float (&xv)[NC * 8], int H, const float* g,
+                                           const float* b, __half* hrow, int lane) {
+  float4 gv[NC * 2], bv[NC * 2];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int c = (lane + 32 * i) * 8;
+    if (c < H) {
+      gv[2 * i] = *reinterpret_cast<const float4*>(g + c);
+      gv[2 * i + 1] = *reinterpret_cast<const float4*>(g + c + 4);
+      bv[2 * i] = *reinterpret_cast<const float4*>(b + c);
+      bv[2 * i + 1] = *reinterpret_cast<const float4*>(b + c + 4);
+    }
+  }
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NC; ++i)
+    if ((lane + 32 * i) * 8 < H)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s = __fadd_rn(s, xv[8 * i + e]);
+  s = warp_sum(s);
+  const float mean = __fdiv_rn(s, (float)H);
+  float ss = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NC; ++i)
+    if ((lane + 32 * i) * 8 < H)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float d = __fsub_rn(xv[8 * i + e], mean);
+        ss = __fadd_rn(ss, __fmul_rn(d, d));
+      }
+  ss = warp_sum(ss);
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)H), 1e-5f)));
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int c = (lane + 32 * i) * 8;
+    if (c < H) {
+      const float* gf = reinterpret_cast<const float*>(&gv[2 * i]);
+      const float* bf = reinterpret_cast<const float*>(&bv[2 * i]);
+      float y[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        y[e] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[8 * i + e], mean), inv), gf[e]), bf[e]);
+      *reinterpret_cast<uint4*>(hrow + c) = pack8(y);
+    }
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) embed_ln_vec_kernel(const EmbedArgs a) {
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + warp;
+  if (row >= a.n_tok) return;
+  int id = (a.ids != nullptr) ? a.ids[row] : (int)argmax_id(a.keys[row]);
+  if (a.remap != nullptr) {
+    id = (id >= 0 && id < a.remap_n) ? a.remap[id] : -1;
+    if (id < 0) id = a.unk_id;
+  }
+  const int p = (a.pos != nullptr) ? a.pos[row] : (*a.len_dev - a.pads[row]);
+  const __half* tr = a.tok_emb + (size_t)id * a.ldw;
+  const __half* pr = a.pos_emb + (size_t)p * a.ldw;
+  const __half* yr = a.type_emb ? a.type_emb + (size_t)a.type_ids[row] * a.ldw : nullptr;
+  uint4 tv[NC], pv[NC], yv[NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int c = (lane + 32 * i) * 8;
+    if (c < a.H) {
+      tv[i] = *reinterpret_cast<const uint4*>(tr + c);
+      pv[i] = *reinterpret_cast<const uint4*>(pr + c);
+      if (yr) yv[i] = *reinterpret_cast<const uint4*>(yr + c);
+    }
+  }
+  __half* xr = a.x + (size_t)row * a.ldx;
+  float xv[NC * 8];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const int c = (lane + 32 * i) * 8;
+    if (c < a.H) {
+      float t[8], q[8];
+      unpack8(tv[i], t);
+      unpack8(pv[i], q);
+      float w[8];
+      if (yr) unpack8(yv[i], w);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float v = __fadd_rn(t[e], q[e]);
+        if (yr) v = __fadd_rn(v, w[e]);
+        xv[8 * i + e] = q16(v);
+      }
+      *reinterpret_cast<uint4*>(xr + c) = pack8(&xv[8 * i]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) xv[8 * i + e] = 0.0f;
+    }
+  }
+  if (a.h != nullptr) ln_row_vec<NC>(xv, a.H, a.ln_g, a.ln_b, a.h + (size_t)row * a.ldx, lane);
+  if (lane == 0 && a.tok_out) a.tok_out[row] = id;
+  if (a.ids == nullptr && lane == 0) a.keys[row] = 0ull;
+  pdl_trigger();
+}
+
 template <int VPL>
 __global__ void __launch_bounds__(256) embed_ln_kernel(const EmbedArgs a) {
   pdl_wait();
@@ -132,6 +254,34 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const LnArgs a) {
       xv[i] = (c < a.H) ? __half2float(xr[c]) : 0.0f;
     }
     ln_row_store<VPL>(xv, a.H, a.g, a.b, a.h + (size_t)row * a.ldh, lane);
+  }
+  pdl_trigger();
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) layernorm_vec_kernel(const LnArgs a) {
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + warp;
+  if (row < a.n_rows) {
+    const __half* xr = a.x + ((size_t)row * a.src_stride + a.src_off) * a.ldx;
+    uint4 raw[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = (lane + 32 * i) * 8;
+      if (c < a.H) raw[i] = *reinterpret_cast<const uint4*>(xr + c);
+    }
+    float xv[NC * 8];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      if ((lane + 32 * i) * 8 < a.H) {
+        unpack8(raw[i], &xv[8 * i]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xv[8 * i + e] = 0.0f;
+      }
+    }
+    ln_row_vec<NC>(xv, a.H, a.g, a.b, a.h + (size_t)row * a.ldh, lane);
   }
   pdl_trigger();
 }

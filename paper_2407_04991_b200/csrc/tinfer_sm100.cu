@@ -95,21 +95,36 @@ CUtensorMap make_kmajor_map(const void* ptr, int rows, int k_extent, int ld, int
 
 // ------------------------------------------------------------------ launch helper
 template <typename Kern, typename... Args>
-void launch(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
-            Args... args) {
+void launch_cluster(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                    int cluster_z, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  int n = 0;
   if (pdl) {
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
   }
+  if (cluster_z > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = 1;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = (unsigned)cluster_z;
+    ++n;
+  }
+  cfg.attrs = n ? attr : nullptr;
+  cfg.numAttrs = n;
   TF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
+template <typename Kern, typename... Args>
+void launch(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+            Args... args) {
+  launch_cluster(kern, grid, block, smem, st, pdl, 1, args...);
 }
 
 int g_num_sms = 0;
@@ -131,6 +146,8 @@ void ensure_gemm_attr() {
   if (!done) {
     TF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<MODE, SWAP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
+    TF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<MODE, SWAP>,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     done = true;
   }
 }
@@ -142,11 +159,14 @@ struct GemmPlan {
 };
 
 // Deterministic split count: a function of (features, K) only, never of the
-// batch, so decode results are batch-invariant.
+// batch, so decode results are batch-invariant. Splits form one cluster per
+// tile: up to 8 (portable) when there are many tiles, up to 16 (non-portable,
+// one cluster per GPC) when a few tiles must cover the machine.
 int pick_splits(int tiles, int k_blocks) {
   const int target = 128;
+  const int cap = tiles >= 16 ? 8 : 16;
   int best = 1;
-  for (int d = 1; d <= k_blocks && d <= 32; ++d) {
+  for (int d = 1; d <= k_blocks && d <= cap; ++d) {
     if (k_blocks % d) continue;
     best = d;
     if (tiles * d >= target) break;
@@ -173,13 +193,16 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
   }
   if (d.splits > 0) {
     TF_REQUIRE(p.k_blocks % d.splits == 0, TF_ERR_ARG, "splits must divide ceil(k/64)");
+    TF_REQUIRE(d.splits <= 16, TF_ERR_ARG, "splits (cluster size) must be <= 16");
     p.splits = d.splits;
   } else {
-    p.splits = p.swap ? pick_splits(p.tiles_a * p.tiles_b, p.k_blocks) : 1;
+    p.splits = (p.swap && d.epilogue != TF_EPI_LOGITS) ? pick_splits(p.tiles_a * p.tiles_b, p.k_blocks) : 1;
   }
+  TF_REQUIRE(p.splits == 1 || d.epilogue != TF_EPI_LOGITS, TF_ERR_ARG,
+             "argmax epilogue does not support split-K");
   const int kb_per = p.k_blocks / p.splits;
   const int stage_bytes = gemm_stage_bytes(p.bn);
-  int st = (int)((kMaxSmem - 2048) / stage_bytes);
+  int st = (int)((kMaxSmem - 4096) / stage_bytes);
   if (st > 8) st = 8;
   if (st > kb_per) st = kb_per;
   if (st < 1) st = 1;
@@ -192,8 +215,8 @@ void launch_gemm_t(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& 
                    const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
   ensure_gemm_attr<MODE, SWAP>();
   dim3 grid(p.tiles_a, p.tiles_b, p.splits);
-  launch(gemm_tc_kernel<MODE, SWAP>, grid, dim3(128), gemm_smem_bytes(p.bn, p.stages), st,
-         d.pdl != 0, ta, tb, args);
+  launch_cluster(gemm_tc_kernel<MODE, SWAP>, grid, dim3(128),
+                 gemm_smem_bytes(p.bn, p.stages, p.splits), st, d.pdl != 0, p.splits, ta, tb, args);
 }
 
 template <int MODE>
@@ -240,8 +263,6 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
   a.T = d.seq_len;
   a.qbase_dev = d.qbase_dev;
   a.keys = d.argmax_keys;
-  a.ws = d.workspace;
-  a.counters = d.counters;
   switch (d.epilogue) {
     case TF_EPI_BIAS:
     case TF_EPI_BIAS_GELU:
@@ -264,13 +285,6 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
       break;
     default:
       throw TfError{TF_ERR_ARG, "gemm: unknown epilogue"};
-  }
-  if (p.splits > 1) {
-    const size_t need = (size_t)p.tiles_a * p.tiles_b * p.splits * p.bn * kTileA * sizeof(float);
-    TF_REQUIRE(d.workspace && d.workspace_bytes >= need, TF_ERR_ARG,
-               "gemm: split-K workspace too small (" + std::to_string(need) + " bytes needed)");
-    TF_REQUIRE(d.counters && d.n_counters >= p.tiles_a * p.tiles_b, TF_ERR_ARG,
-               "gemm: split-K counters too small");
   }
   const void* P = p.swap ? d.wt : d.act;
   const void* Q = p.swap ? d.act : d.wt;
@@ -300,8 +314,23 @@ int vpl_for(int H) {
   return -1;
 }
 
+// 16-byte path needs H % 8 == 0 and 16-byte aligned row strides
+bool vec_ok(int H, int ld1, int ld2) { return H % 8 == 0 && ld1 % 8 == 0 && ld2 % 8 == 0; }
+
 void run_embed(const EmbedArgs& a, cudaStream_t st, bool pdl) {
   const dim3 grid((a.n_tok + 7) / 8);
+  if (vec_ok(a.H, a.ldw, a.ldx) && a.H <= 2048) {
+    const int nc = (a.H / 8 + 31) / 32;
+    switch (nc) {
+      case 1: launch(embed_ln_vec_kernel<1>, grid, dim3(256), 0, st, pdl, a); return;
+      case 2: launch(embed_ln_vec_kernel<2>, grid, dim3(256), 0, st, pdl, a); return;
+      case 3: launch(embed_ln_vec_kernel<3>, grid, dim3(256), 0, st, pdl, a); return;
+      case 4: launch(embed_ln_vec_kernel<4>, grid, dim3(256), 0, st, pdl, a); return;
+      case 6: launch(embed_ln_vec_kernel<6>, grid, dim3(256), 0, st, pdl, a); return;
+      case 8: launch(embed_ln_vec_kernel<8>, grid, dim3(256), 0, st, pdl, a); return;
+      default: break;
+    }
+  }
   switch (vpl_for(a.H)) {
     case 4: launch(embed_ln_kernel<4>, grid, dim3(256), 0, st, pdl, a); break;
     case 8: launch(embed_ln_kernel<8>, grid, dim3(256), 0, st, pdl, a); break;
@@ -316,6 +345,18 @@ void run_embed(const EmbedArgs& a, cudaStream_t st, bool pdl) {
 
 void run_ln(const LnArgs& a, cudaStream_t st, bool pdl) {
   const dim3 grid((a.n_rows + 7) / 8);
+  if (vec_ok(a.H, a.ldx, a.ldh) && a.H <= 2048) {
+    const int nc = (a.H / 8 + 31) / 32;
+    switch (nc) {
+      case 1: launch(layernorm_vec_kernel<1>, grid, dim3(256), 0, st, pdl, a); return;
+      case 2: launch(layernorm_vec_kernel<2>, grid, dim3(256), 0, st, pdl, a); return;
+      case 3: launch(layernorm_vec_kernel<3>, grid, dim3(256), 0, st, pdl, a); return;
+      case 4: launch(layernorm_vec_kernel<4>, grid, dim3(256), 0, st, pdl, a); return;
+      case 6: launch(layernorm_vec_kernel<6>, grid, dim3(256), 0, st, pdl, a); return;
+      case 8: launch(layernorm_vec_kernel<8>, grid, dim3(256), 0, st, pdl, a); return;
+      default: break;
+    }
+  }
   switch (vpl_for(a.H)) {
     case 4: launch(layernorm_kernel<4>, grid, dim3(256), 0, st, pdl, a); break;
     case 8: launch(layernorm_kernel<8>, grid, dim3(256), 0, st, pdl, a); break;
