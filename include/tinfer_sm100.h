@@ -155,6 +155,7 @@ typedef struct tf_session_desc {
   int* out_tokens;                       /* [batch, max_new] */
   const int* pads;                       /* [batch] left-pad offsets = first valid slot */
   const int* remap; int remap_n; int unk_id;  /* optional prompt-id remap */
+  int* beam_indir; int beam;             /* beam search: [batch, capacity] slot->beam table, width */
 } tf_session_desc;
 int tf_session_create(void* model, const tf_session_desc* d, void** session);
 int tf_session_destroy(void* session);
@@ -174,6 +175,25 @@ int tf_forward(void* session, const int* ids, const int* pos, int T, int mode, i
  * by the previous argmax; with use_graph the step is captured once into a CUDA
  * graph and replayed. */
 int tf_decode(void* session, int n_steps, int use_graph, void* stream);
+/* Beam search (no reference implementation; semantics in DESIGN.md §6):
+ * rows b = r*beam + k. After a forward that produced last-row logits, one step
+ * selects, per request, the top-`beam` (beam, token) candidates by
+ * score + log_softmax(f16 logits), ties to the lower flat index; finished beams
+ * propose only (eos, score). Updates scores/finished/tokens, records token and
+ * parent histories at step = len - prompt_len, and rewrites the cache
+ * indirection table (the KV cache itself is never reordered). */
+typedef struct tf_beam_desc {
+  int requests, beam, max_new, prompt_len, eos;
+  float* scores;              /* [requests*beam], init 0 for beam 0 and -inf otherwise */
+  unsigned char* finished;    /* [requests*beam] */
+  int* tokens;                /* [requests*beam] next fed ids */
+  int* tok_hist; int* par_hist; /* [max_new, requests*beam] */
+} tf_beam_desc;
+int tf_beam_select(void* session, const tf_beam_desc* d, void* stream);
+/* n steps of (T=1 forward of `tokens` -> last-row logits -> tf_beam_select),
+ * captured once into a CUDA graph when use_graph. */
+int tf_beam_decode(void* session, const tf_beam_desc* d, int n_steps, int use_graph, void* stream);
+
 /* Kernels launched by one decode step (for the bench's gpu_launches count). */
 int tf_session_launches_per_step(void* session);
 

@@ -473,3 +473,15 @@ def synthetic_prompts(vocab_size, batch, src_len, seed=42, label="prompts"):
     s = Stream(derive_seed(seed, label))
     ids = s.randint(batch * src_len, vocab_size - 3) + 3
     return [list(map(int, r)) for r in ids.reshape(batch, src_len)]
+
+
+def sequence_logprob(w, c: Config, prompt, gen):
+    """Sum of log_softmax(f16 logits) of ``gen`` given ``prompt`` (beam score of a
+    hypothesis, eos included), through the reference forward core."""
+    seq = list(prompt) + list(gen)
+    logits = forward_full(w, c, seq[:-1]) if gen else None
+    total = np.float32(0.0)
+    for t, tok in enumerate(gen):
+        lp = log_softmax_f32(logits[len(prompt) - 1 + t][None, :])[0]
+        total = np.float32(total + lp[tok])
+    return float(total)

@@ -89,6 +89,16 @@ class SessionDesc(C.Structure):
         ("keys", C.c_void_p), ("len_dev", C.c_void_p), ("step_dev", C.c_void_p),
         ("out_tokens", C.c_void_p), ("pads", C.c_void_p),
         ("remap", C.c_void_p), ("remap_n", C.c_int), ("unk_id", C.c_int),
+        ("beam_indir", C.c_void_p), ("beam", C.c_int),
+    ]
+
+
+class BeamDesc(C.Structure):
+    _fields_ = [
+        ("requests", C.c_int), ("beam", C.c_int), ("max_new", C.c_int), ("prompt_len", C.c_int),
+        ("eos", C.c_int),
+        ("scores", C.c_void_p), ("finished", C.c_void_p), ("tokens", C.c_void_p),
+        ("tok_hist", C.c_void_p), ("par_hist", C.c_void_p),
     ]
 
 
@@ -112,6 +122,8 @@ SIGNATURES = {
     "tf_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
                              C.c_void_p]),
     "tf_decode": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "tf_beam_select": (C.c_int, [C.c_void_p, C.POINTER(BeamDesc), C.c_void_p]),
+    "tf_beam_decode": (C.c_int, [C.c_void_p, C.POINTER(BeamDesc), C.c_int, C.c_int, C.c_void_p]),
     "tf_session_launches_per_step": (C.c_int, [C.c_void_p]),
 }
 

@@ -30,6 +30,9 @@ struct AttnArgs {
   float scale;
   __half* out;  // [B*T, ldo]
   int ldo;
+  // beam search: slot s of row b lives in row (b / beam) * beam + indir[b * cap + s]
+  const int* indir;
+  int beam;
 };
 
 // ------------------------------------------------------------------ decode
@@ -55,9 +58,17 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
     pdl_trigger();
     return;
   }
-  const size_t head_off = ((size_t)b * a.NH + h) * a.cap * D;
-  const __half* K = a.kc + head_off;
-  const __half* V = a.vc + head_off;
+  const size_t head_stride = (size_t)a.cap * D;        // one (row, head) block
+  const size_t row_stride = (size_t)a.NH * head_stride;  // one batch row
+  const int* ind = a.indir ? a.indir + (size_t)b * a.cap : nullptr;
+  const int beam0 = a.indir ? (b / a.beam) * a.beam : b;
+  // K/V row of slot s (through the beam indirection when present)
+  auto kv_off = [&](int s) -> size_t {
+    const int src = ind ? beam0 + ind[s] : b;
+    return (size_t)src * row_stride + (size_t)h * head_stride + (size_t)s * D;
+  };
+  const __half* K = a.kc;
+  const __half* V = a.vc;
 
   // ---- scores
   if ((D & 7) == 0 && D <= 256) {
@@ -68,7 +79,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
       const int j = base + sub;
       float acc = 0.0f;
       if (sub < kpw && j < n) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(K + (size_t)(lo + j) * D + gl * 8);
+        const uint4 raw = *reinterpret_cast<const uint4*>(K + kv_off(lo + j) + gl * 8);
         const __half2* kh = reinterpret_cast<const __half2*>(&raw);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -82,7 +93,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
     }
   } else {
     for (int j = tid; j < n; j += 128) {
-      const __half* kr = K + (size_t)(lo + j) * D;
+      const __half* kr = K + kv_off(lo + j);
       float acc = 0.0f;
       for (int d = 0; d < D; ++d) acc = __fadd_rn(acc, __fmul_rn(qs[d], __half2float(kr[d])));
       sc[j] = __fmul_rn(acc, a.scale);
@@ -119,15 +130,15 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
     if ((D & 1) == 0) {
       for (int j = g; j < n; j += groups) {
         const float w = __fmul_rn(sc[j], inv);
-        const float2 vf = __half22float2(*reinterpret_cast<const __half2*>(V + (size_t)(lo + j) * D + d0));
+        const float2 vf = __half22float2(*reinterpret_cast<const __half2*>(V + kv_off(lo + j) + d0));
         o0 = __fadd_rn(o0, __fmul_rn(w, vf.x));
         o1 = __fadd_rn(o1, __fmul_rn(w, vf.y));
       }
     } else {
       for (int j = g; j < n; j += groups) {
         const float w = __fmul_rn(sc[j], inv);
-        o0 = __fadd_rn(o0, __fmul_rn(w, __half2float(V[(size_t)(lo + j) * D + d0])));
-        if (d0 + 1 < D) o1 = __fadd_rn(o1, __fmul_rn(w, __half2float(V[(size_t)(lo + j) * D + d0 + 1])));
+        o0 = __fadd_rn(o0, __fmul_rn(w, __half2float(V[kv_off(lo + j) + d0])));
+        if (d0 + 1 < D) o1 = __fadd_rn(o1, __fmul_rn(w, __half2float(V[kv_off(lo + j) + d0 + 1])));
       }
     }
   }

@@ -1,0 +1,160 @@
+// Beam-search step on the device (north star (3): "fused with a per-row argmax
+// or top-k for greedy and beam search"). The reference has no beam search
+// (SPEC.md:14, 183); semantics follow oracle/tinfer_oracle.py::beam_search_decode:
+//
+//   lp      = (x - max) - log(sum exp(x - max))        over f16-rounded logits, f32
+//   cand    = score[beam] + lp[token]                  (f32)
+//   frozen  : a finished beam proposes only (eos, score)
+//   select  : top-K over the flat (beam, token) index, larger first, ties to the
+//             lower flat index
+//
+// One CTA per request. The KV cache is never reordered: each row keeps an
+// indirection table indir[b][slot] = which beam of the request wrote that slot
+// (FasterTransformer-style cache indirection); the decode attention reads K/V
+// through it. The selecting CTA rewrites its request's K rows of the table in
+// place (parents are always in the same request) via a shared-memory stage.
+#pragma once
+
+#include "common.cuh"
+
+namespace tf {
+
+constexpr int kMaxBeam = 8;
+
+struct BeamArgs {
+  int R, K, V, cap, max_new;
+  int eos;
+  const __half* logits;  // [R*K, ldl]
+  int ldl;
+  float* scores;         // [R*K]
+  unsigned char* finished;  // [R*K]
+  int* tokens;           // [R*K] next token fed to each beam row
+  int* tok_hist;         // [max_new, R*K]
+  int* par_hist;         // [max_new, R*K] parent beam (within request)
+  int* indir;            // [R*K, cap]
+  const int* len_dev;    // cache length = slot the fed token will occupy
+  int prompt_len;        // step index = *len_dev - prompt_len
+};
+
+struct Cand {
+  float v;
+  int i;  // flat index beam*V + token
+};
+__device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {
+  return a.v > b.v || (a.v == b.v && a.i < b.i);
+}
+
+// insert into a descending top-K list (K <= kMaxBeam)
+__device__ __forceinline__ void topk_insert(Cand (&t)[kMaxBeam], int K, Cand c) {
+  if (!cand_better(c, t[K - 1])) return;
+  int j = K - 1;
+  while (j > 0 && cand_better(c, t[j - 1])) {
+    t[j] = t[j - 1];
+    --j;
+  }
+  t[j] = c;
+}
+
+// blockDim = 256; dynamic smem = K * cap ints (indirection staging)
+__global__ void __launch_bounds__(256) beam_select_kernel(const BeamArgs a) {
+  pdl_wait();
+  __shared__ float s_max[kMaxBeam], s_lz[kMaxBeam], s_red[8];
+  __shared__ Cand s_cand[256];
+  __shared__ int s_parent[kMaxBeam], s_tok[kMaxBeam];
+  __shared__ float s_best[kMaxBeam];
+  __shared__ unsigned char s_pfin[kMaxBeam];
+  extern __shared__ int s_indir[];  // [K][cap]
+  const int r = blockIdx.x, K = a.K, V = a.V;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int step = *a.len_dev - a.prompt_len;
+  const int len = *a.len_dev;
+
+  // ---- per-beam max and log(sum exp(x - max)) over the f16 logits
+  for (int k = 0; k < K; ++k) {
+    const __half* row = a.logits + (size_t)(r * K + k) * a.ldl;
+    float m = -INFINITY;
+    for (int v = tid; v < V; v += 256) m = fmaxf(m, __half2float(row[v]));
+    m = warp_max(m);
+    if (lane == 0) s_red[warp] = m;
+    __syncthreads();
+    m = s_red[0];
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, s_red[w]);
+    __syncthreads();
+    float z = 0.0f;
+    for (int v = tid; v < V; v += 256) z += expf(__fsub_rn(__half2float(row[v]), m));
+    z = warp_sum(z);
+    if (lane == 0) s_red[warp] = z;
+    __syncthreads();
+    if (tid == 0) {
+      float t = 0.0f;
+      for (int w = 0; w < 8; ++w) t += s_red[w];
+      s_max[k] = m;
+      s_lz[k] = logf(t);
+    }
+    __syncthreads();
+  }
+  // ---- per-thread top-K over this request's K*V candidates
+  Cand top[kMaxBeam];
+#pragma unroll
+  for (int j = 0; j < kMaxBeam; ++j) top[j] = Cand{-INFINITY, 0x7fffffff};
+  for (int k = 0; k < K; ++k) {
+    const int b = r * K + k;
+    const float sc = a.scores[b];
+    if (a.finished[b]) {  // frozen: proposes only itself, with eos
+      if (tid == 0) topk_insert(top, K, Cand{sc, k * V + a.eos});
+      continue;
+    }
+    if (sc == -INFINITY) continue;
+    const float m = s_max[k], lz = s_lz[k];
+    const __half* row = a.logits + (size_t)b * a.ldl;
+    for (int v = tid; v < V; v += 256) {
+      const float lp = __fsub_rn(__fsub_rn(__half2float(row[v]), m), lz);
+      topk_insert(top, K, Cand{__fadd_rn(sc, lp), k * V + v});
+    }
+  }
+  // ---- block merge: K rounds of arg-best over the per-thread list heads
+  int head = 0;
+  for (int round = 0; round < K; ++round) {
+    const Cand mine = head < K ? top[head] : Cand{-INFINITY, 0x7fffffff};
+    s_cand[tid] = mine;
+    __syncthreads();
+    for (int stride = 128; stride > 0; stride >>= 1) {
+      if (tid < stride && cand_better(s_cand[tid + stride], s_cand[tid])) s_cand[tid] = s_cand[tid + stride];
+      __syncthreads();
+    }
+    const Cand best = s_cand[0];
+    if (head < K && mine.i == best.i && mine.v == best.v) ++head;  // owner pops its head
+    if (tid == 0) {
+      const int pb = best.i / V;
+      s_parent[round] = pb;
+      s_tok[round] = best.i - pb * V;
+      s_best[round] = best.v;
+    }
+    __syncthreads();
+  }
+  // ---- read everything the children inherit before any row is rewritten
+  if (tid < K) s_pfin[tid] = a.finished[r * K + s_parent[tid]];
+  for (int i = tid; i < K * len; i += 256) {
+    const int k = i / len, s = i - k * len;
+    s_indir[k * a.cap + s] = a.indir[(size_t)(r * K + k) * a.cap + s];
+  }
+  __syncthreads();
+  const int span = min(len + 1, a.cap);
+  for (int i = tid; i < K * span; i += 256) {
+    const int k = i / span, s = i - k * span;
+    a.indir[(size_t)(r * K + k) * a.cap + s] = (s < len) ? s_indir[s_parent[k] * a.cap + s] : k;
+  }
+  if (tid < K) {
+    const int b = r * K + tid, tok = s_tok[tid];
+    a.scores[b] = s_best[tid];
+    a.finished[b] = (s_pfin[tid] || tok == a.eos) ? 1 : 0;
+    a.tokens[b] = tok;
+    if (step < a.max_new) {
+      a.tok_hist[(size_t)step * (a.R * K) + b] = tok;
+      a.par_hist[(size_t)step * (a.R * K) + b] = s_parent[tid];
+    }
+  }
+  pdl_trigger();
+}
+
+}  // namespace tf

@@ -13,6 +13,7 @@
 
 #include "../../include/tinfer_sm100.h"
 #include "attention.cuh"
+#include "beam.cuh"
 #include "common.cuh"
 #include "gemm_tc.cuh"
 #include "norm_embed.cuh"
@@ -398,6 +399,8 @@ struct Session {
   Model* m;
   tf_session_desc d;
   cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t beam_graph = nullptr;
+  tf_beam_desc beam_key{};  // descriptor the beam graph was captured with
   int graph_launches = 0;
   int launches_last = 0;
 };
@@ -415,7 +418,7 @@ int* qbase_zero_ptr() {
 // One forward of T tokens per sequence through every layer. Returns the number
 // of kernels launched.
 int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pdl,
-            cudaStream_t st) {
+            cudaStream_t st, bool remap_ids = true) {
   const tf_model_desc& m = s.m->d;
   const tf_session_desc& sd = s.d;
   const int B = sd.batch, M = B * T;
@@ -436,7 +439,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
   e.P = m.max_pos;
   e.ids = ids;
   e.keys = sd.keys;
-  e.remap = ids ? sd.remap : nullptr;
+  e.remap = (ids && remap_ids) ? sd.remap : nullptr;
   e.remap_n = sd.remap_n;
   e.unk_id = sd.unk_id;
   e.pos = pos;
@@ -502,6 +505,10 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     at.scale = (float)(1.0 / std::sqrt((double)D));
     at.out = static_cast<__half*>(sd.attn);
     at.ldo = m.ldk_h;
+    if (T == 1 && sd.beam_indir) {
+      at.indir = sd.beam_indir;
+      at.beam = sd.beam;
+    }
     run_attention(at, st, pdl);
     ++launches;
     // output projection + residual (model.py:478-482)
@@ -617,6 +624,52 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
   }
   ++launches;
   return launches;
+}
+
+BeamArgs beam_args(const Session& s, const tf_beam_desc& d) {
+  TF_REQUIRE(d.beam >= 1 && d.beam <= kMaxBeam, TF_ERR_UNSUPPORTED, "beam width must be in [1, 8]");
+  TF_REQUIRE(d.requests * d.beam == s.d.batch, TF_ERR_SHAPE, "beam: requests*beam != session batch");
+  TF_REQUIRE(s.d.beam_indir && s.d.beam == d.beam, TF_ERR_ARG, "beam: session lacks the indirection table");
+  TF_REQUIRE(s.d.logits && d.scores && d.finished && d.tokens && d.tok_hist && d.par_hist, TF_ERR_ARG,
+             "beam: missing buffer");
+  BeamArgs a{};
+  a.R = d.requests;
+  a.K = d.beam;
+  a.V = s.m->d.vocab;
+  a.cap = s.d.capacity;
+  a.max_new = d.max_new;
+  a.eos = d.eos;
+  a.logits = static_cast<const __half*>(s.d.logits);
+  a.ldl = s.m->d.vocab;
+  a.scores = d.scores;
+  a.finished = d.finished;
+  a.tokens = d.tokens;
+  a.tok_hist = d.tok_hist;
+  a.par_hist = d.par_hist;
+  a.indir = s.d.beam_indir;
+  a.len_dev = s.d.len_dev;
+  a.prompt_len = d.prompt_len;
+  return a;
+}
+
+void run_beam_select(const Session& s, const tf_beam_desc& d, cudaStream_t st, bool pdl) {
+  const BeamArgs a = beam_args(s, d);
+  const size_t smem = (size_t)a.K * a.cap * sizeof(int);
+  static bool attr = false;
+  if (!attr) {
+    TF_CHECK_CUDA(cudaFuncSetAttribute(beam_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kMaxSmem - 8192));
+    attr = true;
+  }
+  TF_REQUIRE(smem <= kMaxSmem - 8192, TF_ERR_UNSUPPORTED, "beam: capacity too large");
+  launch(beam_select_kernel, dim3(a.R), dim3(256), smem, st, pdl, a);
+}
+
+// one beam step: feed `tokens` (generated ids, no remap), last-row logits, select
+int beam_step(Session& s, const tf_beam_desc& d, cudaStream_t st) {
+  int n = forward(s, d.tokens, nullptr, 1, TF_FWD_LOGITS_LAST, true, st, false);
+  run_beam_select(s, d, st, true);
+  return n + 1;
 }
 
 }  // namespace
@@ -748,6 +801,7 @@ int tf_session_destroy(void* session) {
   return guarded([&] {
     Session* s = static_cast<Session*>(session);
     if (s && s->graph) cudaGraphExecDestroy(s->graph);
+    if (s && s->beam_graph) cudaGraphExecDestroy(s->beam_graph);
     delete s;
   });
 }
@@ -794,6 +848,52 @@ int tf_decode(void* session, int n_steps, int use_graph, void* stream) {
       s.graph_launches = launches;
     }
     for (int i = 0; i < n_steps; ++i) TF_CHECK_CUDA(cudaGraphLaunch(s.graph, st));
+    s.launches_last = s.graph_launches;
+  });
+}
+
+int tf_beam_select(void* session, const tf_beam_desc* d, void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(session && d, TF_ERR_ARG, "beam_select: null argument");
+    run_beam_select(*static_cast<Session*>(session), *d, static_cast<cudaStream_t>(stream), false);
+  });
+}
+
+int tf_beam_decode(void* session, const tf_beam_desc* d, int n_steps, int use_graph, void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(session && d, TF_ERR_ARG, "beam_decode: null argument");
+    Session& s = *static_cast<Session*>(session);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n_steps <= 0) return;
+    if (!use_graph) {
+      for (int i = 0; i < n_steps; ++i) s.launches_last = beam_step(s, *d, st);
+      return;
+    }
+    if (s.beam_graph && std::memcmp(&s.beam_key, d, sizeof(*d)) != 0) {
+      cudaGraphExecDestroy(s.beam_graph);
+      s.beam_graph = nullptr;
+    }
+    if (!s.beam_graph) {
+      cudaStream_t cs;
+      TF_CHECK_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      cudaGraph_t g;
+      TF_CHECK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      int launches = 0;
+      try {
+        launches = beam_step(s, *d, cs);
+      } catch (...) {
+        cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        throw;
+      }
+      TF_CHECK_CUDA(cudaStreamEndCapture(cs, &g));
+      TF_CHECK_CUDA(cudaGraphInstantiate(&s.beam_graph, g, 0));
+      TF_CHECK_CUDA(cudaGraphDestroy(g));
+      TF_CHECK_CUDA(cudaStreamDestroy(cs));
+      s.beam_key = *d;
+      s.graph_launches = launches;
+    }
+    for (int i = 0; i < n_steps; ++i) TF_CHECK_CUDA(cudaGraphLaunch(s.beam_graph, st));
     s.launches_last = s.graph_launches;
   });
 }

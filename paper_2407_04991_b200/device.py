@@ -115,14 +115,14 @@ class DeviceModel:
         return n + self.lm_head_t.numel() * 2
 
     def session(self, batch: int, capacity: int, max_tokens: int, max_new: int,
-                logits: bool = False) -> "Session":
-        key = (batch, capacity, max_tokens, max_new, logits)
+                logits=False, beam: int = 0) -> "Session":
+        key = (batch, capacity, max_tokens, max_new, logits, beam)
         s = self._sessions.get(key)
         if s is None:
             if len(self._sessions) >= 8:  # bound the cache; drop the oldest
                 old = next(iter(self._sessions))
                 self._sessions.pop(old).close()
-            s = Session(self, batch, capacity, max_tokens, max_new, logits)
+            s = Session(self, batch, capacity, max_tokens, max_new, logits, beam=beam)
             self._sessions[key] = s
         return s
 
@@ -145,8 +145,10 @@ class Session:
     """One batch shape: KV cache, activations, device step state, native handle."""
 
     def __init__(self, dm: DeviceModel, batch: int, capacity: int, max_tokens: int, max_new: int,
-                 logits: bool, k_cache: torch.Tensor | None = None,
-                 v_cache: torch.Tensor | None = None):
+                 logits, k_cache: torch.Tensor | None = None,
+                 v_cache: torch.Tensor | None = None, beam: int = 0):
+        """``logits``: False (argmax only), "last" ([batch, V] buffer) or True/"all"
+        ([batch*max_tokens, V]); ``beam`` > 0 adds the beam-search state."""
         dev = dm.device
         self.dm, self.batch, self.capacity = dm, batch, capacity
         self.max_tokens, self.max_new = max_tokens, max(1, max_new)
@@ -158,7 +160,8 @@ class Session:
         self.x, self.h = z16(rows, dm.ldk_h), z16(rows, dm.ldk_h)
         self.q, self.attn = z16(rows, dm.ldk_h), z16(rows, dm.ldk_h)
         self.ffn = z16(rows, dm.ldk_f)
-        self.logits = z16(rows, dm.V) if logits else None
+        logit_rows = batch if logits == "last" else rows
+        self.logits = z16(logit_rows, dm.V) if logits else None
         self.keys = torch.zeros(batch, dtype=torch.int64, device=dev)
         # int32 state: [len, step] + pads[B] + ids[rows] + pos[rows]
         self.state = torch.zeros(2 + batch + 2 * rows, dtype=torch.int32, device=dev)
@@ -170,6 +173,14 @@ class Session:
         self.host_in = torch.zeros(self.state.numel(), dtype=torch.int32).pin_memory()
         self.host_out = torch.zeros((batch, self.max_new), dtype=torch.int32).pin_memory()
         self.remap = None
+        self.beam = beam
+        if beam:
+            self.indir = torch.zeros((batch, capacity), dtype=torch.int32, device=dev)
+            self.scores = torch.zeros(batch, dtype=torch.float32, device=dev)
+            self.finished = torch.zeros(batch, dtype=torch.uint8, device=dev)
+            self.beam_tokens = torch.zeros(batch, dtype=torch.int32, device=dev)
+            self.tok_hist = torch.zeros((self.max_new, batch), dtype=torch.int32, device=dev)
+            self.par_hist = torch.zeros((self.max_new, batch), dtype=torch.int32, device=dev)
         d = N.SessionDesc()
         d.batch, d.capacity, d.max_tokens, d.max_new = batch, capacity, max_tokens, self.max_new
         d.k_cache, d.v_cache = self.k_cache.data_ptr(), self.v_cache.data_ptr()
@@ -183,6 +194,8 @@ class Session:
         d.out_tokens = self.out_tokens.data_ptr()
         d.pads = self.pads.data_ptr()
         d.remap, d.remap_n, d.unk_id = None, 0, 0
+        if beam:
+            d.beam_indir, d.beam = self.indir.data_ptr(), beam
         self.desc = d
         h = C.c_void_p()
         N.check(N.lib().tf_session_create(dm.handle, C.byref(d), C.byref(h)), "tf_session_create")

@@ -54,7 +54,8 @@ def test_library_exports_every_declared_symbol():
 @pytest.mark.parametrize("cname,pyname", [("tf_gemm_desc", "GemmDesc"), ("tf_embed_desc", "EmbedDesc"),
                                           ("tf_layer_weights", "LayerWeights"),
                                           ("tf_model_desc", "ModelDesc"),
-                                          ("tf_session_desc", "SessionDesc")])
+                                          ("tf_session_desc", "SessionDesc"),
+                                          ("tf_beam_desc", "BeamDesc")])
 def test_ctypes_structs_mirror_header(cname, pyname):
     from paper_2407_04991_b200 import _native as N
     py = [f[0] for f in getattr(N, pyname)._fields_]
