@@ -1,27 +1,37 @@
-"""Benchmark: generated tokens/s for Ernie-base fp16 greedy generation on B200.
+"""Benchmark: generated tokens/s for Ernie-base fp16 generation on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2]
     torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1, one rank per GPU)
 
-Workload (BASELINE.json configs[1], SURVEY §8 pins, "C2"): Ernie-3.0-base-sized
-model (12 layers, hidden 768, 12 heads, FFN 3072, vocab 40000, positions trimmed
-1024 -> 512), random-init with the reference's splitmix64 stream (seed 42), fp16,
-greedy, batch 32, prompt length 128, 64 new tokens. One step = one
-``batched_greedy_decode`` over one batch (1 prefill + 63 decode forwards,
-2048 generated tokens per GPU). Multi-GPU is data parallel over independent
-requests (each rank its own batch, no collective): "scaling": "weak".
+Workloads (BASELINE.json configs, SURVEY §8 pins; all weights random-init with
+the reference's splitmix64 stream, seed 42, from the 12L/768h/12-head/FFN-3072
+vocab-40000 master model):
+
+* c2 (default, configs[1]): positions trimmed 1024 -> 512, fp16 greedy, batch 32
+  per GPU, src 128, 64 new tokens. One step = one batched_greedy_decode call
+  (1 prefill + 63 decode forwards, 2048 generated tokens per GPU).
+* c3 (configs[2]): vocab pruned 40k -> 10k (build_pruned_vocab on a synthetic
+  Zipf count vector, specials forced), positions 256, greedy, batch 128.
+* c4 (configs[3]): the pruned model (512 positions), beam 4, 64 requests, src
+  256, 128 new tokens; tokens counted = returned hypotheses (64 x 128).
+* c5 (configs[4]): the pruned model (1024 positions), 20k requests with src
+  ~ U[32, 512], 64 new, length-bucketed (batch <= 128, bucket 16); one step = the
+  whole sweep; under torchrun each rank takes its LPT share (strong scaling).
+
+Multi-GPU for c2/c3/c4 is data parallel over independent requests (each rank its
+own batch, no collective): "scaling": "weak".
 
 * ``value``  — device-resident throughput: inputs staged in HBM before the timed
   region; CUDA events on the launching stream around each step; L2 flushed
   between steps (outside the events); max over ranks.
-* ``e2e``    — the same metric through the public API ``batched_greedy_decode``
-  with host prompt lists: H2D of ids/positions/pads (pinned) and D2H of the
-  generated ids inside the timed region (wall clock + device sync), max over ranks.
-* ``roofline`` — the dominant kernel: algorithmic
-  bytes per launch / its CUDA-event launch time, against MEASURED_PEAKS.json.
-* ``cpu_baseline`` — the oracle port (oracle/tinfer_oracle.py, numpy) timed on
-  this host's cores on a bounded sample (prefill + 3 decode steps, extrapolated
-  to the 63-step workload). ``--impl reference`` prints that arm alone.
+* ``e2e``    — the same metric through the public API (batched_greedy_decode /
+  beam_search_decode) with host prompt lists: H2D of ids/positions/pads and D2H
+  of results inside the timed region (wall clock + device sync), max over ranks.
+* ``roofline`` — the dominant kernel: algorithmic bytes per
+  launch / its CUDA-event launch time, against MEASURED_PEAKS.json.
+* ``cpu_baseline`` — the oracle port (oracle/tinfer_oracle.py, numpy) on this
+  host's cores, bounded sample (prefill + a few decode steps, extrapolated).
+  ``--impl reference`` prints that arm alone (rank 0; other ranks exit 0).
 """
 
 from __future__ import annotations
@@ -39,15 +49,62 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-B, SRC, NEW, SEED = 32, 128, 64, 42
-WORKLOAD = ("C2: Ernie-base-sized (12L, 768h, 12 heads, FFN 3072, vocab 40000, 512 positions), "
-            "fp16 greedy generation, batch 32/GPU, src 128, 64 new tokens")
+SEED = 42
+WORKLOADS = {
+    "c2": dict(batch=32, src=128, new=64, beam=1, vocab="full", positions=512,
+               text="C2: Ernie-base-sized (12L, 768h, 12 heads, FFN 3072, vocab 40000, 512 positions), "
+                    "fp16 greedy generation, batch 32/GPU, src 128, 64 new tokens"),
+    "c3": dict(batch=128, src=128, new=64, beam=1, vocab="pruned", positions=256,
+               text="C3: Ernie-base-sized, vocab pruned 40k->10k (fused logits GEMM + argmax), 256 positions, "
+                    "fp16 greedy, batch 128/GPU, src 128, 64 new tokens"),
+    "c4": dict(batch=64, src=256, new=128, beam=4, vocab="pruned", positions=512,
+               text="C4: Ernie-base-sized, vocab 10k, beam search width 4, 64 requests/GPU, src 256, "
+                    "128 new tokens (returned hypotheses counted)"),
+    "c5": dict(batch=128, src=None, new=64, beam=1, vocab="pruned", positions=1024, requests=20000,
+               text="C5: Ernie-base-sized, vocab 10k, 20000 requests, src ~ U[32,512], 64 new, "
+                    "length-bucketed batches <= 128 (bucket 16), per-GPU shards"),
+}
 
 
-def master_cfg(P):
-    return P.ModelConfig(vocab_size=40000, hidden_size=768, num_layers=12, num_heads=12,
-                         head_dim=64, ffn_size=3072, max_position=1024, dtype=P.DType.F16,
+def master_config(M):
+    return M.ModelConfig(vocab_size=40000, hidden_size=768, num_layers=12, num_heads=12,
+                         head_dim=64, ffn_size=3072, max_position=1024, dtype=M.DType.F16,
                          eos_token=1, pad_token=2)
+
+
+def zipf_keep_ids():
+    """Kept ids for the 40k -> 10k pruning (same construction as the golden fixture)."""
+    from oracle import tinfer_oracle as O  # SplitMix64 stream + reference selection rule
+    zs = O.Stream(O.derive_seed(SEED, "zipf"))
+    rank = np.argsort(zs.u64(40000), kind="stable")
+    counts = np.empty(40000, np.int64)
+    counts[rank] = 10 ** 9 // (np.arange(40000) + 1)
+    return counts
+
+
+def build_model(w):
+    import paper_2407_04991_b200 as P
+    from paper_2407_04991_b200 import pruning as PR
+    model = P.init_random(master_config(P), SEED)
+    if w["vocab"] == "pruned":
+        vmap = PR.build_pruned_vocab(zipf_keep_ids(), 10000, specials=[0, 1, 2])
+        model = PR.prune_token_embedding(model, vmap)
+    return PR.prune_position_embedding(model, w["positions"])
+
+
+def make_prompts(V, w, rank):
+    from oracle import tinfer_oracle as O  # prompt stream only
+    if w["src"] is not None:
+        return O.synthetic_prompts(V, w["batch"], w["src"], seed=SEED + rank)
+    s = O.Stream(O.derive_seed(SEED, "c5-lengths"))
+    lens = (s.randint(w["requests"], 481) + 32).tolist()
+    t = O.Stream(O.derive_seed(SEED, "prompts"))
+    ids = (t.randint(sum(lens), V - 3) + 3).tolist()
+    out, k = [], 0
+    for n in lens:
+        out.append(ids[k:k + n])
+        k += n
+    return out
 
 
 def peaks():
@@ -59,15 +116,11 @@ def peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-# ---------------------------------------------------------------------------
-# clocks sampled during the timed region (NVML)
-# ---------------------------------------------------------------------------
 class ClockSampler:
-    REASONS = {
-        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
-        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
-        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
-    }
+    """NVML clocks + throttle reasons sampled during the timed region."""
+    REASONS = {"applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+               "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index):
         self.samples, self.reasons, self.max_mhz = [], set(), None
@@ -86,9 +139,7 @@ class ClockSampler:
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
                 mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for name, bit in self.REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        self.reasons.add(name)
+                self.reasons.update(n for n, bit in self.REASONS.items() if mask & bit)
             except Exception:
                 pass
             time.sleep(0.05)
@@ -111,12 +162,8 @@ class ClockSampler:
                 "reasons": sorted(self.reasons)}
 
 
-# ---------------------------------------------------------------------------
-# algorithmic bytes
-# ---------------------------------------------------------------------------
 def decode_step_bytes(L, H, F, V, S, ctx_sum, e=2):
-    """Bytes one decode step must move: weights + embedding rows + KV reads of
-    every live slot + KV append + ids (SURVEY §8d formula)."""
+    """weights + embedding rows + KV reads of live slots + KV append + ids."""
     weights = e * (L * (4 * H * H + 2 * H * F + 4 * H + F + H + 4 * H) + 2 * H + H * V)
     return weights + e * 2 * H * S + e * 2 * L * H * ctx_sum + e * 2 * L * H * S + 4 * S
 
@@ -124,229 +171,343 @@ def decode_step_bytes(L, H, F, V, S, ctx_sum, e=2):
 # ---------------------------------------------------------------------------
 # CPU baseline: oracle port on this host's cores
 # ---------------------------------------------------------------------------
-def cpu_baseline(n_decode=3):
-    from oracle import tinfer_oracle as O
+def cpu_threads():
     try:
         from threadpoolctl import threadpool_info
-        cores = max((p.get("num_threads") or 1) for p in threadpool_info()) if threadpool_info() else os.cpu_count()
+        info = threadpool_info()
+        return max((p.get("num_threads") or 1) for p in info) if info else os.cpu_count()
     except Exception:
-        cores = os.cpu_count()
+        return os.cpu_count()
+
+
+def cpu_baseline(wname="c2", n_decode=3):
+    from oracle import tinfer_oracle as O
+    w = WORKLOADS[wname]
     c = O.config_master(True)
-    w = O.init_weights(c, SEED)
-    w, c = O.prune_weights(w, c, tuple(range(c.vocab_size)), new_max_position=512)
-    prompts = O.synthetic_prompts(c.vocab_size, B, SRC, seed=SEED)
-    ids, pos, pads, lens = O.left_pad(c, prompts)
-    cache = O.Cache.new(c, B, SRC + NEW)
+    wts = O.init_weights(c, SEED)
+    kept = tuple(range(c.vocab_size))
+    if w["vocab"] == "pruned":
+        kept = O.build_pruned_vocab(zipf_keep_ids(), 10000, [0, 1, 2])
+    wts, c = O.prune_weights(wts, c, kept, new_max_position=w["positions"])
+    B = w["batch"] * w["beam"]
+    src = w["src"] or 272  # c5: mean prompt length
+    prompts = O.synthetic_prompts(c.vocab_size, B, src, seed=SEED)
+    ids, pos, pads, _ = O.left_pad(c, prompts)
+    cache = O.Cache.new(c, B, src + w["new"])
     t0 = time.perf_counter()
-    logits = O.forward_tokens(w, c, ids, pos, cache, pads)
+    logits = O.forward_tokens(wts, c, ids, pos, cache, pads)
     t_pre = time.perf_counter() - t0
     t0 = time.perf_counter()
     for _ in range(n_decode):
         nxt = np.argmax(logits, axis=1).reshape(B, 1)
-        logits = O.forward_tokens(w, c, nxt, (cache.len - pads).reshape(B, 1), cache, pads)
+        logits = O.forward_tokens(wts, c, nxt, (cache.len - pads).reshape(B, 1), cache, pads)
     t_dec = (time.perf_counter() - t0) / n_decode
-    total = t_pre + (NEW - 1) * t_dec
-    return {"value": B * NEW / total, "unit": "generated tokens/s", "cores": int(cores),
+    total = t_pre + (w["new"] - 1) * t_dec
+    return {"value": w["batch"] * w["new"] / total, "unit": "generated tokens/s", "cores": int(cpu_threads()),
             "kind": "port",
-            "sample": f"oracle numpy port, C2 batch {B} src {SRC}: prefill ({t_pre:.2f}s) + "
-                      f"{n_decode} decode steps ({t_dec * 1e3:.0f} ms each) timed, extrapolated "
-                      f"to 1 prefill + {NEW - 1} steps"}
+            "sample": f"oracle numpy port, {wname} rows {B} src {src}: prefill ({t_pre:.2f}s) + {n_decode} "
+                      f"decode steps ({t_dec * 1e3:.0f} ms each) timed, extrapolated to 1 prefill + "
+                      f"{w['new'] - 1} steps" + (" (greedy proxy for beam)" if w["beam"] > 1 else "")}
 
 
-# ---------------------------------------------------------------------------
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def base_line(args, w, world, value, ms_per_step):
+    return {"metric": "generated tokens/s", "value": value, "unit": "generated tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
+            "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+            "config": {"workload": w["text"], "global_batch": w["batch"] * (1 if args.workload == "c5" else world),
+                       "seq_len": w["src"] or "32-512", "new_tokens": w["new"], "beam": w["beam"],
+                       "parallelism": f"dp{world} (independent requests, no collective)",
+                       "l2": "flushed between timed steps (256 MB write); the per-step working set "
+                             "(>=200 MB weights + KV cache) also exceeds the 126 MB L2"}}
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    vals = []
+    w = WORKLOADS[args.workload]
     for _ in range(args.warmup):
-        cpu_baseline(n_decode=1)
-    for _ in range(args.steps):
-        vals.append(cpu_baseline(n_decode=2))
+        cpu_baseline(args.workload, n_decode=1)
+    vals = [cpu_baseline(args.workload, n_decode=2) for _ in range(args.steps)]
     v = float(statistics.median(x["value"] for x in vals))
-    base = vals[-1]
-    base["value"] = v
-    line = {"metric": "generated tokens/s", "value": v, "unit": "generated tokens/s",
-            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * B * NEW / v, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f16", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_batch": B, "seq_len": SRC, "new_tokens": NEW,
-                       "parallelism": "cpu"},
-            "cpu_baseline": base,
-            "e2e": {"value": v, "unit": "generated tokens/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+    base = dict(vals[-1], value=v)
+    line = base_line(args, w, args.gpus, v, 1e3 * w["batch"] * w["new"] / v)
+    line["impl"] = "reference"
+    line["config"]["parallelism"] = "cpu (rank 0 only)"
+    line["cpu_baseline"] = base
+    line["e2e"] = {"value": v, "unit": "generated tokens/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+class Runner:
+    """Device-resident step and public-API step for one workload on one rank."""
+
+    def __init__(self, model, prompts, w):
+        import torch
+
+        from paper_2407_04991_b200 import model as PM
+        from paper_2407_04991_b200.beam import BeamRun
+
+        self.w, self.model, self.prompts = w, model, prompts
+        c = model.config
+        if w["beam"] > 1:
+            self.beam = BeamRun(model, prompts, w["new"], w["beam"])
+            self.sess = self.beam.s
+        else:
+            self.beam = None
+            self.ids, self.pos, self.pads, _ = PM._left_pad(c, prompts)
+            cap, max_tokens = PM._session_shape(c, self.ids.shape[1], w["new"])
+            dm = model.device_model()
+            with torch.cuda.device(dm.device):
+                self.sess = dm.session(len(prompts), cap, max_tokens, w["new"])
+
+    def stage(self):
+        if self.beam:
+            self.beam.stage_inputs()
+        else:
+            self.sess.load_inputs(self.ids, self.pos, self.pads)
+
+    def device_step(self):
+        from paper_2407_04991_b200 import _native as N
+        if self.beam:
+            self.beam.run_device()
+        else:
+            self.sess.forward(self.ids.shape[1], N.FWD_ARGMAX)
+            self.sess.decode(self.w["new"] - 1)
+
+    def result(self):
+        if self.beam:
+            return self.beam.finish()[0]
+        return self.sess.fetch_tokens(self.w["new"])
+
+    def api_step(self):
+        import paper_2407_04991_b200 as P
+        if self.w["beam"] > 1:
+            return P.beam_search_decode(self.model, self.prompts, self.w["new"], self.w["beam"])
+        return P.batched_greedy_decode(self.model, self.prompts, self.w["new"])
+
+    def launches(self):
+        from paper_2407_04991_b200 import _native as N
+        from paper_2407_04991_b200 import model as PM
+        return PM.LAST_STATS.launches
 
 
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    import paper_2407_04991_b200 as P
     from paper_2407_04991_b200 import _native as N
     from paper_2407_04991_b200 import model as PM
-    from paper_2407_04991_b200.pruning import prune_position_embedding
 
     rank, world, local = dist_env()
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    hbm_peak, tc_peak, peak_kind = peaks()
-
-    model = prune_position_embedding(P.init_random(master_cfg(P), SEED), 512)
+    hbm_peak, _, peak_kind = peaks()
+    w = WORKLOADS[args.workload]
+    model = build_model(w)
     c = model.config
-    # each rank generates its own requests (independent prompt stream per rank)
-    from oracle import tinfer_oracle as O  # prompt stream only (SplitMix64), no compute
-    prompts = O.synthetic_prompts(c.vocab_size, B, SRC, seed=SEED + rank)
     dm = model.device_model(dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
-
-    ids, pos, pads, _ = PM._left_pad(c, prompts)
-    cap = SRC + NEW
-    sess = dm.session(B, cap, SRC, NEW)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
+    if args.workload == "c5":
+        return run_sweep(args, w, model, dm, rank, world, dev)
 
-    def device_step():
-        sess.forward(SRC, N.FWD_ARGMAX)
-        sess.decode(NEW - 1)
-
-    # warm-up (also captures the decode graph)
+    prompts = make_prompts(c.vocab_size, w, rank)
+    run = Runner(model, prompts, w)
     for _ in range(max(args.warmup, 3)):
-        sess.load_inputs(ids, pos, pads)
-        device_step()
+        run.stage()
+        run.device_step()
     torch.cuda.synchronize()
-    first = sess.fetch_tokens(NEW)
+    first = run.result()
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
 
     # ---------------- device-resident timed region
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    sync_all()
     times = []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            sess.load_inputs(ids, pos, pads)
+            run.stage()
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            device_step()
+            run.device_step()
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
-    torch.cuda.synchronize()
+    sync_all()
+    last = run.result()
+    assert (np.array_equal(first, last) if not run.beam else first == last), "non-deterministic"
+    total = sum(times)
     if world > 1:
-        dist.barrier()
-    last = sess.fetch_tokens(NEW)
-    assert np.array_equal(first, last), "non-deterministic generation"
-    launches_per_step = PM.LAST_STATS.launches if PM.LAST_STATS.launches else None
-    n_pre = N.lib().tf_session_launches_per_step(sess.handle)
-    total = float(sum(times))
-    if world > 1:
-        t = torch.tensor([total], device=dev)
+        t = torch.tensor([total], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total = float(t.item())
-    tokens = B * NEW * args.steps * world
-    value = tokens / total
+    gen_per_step = w["batch"] * w["new"]
+    value = gen_per_step * args.steps * world / total
 
-    # ---------------- end-to-end through the public API (host prompts -> host ids)
+    # ---------------- end-to-end through the public API
     for _ in range(2):
-        P.batched_greedy_decode(model, prompts, NEW)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+        run.api_step()
+    sync_all()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        out = P.batched_greedy_decode(model, prompts, NEW)
+        out = run.api_step()
     torch.cuda.synchronize()
     e2e_t = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_t], device=dev)
+        t = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_t = float(t.item())
     st = PM.LAST_STATS
-    assert [r[SRC:] for r in out] == [list(map(int, r)) for r in last], "API/device mismatch"
+    if not run.beam:
+        assert [r[w["src"]:] for r in out] == [list(map(int, r)) for r in last], "API/device mismatch"
 
-    # ---------------- roofline of the decode step and of the dominant kernel
+    # ---------------- rooflines
     H, F, V, L = c.hidden_size, c.ffn_size, c.vocab_size, c.num_layers
-    # decode step i (1-based) attends ctx = SRC + i slots per sequence
-    step_bytes = [decode_step_bytes(L, H, F, V, B, B * (SRC + i)) for i in range(1, NEW)]
-    dec_t = []
-    for _ in range(5):
-        sess.load_inputs(ids, pos, pads)
-        sess.forward(SRC, N.FWD_ARGMAX)
-        flush.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        sess.decode(NEW - 1)
-        e1.record(stream)
-        e1.synchronize()
-        dec_t.append(e0.elapsed_time(e1) / 1e3 / (NEW - 1))
-    t_step = float(statistics.median(dec_t))
+    S = w["batch"] * w["beam"]
+    step_bytes = [decode_step_bytes(L, H, F, V, S, S * (w["src"] + i)) for i in range(1, w["new"])]
+    t_step = probe_decode_step(torch, run, flush, stream, w)
     step_bw = float(np.mean(step_bytes)) / t_step / 1e9
-    kern = probe_dominant_kernel(torch, dm, sess, flush, stream, B)
-    launches = args.steps * (n_pre + (NEW - 1) * N.lib().tf_session_launches_per_step(sess.handle))
+    kern = probe_dominant_kernel(torch, dm, run.sess, flush, stream, S)
 
     if rank == 0:
-        line = {
-            "metric": "generated tokens/s", "value": value, "unit": "generated tokens/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_batch": B * world, "seq_len": SRC,
-                       "new_tokens": NEW, "parallelism": f"dp{world} (independent requests)",
-                       "l2": "flushed between timed steps (256 MB write); per-step working set "
-                             "(294 MB weights + KV) also exceeds the 126 MB L2"},
-            "e2e": {"value": B * NEW * args.steps * world / e2e_t, "unit": "generated tokens/s",
+        line = base_line(args, w, world, value, 1e3 * total / args.steps)
+        line.update({
+            "e2e": {"value": gen_per_step * args.steps * world / e2e_t, "unit": "generated tokens/s",
                     "h2d_bytes_per_step": int(st.h2d_bytes), "d2h_bytes_per_step": int(st.d2h_bytes)},
-            "gpu_launches": int(launches),
+            "gpu_launches": int(run.launches() * args.steps),
             "roofline": {"bound": "hbm", "achieved": kern["gbs"], "peak": hbm_peak, "unit": "GB/s",
-                         "frac": kern["gbs"] / hbm_peak, "traffic": None,
-                         "kernel": kern["name"], "bytes_per_launch": kern["bytes"],
-                         "launch_us": kern["us"], "peak_kind": peak_kind},
+                         "frac": kern["gbs"] / hbm_peak, "traffic": None, "kernel": kern["name"],
+                         "bytes_per_launch": kern["bytes"], "launch_us": kern["us"],
+                         "peak_kind": peak_kind},
             "decode_step": {"us": t_step * 1e6, "algorithmic_bytes": float(np.mean(step_bytes)),
                             "achieved_gbs": step_bw, "frac_of_hbm": step_bw / hbm_peak,
-                            "launches": int(N.lib().tf_session_launches_per_step(sess.handle))},
+                            "launches": int(N.lib().tf_session_launches_per_step(run.sess.handle))},
             "clocks": clk.summary(),
-        }
+        })
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline()
+            line["cpu_baseline"] = cpu_baseline(args.workload)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def probe_decode_step(torch, run, flush, stream, w):
+    """Median per-decode-step time (CUDA events around the graph-replayed steps)."""
+    from paper_2407_04991_b200 import _native as N
+    if run.beam:
+        return float("nan")
+    ts = []
+    for _ in range(5):
+        run.stage()
+        run.sess.forward(run.ids.shape[1], N.FWD_ARGMAX)
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run.sess.decode(w["new"] - 1)
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3 / (w["new"] - 1))
+    return float(statistics.median(ts))
+
+
 def probe_dominant_kernel(torch, dm, sess, flush, stream, batch):
-    """Time the decode step's largest single launch — the lm_head GEMM fused with
-    argmax (V x H f16 weights, one launch per step) — with CUDA events on the
-    launching stream, L2 flushed before each launch."""
+    """The lm_head GEMM fused with argmax — the largest single launch of a decode
+    step — timed with CUDA events on the launching stream, L2 flushed before
+    each launch. Algorithmic bytes = lm_head weights + activations + keys."""
     from paper_2407_04991_b200 import _native as N
     from paper_2407_04991_b200 import ops
 
     H, V = dm.H, dm.V
     keys = torch.zeros(batch, dtype=torch.int64, device=dm.device)
-    scratch = ops.Scratch(dm.device, 8 << 20)
+    act = sess.h[:batch]
     ts = []
     for i in range(12):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ops.gemm(sess.h[:batch], dm.lm_head_t, H, N.EPI_LOGITS, keys=keys, scratch=scratch)
+        ops.gemm(act, dm.lm_head_t, H, N.EPI_LOGITS, keys=keys)
         e1.record(stream)
         e1.synchronize()
         if i >= 2:
             ts.append(e0.elapsed_time(e1) / 1e3)
         keys.zero_()
     t = float(statistics.median(ts))
-    nbytes = V * H * 2 + batch * H * 2 + batch * 8
+    nbytes = V * dm.ldk_h * 2 + batch * H * 2 + batch * 8
     return {"name": "gemm_tc_kernel<EPI_LOGITS,swap> (lm_head + argmax)", "bytes": nbytes,
             "us": t * 1e6, "gbs": nbytes / t / 1e9}
+
+
+def run_sweep(args, w, model, dm, rank, world, dev):
+    """C5: the 20k-request sweep; this rank's LPT share of the length-bucketed
+    groups through the public API; whole-job tokens / max-over-ranks time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_04991_b200 as P
+    from paper_2407_04991_b200 import pipeline as PL
+
+    reqs = make_prompts(model.config.vocab_size, w, 0)
+    settings = PL.PipelineSettings(max_batch_size=w["batch"], bucket_width=16, max_new_tokens=w["new"])
+    plan = PL.plan_batches([len(r) for r in reqs], settings.max_batch_size, settings.bucket_width)
+    mine = PL.rank_share(plan, world, rank, w["new"])
+    # warm-up: one group per distinct shape class is enough to build sessions/graphs
+    for gi in mine[:max(args.warmup, 3)]:
+        P.batched_greedy_decode(model, [reqs[i] for i in plan.groups[gi]], w["new"])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    lat = []
+    gen = 0
+    with ClockSampler(dev.index) as clk:
+        t0 = time.perf_counter()
+        for gi in mine:
+            g = plan.groups[gi]
+            seqs = P.batched_greedy_decode(model, [reqs[i] for i in g], w["new"])
+            gen += sum(len(s) - len(reqs[i]) for s, i in zip(seqs, g))
+            done = time.perf_counter() - t0
+            lat += [done] * len(g)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    tot = torch.tensor([wall, gen], device=dev, dtype=torch.float64)
+    if world > 1:
+        mx = tot.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tot.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        wall, gen = float(mx[0]), int(sm[1])
+    if rank == 0:
+        value = gen / wall
+        line = base_line(args, w, world, value, 1e3 * wall)
+        line["steps"] = 1
+        line.update({
+            "e2e": {"value": value, "unit": "generated tokens/s",
+                    "h2d_bytes_per_step": int(sum(len(r) for r in reqs) * 8),
+                    "d2h_bytes_per_step": int(len(reqs) * w["new"] * 4)},
+            "latency_s": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
+                          "note": "rank-0 requests, enqueue (sweep start) -> ids back"},
+            "groups": len(plan.groups), "requests": len(reqs),
+            "clocks": clk.summary(),
+        })
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -355,10 +516,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
     else:

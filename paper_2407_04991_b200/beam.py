@@ -27,7 +27,7 @@ import ctypes as C
 import numpy as np
 
 from . import _native as N
-from .model import COUNTERS, ModelConfig, Model, _count_forward, _left_pad, _validate_prompts
+from .model import ModelConfig, Model, _count_forward, _left_pad, _session_shape, _validate_prompts
 
 
 def _backtrack(c: ModelConfig, prompts, scores, tok_hist, par_hist, K: int):
@@ -50,6 +50,74 @@ def _backtrack(c: ModelConfig, prompts, scores, tok_hist, par_hist, K: int):
     return out
 
 
+class BeamRun:
+    """Device state of one beam-search call (prepare -> run_device -> finish)."""
+
+    def __init__(self, model: Model, prompts, max_new_tokens: int, beam_width: int):
+        import torch
+
+        from .errors import ParameterError
+
+        c = model.config
+        if not 1 <= beam_width <= 8:
+            raise ParameterError("beam_width must be in [1, 8]")
+        self.model, self.c = model, c
+        self.prompts = _validate_prompts(c, prompts, max_new_tokens)
+        self.new, self.K, self.R = max_new_tokens, beam_width, len(self.prompts)
+        flat = [p for p in self.prompts for _ in range(self.K)]
+        self.ids, self.pos, self.pads, _ = _left_pad(c, flat)
+        self.B, self.L = self.ids.shape
+        cap, max_tokens = _session_shape(c, self.L, max_new_tokens)
+        self.dm = model.device_model()
+        with torch.cuda.device(self.dm.device):
+            self.s = self.dm.session(self.B, cap, max_tokens, max_new_tokens, logits="last", beam=self.K)
+        d = N.BeamDesc()
+        d.requests, d.beam, d.max_new, d.prompt_len, d.eos = self.R, self.K, max_new_tokens, self.L, c.eos_token
+        s = self.s
+        d.scores, d.finished, d.tokens = s.scores.data_ptr(), s.finished.data_ptr(), s.beam_tokens.data_ptr()
+        d.tok_hist, d.par_hist = s.tok_hist.data_ptr(), s.par_hist.data_ptr()
+        self.desc = d
+        self.launches = 0
+
+    def stage_inputs(self) -> int:
+        """H2D of ids/positions/pads + device-side state init; returns H2D bytes."""
+        import torch
+        s, B, K = self.s, self.B, self.K
+        nbytes = s.load_inputs(self.ids, self.pos, self.pads)
+        s.indir.copy_((torch.arange(B, device=s.indir.device, dtype=torch.int32) % K)[:, None]
+                      .expand(B, s.capacity))
+        s.scores.fill_(float("-inf"))
+        s.scores[::K] = 0.0
+        s.finished.zero_()
+        return nbytes
+
+    def run_device(self, use_graph: bool = True) -> None:
+        import torch
+        s = self.s
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        n_pre = s.forward(self.L, N.FWD_LOGITS_LAST)
+        N.check(N.lib().tf_beam_select(s.handle, C.byref(self.desc), stream), "tf_beam_select")
+        per_step = 0
+        if self.new > 1:
+            N.check(N.lib().tf_beam_decode(s.handle, C.byref(self.desc), self.new - 1,
+                                           1 if use_graph else 0, stream), "tf_beam_decode")
+            s.len += self.new - 1
+            per_step = N.lib().tf_session_launches_per_step(s.handle)
+        self.launches = n_pre + 1 + (self.new - 1) * per_step
+        _count_forward(self.c, self.B, self.L, 0, int(self.pads.sum()), self.B, n_pre + 1)
+        for step in range(1, self.new):
+            _count_forward(self.c, self.B, 1, self.L + step - 1, int(self.pads.sum()), self.B, per_step)
+
+    def finish(self):
+        """D2H of scores and histories, host backtrack; returns (seqs, D2H bytes)."""
+        s = self.s
+        scores = s.scores.cpu().numpy()
+        tok_hist = s.tok_hist.cpu().numpy()
+        par_hist = s.par_hist.cpu().numpy()
+        nbytes = scores.nbytes + tok_hist.nbytes + par_hist.nbytes
+        return _backtrack(self.c, self.prompts, scores, tok_hist, par_hist, self.K), nbytes
+
+
 def beam_search_decode(model: Model, prompts: list[list[int]], max_new_tokens: int,
                        beam_width: int = 4, use_graph: bool = True) -> list[list[int]]:
     """Beam search for a group of prompts; returns one sequence per prompt."""
@@ -65,36 +133,13 @@ def beam_search_decode(model: Model, prompts: list[list[int]], max_new_tokens: i
     checked = _validate_prompts(c, prompts, max_new_tokens)
     if max_new_tokens == 0:
         return [list(p) for p in checked]
-    R, K = len(checked), beam_width
-    flat = [p for p in checked for _ in range(K)]
-    ids, pos, pads, _ = _left_pad(c, flat)
-    B, L = ids.shape
-    cap = min(L + max_new_tokens, c.max_position)
-    dm = model.device_model()
-    with dm.lock, torch.cuda.device(dm.device):
-        s = dm.session(B, cap, L, max_new_tokens, logits="last", beam=K)
-        s.load_inputs(ids, pos, pads)
-        s.indir.copy_((torch.arange(B, device=dm.device, dtype=torch.int32) % K)[:, None].expand(B, cap))
-        init = torch.full((B,), float("-inf"), dtype=torch.float32, device=dm.device)
-        init[::K] = 0.0
-        s.scores.copy_(init)
-        s.finished.zero_()
-        d = N.BeamDesc()
-        d.requests, d.beam, d.max_new, d.prompt_len, d.eos = R, K, max_new_tokens, L, c.eos_token
-        d.scores, d.finished, d.tokens = s.scores.data_ptr(), s.finished.data_ptr(), s.beam_tokens.data_ptr()
-        d.tok_hist, d.par_hist = s.tok_hist.data_ptr(), s.par_hist.data_ptr()
-        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-        n_pre = s.forward(L, N.FWD_LOGITS_LAST)
-        N.check(N.lib().tf_beam_select(s.handle, C.byref(d), stream), "tf_beam_select")
-        if max_new_tokens > 1:
-            N.check(N.lib().tf_beam_decode(s.handle, C.byref(d), max_new_tokens - 1,
-                                           1 if use_graph else 0, stream), "tf_beam_decode")
-            s.len += max_new_tokens - 1
-        per_step = N.lib().tf_session_launches_per_step(s.handle)
-        scores = s.scores.cpu().numpy()
-        tok_hist = s.tok_hist.cpu().numpy()
-        par_hist = s.par_hist.cpu().numpy()
-    _count_forward(c, B, L, 0, int(pads.sum()), B, n_pre + 1)
-    for step in range(1, max_new_tokens):
-        _count_forward(c, B, 1, L + step - 1, int(pads.sum()), B, per_step)
-    return _backtrack(c, checked, scores, tok_hist, par_hist, K)
+    run = BeamRun(model, checked, max_new_tokens, beam_width)
+    with run.dm.lock, torch.cuda.device(run.dm.device):
+        h2d = run.stage_inputs()
+        run.run_device(use_graph)
+        seqs, d2h = run.finish()
+    from . import model as M
+    st = M.GenerateStats()
+    st.h2d_bytes, st.d2h_bytes, st.launches = h2d, d2h, run.launches
+    M.LAST_STATS = st
+    return seqs

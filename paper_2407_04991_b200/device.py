@@ -99,10 +99,10 @@ class DeviceModel:
         h = C.c_void_p()
         N.check(N.lib().tf_model_create(C.byref(d), C.byref(h)), "tf_model_create")
         self.handle = h
-        # shared split-K scratch (sessions of one model run sequentially under self.lock)
-        self.ws_bytes = 64 << 20
+        # reserved C-ABI scratch fields (split-K reduces through DSMEM; kept tiny)
+        self.ws_bytes = 1 << 12
         self.ws = torch.empty(self.ws_bytes // 4, dtype=torch.float32, device=device)
-        self.n_counters = 1 << 16
+        self.n_counters = 16
         self.counters = torch.zeros(self.n_counters, dtype=torch.int32, device=device)
         self._sessions: dict[tuple, Session] = {}
 
@@ -119,7 +119,7 @@ class DeviceModel:
         key = (batch, capacity, max_tokens, max_new, logits, beam)
         s = self._sessions.get(key)
         if s is None:
-            if len(self._sessions) >= 8:  # bound the cache; drop the oldest
+            if len(self._sessions) >= 16:  # bound the cache; drop the oldest
                 old = next(iter(self._sessions))
                 self._sessions.pop(old).close()
             s = Session(self, batch, capacity, max_tokens, max_new, logits, beam=beam)

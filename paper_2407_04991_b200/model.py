@@ -502,6 +502,17 @@ def _left_pad(c: ModelConfig, prompts):
     return ids, pos, pads, lens
 
 
+def _session_shape(c: ModelConfig, L: int, max_new_tokens: int) -> tuple[int, int]:
+    """(capacity, max_tokens) of the session serving prompts of padded length L:
+    rounded up to multiples of 64 so groups of nearby lengths share one session
+    (and its captured decode graph); capacity never exceeds max_position and
+    always covers L + max_new_tokens (the reference sizes it exactly,
+    model.py:643-644 — a larger cache changes nothing but memory)."""
+    r64 = lambda n: (n + 63) // 64 * 64  # noqa: E731
+    cap = min(r64(L + max_new_tokens), c.max_position)
+    return max(cap, min(L + max_new_tokens, c.max_position)), r64(L)
+
+
 def _validate_prompts(c: ModelConfig, prompts, max_new_tokens: int) -> list[list[int]]:
     checked = []
     for p in prompts:
@@ -551,11 +562,11 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
         return seqs
     ids, pos, pads, lens = _left_pad(c, checked)
     B, L = ids.shape
-    cap = min(L + max_new_tokens, c.max_position)
+    cap, max_tokens = _session_shape(c, L, max_new_tokens)
     dm = model.device_model()
     stats = GenerateStats()
     with dm.lock, torch.cuda.device(dm.device):
-        s = dm.session(B, cap, L, max_new_tokens)
+        s = dm.session(B, cap, max_tokens, max_new_tokens)
         stats.h2d_bytes = s.load_inputs(ids, pos, pads)
         n_pre = s.forward(L, N.FWD_ARGMAX)
         n_dec = s.decode(max_new_tokens - 1)
