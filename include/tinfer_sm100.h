@@ -194,6 +194,11 @@ int tf_beam_select(void* session, const tf_beam_desc* d, void* stream);
  * captured once into a CUDA graph when use_graph. */
 int tf_beam_decode(void* session, const tf_beam_desc* d, int n_steps, int use_graph, void* stream);
 
+/* Diagnostics: record per-task globaltimer stamps of decode step 1 of the next
+ * megakernel launch into trace_buf ([n_items + n_aux][3] int64; NULL disables);
+ * reports the session's task counts and copies the plan (int4 per task). */
+int tf_debug_mk_trace(void* session, void* trace_buf, int* n_items, int* n_aux, void* plan_out);
+
 /* Kernels launched by one decode step (for the bench's gpu_launches count). */
 int tf_session_launches_per_step(void* session);
 

@@ -70,23 +70,6 @@ __device__ __forceinline__ void ln_row_store(const float (&xv)[VPL], int H, cons
 // ---- 16-byte vectorised variants (H % 8 == 0): lane owns 8-element chunks
 // c8 = lane + 32*i; every load of the row (x, gamma, beta) is issued before the
 // first use so one row costs ~one memory round trip.
-__device__ __forceinline__ void unpack8(const uint4& r, float* f) {
-  const __half2* h = reinterpret_cast<const __half2*>(&r);
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const float2 t = __half22float2(h[e]);
-    f[2 * e] = t.x;
-    f[2 * e + 1] = t.y;
-  }
-}
-__device__ __forceinline__ uint4 pack8(const float* f) {
-  uint4 r;
-  __half* h = reinterpret_cast<__half*>(&r);
-#pragma unroll
-  for (int e = 0; e < 8; ++e) h[e] = f16_sat(f[e]);
-  return r;
-}
-
 template <int NC>
 __device__ __forceinline__ void ln_row_vec(float (&xv)[NC * 8], int H, const float* g,
                                            const float* b, __half* hrow, int lane) {

@@ -14,6 +14,7 @@
 #include "../../include/tinfer_sm100.h"
 #include "attention.cuh"
 #include "beam.cuh"
+#include "decode_mk.cuh"
 #include "common.cuh"
 #include "gemm_tc.cuh"
 #include "norm_embed.cuh"
@@ -395,9 +396,26 @@ struct Model {
   std::vector<tf_layer_weights> layers;
 };
 
+// Session-owned scratch of the persistent decode megakernel (allocated on first use).
+struct MkState {
+  bool ready = false;
+  int bn = 0, ws = 0, bs = 0, grid = 0, n_ctr = 0;
+  void* mem = nullptr;  // one allocation carved into the pieces below
+  __half *x, *h1, *h2, *attn, *hf;
+  float *p_qkv, *p_wo, *p_w1, *p_w2;
+  int* ctr;
+  int4* items;
+  int* item_off;
+  int4* aux;
+  int* aux_off;
+  mk::Layer* layers;
+  mk::Maps maps;
+};
+
 struct Session {
   Model* m;
   tf_session_desc d;
+  MkState mk;
   cudaGraphExec_t graph = nullptr;
   cudaGraphExec_t beam_graph = nullptr;
   tf_beam_desc beam_key{};  // descriptor the beam graph was captured with
@@ -626,6 +644,223 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
   return launches;
 }
 
+// ---------------------------------------------------------------- megakernel
+long long* g_mk_trace = nullptr;  // tf_debug_set_trace (diagnostics only)
+
+bool mk_enabled() {  // opt-in until it beats the graph path (TF_MEGAKERNEL=1)
+  const char* e = getenv("TF_MEGAKERNEL");
+  return e && e[0] == '1';
+}
+
+bool mk_eligible(const Session& s) {
+  const tf_model_desc& m = s.m->d;
+  return m.head_dim == 64 && m.hidden % 128 == 0 && m.ffn % 128 == 0 && m.layers <= mk::kMaxLayers &&
+         m.hidden <= 1024 && s.d.batch <= 128 && s.d.beam_indir == nullptr && s.d.out_tokens &&
+         mk::smem_bytes(4, 4, ((s.d.batch + 15) / 16) * 16, s.d.capacity) <= kMaxSmem;
+}
+
+void mk_prepare(Session& s) {
+  MkState& k = s.mk;
+  if (k.ready) return;
+  const tf_model_desc& m = s.m->d;
+  const int L = m.layers, H = m.hidden, F = m.ffn, NH = m.heads, V = m.vocab, B = s.d.batch;
+  const int bn = ((B + 15) / 16) * 16;
+  const int nck = H / 128, ncf = F / 128, nqkv = 3 * H / 128, lmt = (V + 127) / 128;
+  int dev = 0;
+  TF_CHECK_CUDA(cudaGetDevice(&dev));
+  int sms = 0;
+  TF_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  k.bn = bn;
+  k.ws = 8;
+  k.bs = 8;
+  while (mk::smem_bytes(k.ws, k.bs, bn, s.d.capacity) > kMaxSmem && k.ws > 4) {
+    --k.ws;
+    if (mk::smem_bytes(k.ws, k.bs, bn, s.d.capacity) > kMaxSmem && k.bs > 4) --k.bs;
+  }
+  k.grid = sms;
+  // ---- static plan: GEMM items and aux tasks in one topological order,
+  // dealt to CTAs so every CTA's list is a subsequence of that order
+  std::vector<std::vector<int4>> gi(k.grid), ai(k.grid);
+  std::vector<long> load(k.grid, 0);
+  auto put_gemm = [&](int type, int layer, int tile, int chunk, int kblocks) {
+    int best = 0;
+    for (int c = 1; c < k.grid; ++c)
+      if (load[c] < load[best]) best = c;
+    gi[best].push_back(make_int4(type, layer, tile, chunk));
+    load[best] += kblocks;
+  };
+  int rr = 0;
+  auto put_aux = [&](int type, int layer, int b, int h) {
+    ai[rr % k.grid].push_back(make_int4(type, layer, b, h));
+    ++rr;
+  };
+  for (int b = 0; b < B; ++b) put_aux(mk::A_EMB, 0, b, 0);
+  for (int l = 0; l < L; ++l) {
+    for (int t = 0; t < nqkv; ++t)
+      for (int c = 0; c < nck; ++c) put_gemm(mk::G_QKV, l, t, c, 2);
+    // attention: per-warp tasks, dealt 4 per aux entry (one per aux warp)
+    for (int id = 0; id < NH * B; id += 4) put_aux(mk::A_ATT, l, id, std::min(4, NH * B - id));
+    for (int c = 0; c < nck; ++c)
+      for (int t = 0; t < nck; ++t) put_gemm(mk::G_WO, l, t, c, 2);
+    for (int b = 0; b < B; ++b) put_aux(mk::A_R2, l, b, 0);
+    for (int t = 0; t < ncf; ++t)
+      for (int c = 0; c < nck; ++c) put_gemm(mk::G_W1, l, t, c, 2);
+    for (int c = 0; c < ncf; ++c)
+      for (int t = 0; t < nck; ++t) put_gemm(mk::G_W2, l, t, c, 2);
+    for (int b = 0; b < B; ++b) put_aux(mk::A_R1, l, b, 0);
+  }
+  for (int t = 0; t < lmt; ++t) put_gemm(mk::G_LM, 0, t, 0, 2 * nck);
+  std::vector<int4> items, aux;
+  std::vector<int> ioff(k.grid + 1, 0), aoff(k.grid + 1, 0);
+  for (int c = 0; c < k.grid; ++c) {
+    ioff[c] = (int)items.size();
+    items.insert(items.end(), gi[c].begin(), gi[c].end());
+    aoff[c] = (int)aux.size();
+    aux.insert(aux.end(), ai[c].begin(), ai[c].end());
+  }
+  ioff[k.grid] = (int)items.size();
+  aoff[k.grid] = (int)aux.size();
+  // ---- one device allocation for everything
+  const int ldx = m.ldk_h;
+  k.n_ctr = mk::ctr_count(L, nqkv, NH, ncf);
+  const size_t act = (size_t)bn * ldx * sizeof(__half);
+  const size_t tile = (size_t)bn * 128 * sizeof(float);
+  size_t off = 0;
+  auto take = [&](size_t n) {
+    size_t o = off;
+    off += (n + 255) / 256 * 256;
+    return o;
+  };
+  const size_t o_x = take(act), o_h1 = take(act), o_h2 = take(act), o_at = take(act), o_hf = take(act);
+  const size_t o_pq = take(tile * nqkv * nck), o_pwo = take(tile * nck * nck);
+  const size_t o_pw1 = take(tile * ncf * nck), o_pw2 = take(tile * nck * ncf);
+  const size_t o_ctr = take(sizeof(int) * k.n_ctr);
+  const size_t o_it = take(sizeof(int4) * items.size()), o_io = take(sizeof(int) * ioff.size());
+  const size_t o_ax = take(sizeof(int4) * aux.size()), o_ao = take(sizeof(int) * aoff.size());
+  const size_t o_ly = take(sizeof(mk::Layer) * L);
+  TF_CHECK_CUDA(cudaMalloc(&k.mem, off));
+  TF_CHECK_CUDA(cudaMemset(k.mem, 0, off));
+  uint8_t* base = static_cast<uint8_t*>(k.mem);
+  k.x = reinterpret_cast<__half*>(base + o_x);
+  k.h1 = reinterpret_cast<__half*>(base + o_h1);
+  k.h2 = reinterpret_cast<__half*>(base + o_h2);
+  k.attn = reinterpret_cast<__half*>(base + o_at);
+  k.hf = reinterpret_cast<__half*>(base + o_hf);
+  k.p_qkv = reinterpret_cast<float*>(base + o_pq);
+  k.p_wo = reinterpret_cast<float*>(base + o_pwo);
+  k.p_w1 = reinterpret_cast<float*>(base + o_pw1);
+  k.p_w2 = reinterpret_cast<float*>(base + o_pw2);
+  k.ctr = reinterpret_cast<int*>(base + o_ctr);
+  k.items = reinterpret_cast<int4*>(base + o_it);
+  k.item_off = reinterpret_cast<int*>(base + o_io);
+  k.aux = reinterpret_cast<int4*>(base + o_ax);
+  k.aux_off = reinterpret_cast<int*>(base + o_ao);
+  k.layers = reinterpret_cast<mk::Layer*>(base + o_ly);
+  std::vector<mk::Layer> ly(L);
+  for (int l = 0; l < L; ++l) {
+    const tf_layer_weights& w = s.m->layers[l];
+    ly[l] = mk::Layer{w.ln1_gamma, w.ln1_beta, w.bqkv, w.bo, w.ln2_gamma, w.ln2_beta, w.b1, w.b2};
+  }
+  TF_CHECK_CUDA(cudaMemcpy(k.items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
+  TF_CHECK_CUDA(cudaMemcpy(k.item_off, ioff.data(), sizeof(int) * ioff.size(), cudaMemcpyHostToDevice));
+  TF_CHECK_CUDA(cudaMemcpy(k.aux, aux.data(), sizeof(int4) * aux.size(), cudaMemcpyHostToDevice));
+  TF_CHECK_CUDA(cudaMemcpy(k.aux_off, aoff.data(), sizeof(int) * aoff.size(), cudaMemcpyHostToDevice));
+  TF_CHECK_CUDA(cudaMemcpy(k.layers, ly.data(), sizeof(mk::Layer) * L, cudaMemcpyHostToDevice));
+  // ---- tensor maps
+  for (int l = 0; l < L; ++l) {
+    const tf_layer_weights& w = s.m->layers[l];
+    k.maps.w[4 * l + 0] = make_kmajor_map(w.wqkv_t, 3 * H, pad64(H), m.ldk_h, 128);
+    k.maps.w[4 * l + 1] = make_kmajor_map(w.wo_t, H, pad64(H), m.ldk_h, 128);
+    k.maps.w[4 * l + 2] = make_kmajor_map(w.w1_t, F, pad64(H), m.ldk_h, 128);
+    k.maps.w[4 * l + 3] = make_kmajor_map(w.w2_t, H, pad64(F), m.ldk_f, 128);
+  }
+  k.maps.w[4 * L] = make_kmajor_map(m.lm_head_t, V, pad64(H), m.ldk_h, 128);
+  k.maps.act[0] = make_kmajor_map(k.h1, bn, pad64(H), ldx, bn);
+  k.maps.act[1] = make_kmajor_map(k.attn, bn, pad64(H), ldx, bn);
+  k.maps.act[2] = make_kmajor_map(k.h2, bn, pad64(H), ldx, bn);
+  k.maps.act[3] = make_kmajor_map(k.hf, bn, pad64(H), ldx, bn);
+  TF_CHECK_CUDA(cudaFuncSetAttribute(mk::decode_megakernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kMaxSmem));
+  k.ready = true;
+}
+
+int mk_decode(Session& s, int n_steps, cudaStream_t st) {
+  mk_prepare(s);
+  MkState& k = s.mk;
+  const tf_model_desc& m = s.m->d;
+  mk::Params p{};
+  p.L = m.layers;
+  p.H = m.hidden;
+  p.F = m.ffn;
+  p.NH = m.heads;
+  p.V = m.vocab;
+  p.B = s.d.batch;
+  p.bn = k.bn;
+  p.cap = s.d.capacity;
+  p.n_steps = n_steps;
+  p.ws = k.ws;
+  p.bs = k.bs;
+  p.nck = m.hidden / 128;
+  p.ncf = m.ffn / 128;
+  p.nqkv = 3 * m.hidden / 128;
+  p.lm_tiles = (m.vocab + 127) / 128;
+  p.layers = k.layers;
+  p.fin_g = m.final_gamma;
+  p.fin_b = m.final_beta;
+  p.tok_emb = static_cast<const __half*>(m.tok_emb);
+  p.pos_emb = static_cast<const __half*>(m.pos_emb);
+  p.ldw = m.ldw;
+  p.x = k.x;
+  p.h1 = k.h1;
+  p.h2 = k.h2;
+  p.attn = k.attn;
+  p.hf = k.hf;
+  p.ldx = m.ldk_h;
+  p.p_qkv = k.p_qkv;
+  p.p_wo = k.p_wo;
+  p.p_w1 = k.p_w1;
+  p.p_w2 = k.p_w2;
+  p.kc = static_cast<__half*>(s.d.k_cache);
+  p.vc = static_cast<__half*>(s.d.v_cache);
+  p.pads = s.d.pads;
+  p.len_dev = s.d.len_dev;
+  p.step_dev = s.d.step_dev;
+  p.keys = s.d.keys;
+  p.out_tokens = s.d.out_tokens;
+  p.max_new = s.d.max_new;
+  p.ctr = k.ctr;
+  p.items = k.items;
+  p.item_off = k.item_off;
+  p.aux = k.aux;
+  p.aux_off = k.aux_off;
+  p.scale = 0.125f;
+  p.trace = g_mk_trace;
+  p.trace_step = 1;
+  {
+    const char* f = getenv("TF_MK_FLAGS");
+    const char* z = getenv("TF_MK_SLEEP");
+    p.flags = f ? atoi(f) : 1;
+    p.sleep_ns = z ? atoi(z) : 128;
+    const int mode = (p.flags >> 1) & 1;
+    TF_CHECK_CUDA(cudaMemcpyToSymbolAsync(mk::g_poll_mode, &mode, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+    TF_CHECK_CUDA(cudaMemcpyToSymbolAsync(mk::g_poll_sleep, &p.sleep_ns, sizeof(int), 0,
+                                          cudaMemcpyHostToDevice, st));
+  }
+  TF_CHECK_CUDA(cudaMemsetAsync(k.ctr, 0, sizeof(int) * k.n_ctr, st));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(k.grid);
+  cfg.blockDim = dim3(mk::kThreads);
+  cfg.dynamicSmemBytes = mk::smem_bytes(k.ws, k.bs, k.bn, s.d.capacity);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (spin-waits are safe)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, mk::decode_megakernel, k.maps, p));
+  return 2;  // memset + kernel
+}
+
 BeamArgs beam_args(const Session& s, const tf_beam_desc& d) {
   TF_REQUIRE(d.beam >= 1 && d.beam <= kMaxBeam, TF_ERR_UNSUPPORTED, "beam width must be in [1, 8]");
   TF_REQUIRE(d.requests * d.beam == s.d.batch, TF_ERR_SHAPE, "beam: requests*beam != session batch");
@@ -802,6 +1037,7 @@ int tf_session_destroy(void* session) {
     Session* s = static_cast<Session*>(session);
     if (s && s->graph) cudaGraphExecDestroy(s->graph);
     if (s && s->beam_graph) cudaGraphExecDestroy(s->beam_graph);
+    if (s && s->mk.mem) cudaFree(s->mk.mem);
     delete s;
   });
 }
@@ -821,6 +1057,11 @@ int tf_decode(void* session, int n_steps, int use_graph, void* stream) {
     Session& s = *static_cast<Session*>(session);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (n_steps <= 0) return;
+    if (use_graph && mk_enabled() && mk_eligible(s)) {
+      mk_decode(s, n_steps, st);
+      s.launches_last = 1;  // one persistent kernel for all n steps
+      return;
+    }
     if (!use_graph) {
       for (int i = 0; i < n_steps; ++i)
         s.launches_last = forward(s, nullptr, nullptr, 1, TF_FWD_ARGMAX, true, st);
@@ -895,6 +1136,26 @@ int tf_beam_decode(void* session, const tf_beam_desc* d, int n_steps, int use_gr
     }
     for (int i = 0; i < n_steps; ++i) TF_CHECK_CUDA(cudaGraphLaunch(s.beam_graph, st));
     s.launches_last = s.graph_launches;
+  });
+}
+
+int tf_debug_mk_trace(void* session, void* trace_buf, int* n_items, int* n_aux, void* plan_out) {
+  return guarded([&] {
+    TF_REQUIRE(session, TF_ERR_ARG, "trace: null session");
+    Session& s = *static_cast<Session*>(session);
+    g_mk_trace = static_cast<long long*>(trace_buf);
+    if (s.mk.ready && n_items && n_aux) {
+      int off[2];
+      TF_CHECK_CUDA(cudaMemcpy(off, s.mk.item_off + s.mk.grid, sizeof(int), cudaMemcpyDeviceToHost));
+      TF_CHECK_CUDA(cudaMemcpy(off + 1, s.mk.aux_off + s.mk.grid, sizeof(int), cudaMemcpyDeviceToHost));
+      *n_items = off[0];
+      *n_aux = off[1];
+      if (plan_out) {
+        TF_CHECK_CUDA(cudaMemcpy(plan_out, s.mk.items, sizeof(int4) * off[0], cudaMemcpyDeviceToHost));
+        TF_CHECK_CUDA(cudaMemcpy(static_cast<int4*>(plan_out) + off[0], s.mk.aux, sizeof(int4) * off[1],
+                                 cudaMemcpyDeviceToHost));
+      }
+    }
   });
 }
 
