@@ -399,10 +399,10 @@ struct Model {
 // Session-owned scratch of the persistent decode megakernel (allocated on first use).
 struct MkState {
   bool ready = false;
-  int bn = 0, ws = 0, bs = 0, grid = 0, n_ctr = 0;
+  int bn = 0, ws = 0, bs = 0, att_slots = 0, grid = 0, n_ctr = 0;
   void* mem = nullptr;  // one allocation carved into the pieces below
-  __half *x, *h1, *h2, *attn, *hf;
-  float *p_qkv, *p_wo, *p_w1, *p_w2;
+  __half *x, *h1, *h2, *attn, *hf, *q, *f;
+  float* p_w2;
   int* ctr;
   int4* items;
   int* item_off;
@@ -654,9 +654,9 @@ bool mk_enabled() {  // opt-in until it beats the graph path (TF_MEGAKERNEL=1)
 
 bool mk_eligible(const Session& s) {
   const tf_model_desc& m = s.m->d;
-  return m.head_dim == 64 && m.hidden % 128 == 0 && m.ffn % 128 == 0 && m.layers <= mk::kMaxLayers &&
+  return m.head_dim == 64 && m.hidden % 128 == 0 && m.ffn % m.hidden == 0 && m.layers <= mk::kMaxLayers &&
          m.hidden <= 1024 && s.d.batch <= 128 && s.d.beam_indir == nullptr && s.d.out_tokens &&
-         mk::smem_bytes(4, 4, ((s.d.batch + 15) / 16) * 16, s.d.capacity) <= kMaxSmem;
+         mk::smem_bytes(4, 3, ((s.d.batch + 15) / 16) * 16, s.d.capacity, 16) <= kMaxSmem;
 }
 
 void mk_prepare(Session& s) {
@@ -665,29 +665,32 @@ void mk_prepare(Session& s) {
   const tf_model_desc& m = s.m->d;
   const int L = m.layers, H = m.hidden, F = m.ffn, NH = m.heads, V = m.vocab, B = s.d.batch;
   const int bn = ((B + 15) / 16) * 16;
-  const int nck = H / 128, ncf = F / 128, nqkv = 3 * H / 128, lmt = (V + 127) / 128;
+  const int nth = H / 128, nff = F / 128, nqkv = 3 * H / 128, nsplit = F / H, lmt = (V + 127) / 128;
   int dev = 0;
   TF_CHECK_CUDA(cudaGetDevice(&dev));
   int sms = 0;
   TF_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   k.bn = bn;
-  k.ws = 8;
-  k.bs = 8;
-  while (mk::smem_bytes(k.ws, k.bs, bn, s.d.capacity) > kMaxSmem && k.ws > 4) {
-    --k.ws;
-    if (mk::smem_bytes(k.ws, k.bs, bn, s.d.capacity) > kMaxSmem && k.bs > 4) --k.bs;
-  }
   k.grid = sms;
+  // smem: weight ring, activation ring, then as many attention K slots as fit
+  k.ws = 6;
+  k.bs = 4;
+  auto slots_for = [&](int ws, int bs) {
+    const long left = (long)kMaxSmem - (long)mk::smem_bytes(ws, bs, bn, s.d.capacity, 0);
+    return (int)std::max(0L, left / (4 * 128));
+  };
+  if (slots_for(k.ws, k.bs) < 64) k.ws = 4;
+  k.att_slots = std::min(slots_for(k.ws, k.bs), s.d.capacity);
   // ---- static plan: GEMM items and aux tasks in one topological order,
   // dealt to CTAs so every CTA's list is a subsequence of that order
   std::vector<std::vector<int4>> gi(k.grid), ai(k.grid);
   std::vector<long> load(k.grid, 0);
-  auto put_gemm = [&](int type, int layer, int tile, int chunk, int kblocks) {
-    int best = 0;
-    for (int c = 1; c < k.grid; ++c)
-      if (load[c] < load[best]) best = c;
-    gi[best].push_back(make_int4(type, layer, tile, chunk));
-    load[best] += kblocks;
+  int next_g = 0;
+  auto put_gemm = [&](int type, int layer, int tile, int split) {
+    // all items stream the same bytes; deal round-robin (least loaded == next)
+    gi[next_g].push_back(make_int4(type, layer, tile, split));
+    load[next_g] += 1;
+    next_g = (next_g + 1) % k.grid;
   };
   int rr = 0;
   auto put_aux = [&](int type, int layer, int b, int h) {
@@ -696,20 +699,16 @@ void mk_prepare(Session& s) {
   };
   for (int b = 0; b < B; ++b) put_aux(mk::A_EMB, 0, b, 0);
   for (int l = 0; l < L; ++l) {
-    for (int t = 0; t < nqkv; ++t)
-      for (int c = 0; c < nck; ++c) put_gemm(mk::G_QKV, l, t, c, 2);
-    // attention: per-warp tasks, dealt 4 per aux entry (one per aux warp)
+    for (int t = 0; t < nqkv; ++t) put_gemm(mk::G_QKV, l, t, 0);
     for (int id = 0; id < NH * B; id += 4) put_aux(mk::A_ATT, l, id, std::min(4, NH * B - id));
-    for (int c = 0; c < nck; ++c)
-      for (int t = 0; t < nck; ++t) put_gemm(mk::G_WO, l, t, c, 2);
+    for (int t = 0; t < nth; ++t) put_gemm(mk::G_WO, l, t, 0);
     for (int b = 0; b < B; ++b) put_aux(mk::A_R2, l, b, 0);
-    for (int t = 0; t < ncf; ++t)
-      for (int c = 0; c < nck; ++c) put_gemm(mk::G_W1, l, t, c, 2);
-    for (int c = 0; c < ncf; ++c)
-      for (int t = 0; t < nck; ++t) put_gemm(mk::G_W2, l, t, c, 2);
+    for (int t = 0; t < nff; ++t) put_gemm(mk::G_W1, l, t, 0);
+    for (int c = 0; c < nsplit; ++c)
+      for (int t = 0; t < nth; ++t) put_gemm(mk::G_W2, l, t, c);
     for (int b = 0; b < B; ++b) put_aux(mk::A_R1, l, b, 0);
   }
-  for (int t = 0; t < lmt; ++t) put_gemm(mk::G_LM, 0, t, 0, 2 * nck);
+  for (int t = 0; t < lmt; ++t) put_gemm(mk::G_LM, 0, t, 0);
   std::vector<int4> items, aux;
   std::vector<int> ioff(k.grid + 1, 0), aoff(k.grid + 1, 0);
   for (int c = 0; c < k.grid; ++c) {
@@ -721,10 +720,9 @@ void mk_prepare(Session& s) {
   ioff[k.grid] = (int)items.size();
   aoff[k.grid] = (int)aux.size();
   // ---- one device allocation for everything
-  const int ldx = m.ldk_h;
-  k.n_ctr = mk::ctr_count(L, nqkv, NH, ncf);
+  const int ldx = m.ldk_h, ldf = m.ldk_f;
+  k.n_ctr = mk::ctr_count(L, nqkv, NH, nff);
   const size_t act = (size_t)bn * ldx * sizeof(__half);
-  const size_t tile = (size_t)bn * 128 * sizeof(float);
   size_t off = 0;
   auto take = [&](size_t n) {
     size_t o = off;
@@ -732,8 +730,8 @@ void mk_prepare(Session& s) {
     return o;
   };
   const size_t o_x = take(act), o_h1 = take(act), o_h2 = take(act), o_at = take(act), o_hf = take(act);
-  const size_t o_pq = take(tile * nqkv * nck), o_pwo = take(tile * nck * nck);
-  const size_t o_pw1 = take(tile * ncf * nck), o_pw2 = take(tile * nck * ncf);
+  const size_t o_q = take(act), o_f = take((size_t)bn * ldf * sizeof(__half));
+  const size_t o_pw2 = take((size_t)nth * bn * nsplit * 128 * sizeof(float));
   const size_t o_ctr = take(sizeof(int) * k.n_ctr);
   const size_t o_it = take(sizeof(int4) * items.size()), o_io = take(sizeof(int) * ioff.size());
   const size_t o_ax = take(sizeof(int4) * aux.size()), o_ao = take(sizeof(int) * aoff.size());
@@ -746,9 +744,8 @@ void mk_prepare(Session& s) {
   k.h2 = reinterpret_cast<__half*>(base + o_h2);
   k.attn = reinterpret_cast<__half*>(base + o_at);
   k.hf = reinterpret_cast<__half*>(base + o_hf);
-  k.p_qkv = reinterpret_cast<float*>(base + o_pq);
-  k.p_wo = reinterpret_cast<float*>(base + o_pwo);
-  k.p_w1 = reinterpret_cast<float*>(base + o_pw1);
+  k.q = reinterpret_cast<__half*>(base + o_q);
+  k.f = reinterpret_cast<__half*>(base + o_f);
   k.p_w2 = reinterpret_cast<float*>(base + o_pw2);
   k.ctr = reinterpret_cast<int*>(base + o_ctr);
   k.items = reinterpret_cast<int4*>(base + o_it);
@@ -769,16 +766,17 @@ void mk_prepare(Session& s) {
   // ---- tensor maps
   for (int l = 0; l < L; ++l) {
     const tf_layer_weights& w = s.m->layers[l];
-    k.maps.w[4 * l + 0] = make_kmajor_map(w.wqkv_t, 3 * H, pad64(H), m.ldk_h, 128);
-    k.maps.w[4 * l + 1] = make_kmajor_map(w.wo_t, H, pad64(H), m.ldk_h, 128);
-    k.maps.w[4 * l + 2] = make_kmajor_map(w.w1_t, F, pad64(H), m.ldk_h, 128);
-    k.maps.w[4 * l + 3] = make_kmajor_map(w.w2_t, H, pad64(F), m.ldk_f, 128);
+    k.maps.w[4 * l + 0] = make_kmajor_map(w.wqkv_t, 3 * H, H, m.ldk_h, 128);
+    k.maps.w[4 * l + 1] = make_kmajor_map(w.wo_t, H, H, m.ldk_h, 128);
+    k.maps.w[4 * l + 2] = make_kmajor_map(w.w1_t, F, H, m.ldk_h, 128);
+    k.maps.w[4 * l + 3] = make_kmajor_map(w.w2_t, H, F, m.ldk_f, 128);
   }
-  k.maps.w[4 * L] = make_kmajor_map(m.lm_head_t, V, pad64(H), m.ldk_h, 128);
-  k.maps.act[0] = make_kmajor_map(k.h1, bn, pad64(H), ldx, bn);
-  k.maps.act[1] = make_kmajor_map(k.attn, bn, pad64(H), ldx, bn);
-  k.maps.act[2] = make_kmajor_map(k.h2, bn, pad64(H), ldx, bn);
-  k.maps.act[3] = make_kmajor_map(k.hf, bn, pad64(H), ldx, bn);
+  k.maps.w[4 * L] = make_kmajor_map(m.lm_head_t, V, H, m.ldk_h, 128);
+  k.maps.act[0] = make_kmajor_map(k.h1, bn, H, ldx, bn);
+  k.maps.act[1] = make_kmajor_map(k.attn, bn, H, ldx, bn);
+  k.maps.act[2] = make_kmajor_map(k.h2, bn, H, ldx, bn);
+  k.maps.act[3] = make_kmajor_map(k.f, bn, F, ldf, bn);
+  k.maps.act[4] = make_kmajor_map(k.hf, bn, H, ldx, bn);
   TF_CHECK_CUDA(cudaFuncSetAttribute(mk::decode_megakernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kMaxSmem));
   k.ready = true;
@@ -800,10 +798,13 @@ int mk_decode(Session& s, int n_steps, cudaStream_t st) {
   p.n_steps = n_steps;
   p.ws = k.ws;
   p.bs = k.bs;
-  p.nck = m.hidden / 128;
-  p.ncf = m.ffn / 128;
+  p.nkb = m.hidden / 64;
+  p.nth = m.hidden / 128;
   p.nqkv = 3 * m.hidden / 128;
+  p.nff = m.ffn / 128;
+  p.nsplit = m.ffn / m.hidden;
   p.lm_tiles = (m.vocab + 127) / 128;
+  p.att_slots = k.att_slots;
   p.layers = k.layers;
   p.fin_g = m.final_gamma;
   p.fin_b = m.final_beta;
@@ -815,10 +816,10 @@ int mk_decode(Session& s, int n_steps, cudaStream_t st) {
   p.h2 = k.h2;
   p.attn = k.attn;
   p.hf = k.hf;
+  p.q = k.q;
+  p.f = k.f;
   p.ldx = m.ldk_h;
-  p.p_qkv = k.p_qkv;
-  p.p_wo = k.p_wo;
-  p.p_w1 = k.p_w1;
+  p.ldf = m.ldk_f;
   p.p_w2 = k.p_w2;
   p.kc = static_cast<__half*>(s.d.k_cache);
   p.vc = static_cast<__half*>(s.d.v_cache);
@@ -836,21 +837,13 @@ int mk_decode(Session& s, int n_steps, cudaStream_t st) {
   p.scale = 0.125f;
   p.trace = g_mk_trace;
   p.trace_step = 1;
-  {
-    const char* f = getenv("TF_MK_FLAGS");
-    const char* z = getenv("TF_MK_SLEEP");
-    p.flags = f ? atoi(f) : 1;
-    p.sleep_ns = z ? atoi(z) : 128;
-    const int mode = (p.flags >> 1) & 1;
-    TF_CHECK_CUDA(cudaMemcpyToSymbolAsync(mk::g_poll_mode, &mode, sizeof(int), 0, cudaMemcpyHostToDevice, st));
-    TF_CHECK_CUDA(cudaMemcpyToSymbolAsync(mk::g_poll_sleep, &p.sleep_ns, sizeof(int), 0,
-                                          cudaMemcpyHostToDevice, st));
-  }
+  const char* fl = getenv("TF_MK_FLAGS");
+  p.flags = fl ? atoi(fl) : 1;
   TF_CHECK_CUDA(cudaMemsetAsync(k.ctr, 0, sizeof(int) * k.n_ctr, st));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(k.grid);
   cfg.blockDim = dim3(mk::kThreads);
-  cfg.dynamicSmemBytes = mk::smem_bytes(k.ws, k.bs, k.bn, s.d.capacity);
+  cfg.dynamicSmemBytes = mk::smem_bytes(k.ws, k.bs, k.bn, s.d.capacity, k.att_slots);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (spin-waits are safe)

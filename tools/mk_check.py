@@ -16,8 +16,10 @@ else:
     m = prune_position_embedding(P.init_random(cfg, 42), 512)
 prompts = O.synthetic_prompts(m.config.vocab_size, B, SRC)
 prompts[0] = prompts[0][: SRC // 2]  # ragged: left padding
+import bench
 res = {}
 for mk in ("0", "1"):
+    os.environ["TF_MEGAKERNEL"] = mk
     os.environ["TF_MEGAKERNEL"] = mk
     out = P.batched_greedy_decode(m, prompts, NEW)
     torch.cuda.synchronize()

@@ -54,5 +54,5 @@ def sub(name, cols):
 sub("ATT", [(0, 1), (1, 3), (3, 4), (4, 5), (5, 6), (6, 7)])
 sub("R1", [(0, 1), (1, 2)])
 sub("R2", [(0, 1), (1, 2)])
-sub("W2", [(0, 3), (3, 4), (4, 5), (5, 2), (1, 2)])
-sub("QKV", [(0, 1), (1, 5), (5, 2)])
+for g in ("QKV", "WO", "W1", "W2"):
+    sub(g, [(0, 1), (1, 5), (5, 2)])
