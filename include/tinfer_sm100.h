@@ -88,6 +88,11 @@ typedef struct tf_gemm_desc {
   int force_swap;                /* -1 auto (swap-AB when m_tok <= 256), 0, 1      */
   int splits;                    /* 0 auto; else divides ceil(k/64), <= 16 (cluster) */
   int pdl;                       /* launch with programmatic dependent launch       */
+  /* optional fused LayerNorm of the activation operand (swap-AB only): act is
+   * ignored and row t of the operand is q16(LN(ln_x[t*ln_src_stride+ln_src_off]))
+   * over ln_hidden features (tensor.py:153-160); ln_hidden <= 1024, % 8 == 0 */
+  const void* ln_x; int ln_ldx, ln_src_stride, ln_src_off, ln_hidden;
+  const float* ln_gamma; const float* ln_beta;
 } tf_gemm_desc;
 int tf_gemm(const tf_gemm_desc* d, void* stream);
 

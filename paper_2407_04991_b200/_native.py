@@ -38,6 +38,9 @@ class GemmDesc(C.Structure):
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
         ("counters", C.c_void_p), ("n_counters", C.c_int),
         ("force_swap", C.c_int), ("splits", C.c_int), ("pdl", C.c_int),
+        ("ln_x", C.c_void_p), ("ln_ldx", C.c_int), ("ln_src_stride", C.c_int),
+        ("ln_src_off", C.c_int), ("ln_hidden", C.c_int),
+        ("ln_gamma", C.c_void_p), ("ln_beta", C.c_void_p),
     ]
 
 

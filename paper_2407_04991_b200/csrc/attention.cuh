@@ -36,26 +36,28 @@ struct AttnArgs {
 };
 
 // ------------------------------------------------------------------ decode
-// blockDim = 128. Dynamic smem: (D + cap + 256) floats.
-__global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
+// blockDim = kDecThreads. Dynamic smem: (D + cap + 2 * kDecThreads) floats.
+constexpr int kDecThreads = 256;
+constexpr int kDecWarps = kDecThreads / 32;
+__global__ void __launch_bounds__(256) attn_decode_kernel(const AttnArgs a) {
   extern __shared__ float sm[];
   pdl_wait();
+  pdl_trigger();
   const int h = blockIdx.x, b = blockIdx.y;
   const int D = a.D;
   float* qs = sm;               // [D]
   float* sc = sm + D;           // [cap] scores / weights
-  float* red = sc + a.cap;      // [256] partial outputs / reduction scratch
+  float* red = sc + a.cap;      // [2 * kDecThreads] partial outputs / reduction scratch
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int qbase = *a.qbase_dev;
   const int lo = a.start[b], hi = qbase;  // inclusive window [lo, hi]
   const int n = hi - lo + 1;
   const __half* qrow = a.q + (size_t)b * a.ldq + (size_t)h * D;  // T == 1
-  for (int d = tid; d < D; d += 128) qs[d] = __half2float(qrow[d]);
+  for (int d = tid; d < D; d += kDecThreads) qs[d] = __half2float(qrow[d]);
   __syncthreads();
   __half* orow = a.out + (size_t)b * a.ldo + (size_t)h * D;
   if (n <= 0) {
-    for (int d = tid; d < D; d += 128) orow[d] = __float2half_rn(0.0f);
-    pdl_trigger();
+    for (int d = tid; d < D; d += kDecThreads) orow[d] = __float2half_rn(0.0f);
     return;
   }
   const size_t head_stride = (size_t)a.cap * D;        // one (row, head) block
@@ -73,26 +75,34 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
   // ---- scores
   if ((D & 7) == 0 && D <= 256) {
     const int G = D >> 3;                 // lanes per key (16 B each)
-    const int kpw = 32 / G > 0 ? 32 / G : 1;  // keys per warp iteration
+    const int kpw = 32 / G > 0 ? 32 / G : 1;  // keys per warp load
     const int sub = lane / G, gl = lane - sub * G;
-    for (int base = warp * kpw; base < n; base += 4 * kpw) {
-      const int j = base + sub;
-      float acc = 0.0f;
-      if (sub < kpw && j < n) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(K + kv_off(lo + j) + gl * 8);
-        const __half2* kh = reinterpret_cast<const __half2*>(&raw);
+    // 8 loads in flight per lane: each warp covers 8 * kpw keys per round
+    for (int base = warp * 8 * kpw; base < n; base += 64 * kpw) {
+      uint4 raw[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = base + u * kpw + sub;
+        raw[u] = (sub < kpw && j < n) ? *reinterpret_cast<const uint4*>(K + kv_off(lo + j) + gl * 8)
+                                      : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = base + u * kpw + sub;
+        float acc = 0.0f;
+        const __half2* kh = reinterpret_cast<const __half2*>(&raw[u]);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 kf = __half22float2(kh[e]);
           acc = __fadd_rn(acc, __fmul_rn(qs[gl * 8 + 2 * e], kf.x));
           acc = __fadd_rn(acc, __fmul_rn(qs[gl * 8 + 2 * e + 1], kf.y));
         }
+        for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (sub < kpw && gl == 0 && j < n) sc[j] = __fmul_rn(acc, a.scale);
       }
-      for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (sub < kpw && gl == 0 && j < n) sc[j] = __fmul_rn(acc, a.scale);
     }
   } else {
-    for (int j = tid; j < n; j += 128) {
+    for (int j = tid; j < n; j += kDecThreads) {
       const __half* kr = K + kv_off(lo + j);
       float acc = 0.0f;
       for (int d = 0; d < D; ++d) acc = __fadd_rn(acc, __fmul_rn(qs[d], __half2float(kr[d])));
@@ -102,14 +112,15 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
   __syncthreads();
   // ---- max, exp, sum
   float m = -INFINITY;
-  for (int j = tid; j < n; j += 128) m = fmaxf(m, sc[j]);
+  for (int j = tid; j < n; j += kDecThreads) m = fmaxf(m, sc[j]);
   m = warp_max(m);
   if (lane == 0) red[warp] = m;
   __syncthreads();
-  m = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  m = red[0];
+  for (int w = 1; w < kDecWarps; ++w) m = fmaxf(m, red[w]);
   __syncthreads();
   float z = 0.0f;
-  for (int j = tid; j < n; j += 128) {
+  for (int j = tid; j < n; j += kDecThreads) {
     const float e = expf(__fsub_rn(sc[j], m));
     sc[j] = e;
     z += e;
@@ -117,22 +128,35 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
   z = warp_sum(z);
   if (lane == 0) red[warp] = z;
   __syncthreads();
-  z = (red[0] + red[1]) + (red[2] + red[3]);
+  z = 0.0f;
+  for (int w = 0; w < kDecWarps; ++w) z += red[w];
   const float inv = __fdiv_rn(1.0f, z);
   __syncthreads();
   // ---- weighted sum of V: threads = (dim pair, key group)
   const int DP = (D + 1) >> 1;  // dim pairs
-  const int groups = 128 / DP > 0 ? 128 / DP : 1;
+  const int groups = kDecThreads / DP > 0 ? kDecThreads / DP : 1;
   const int g = tid / DP, dp = tid - g * DP;
   float o0 = 0.0f, o1 = 0.0f;
   if (g < groups) {
     const int d0 = 2 * dp;
     if ((D & 1) == 0) {
-      for (int j = g; j < n; j += groups) {
-        const float w = __fmul_rn(sc[j], inv);
-        const float2 vf = __half22float2(*reinterpret_cast<const __half2*>(V + kv_off(lo + j) + d0));
-        o0 = __fadd_rn(o0, __fmul_rn(w, vf.x));
-        o1 = __fadd_rn(o1, __fmul_rn(w, vf.y));
+      for (int j0 = g; j0 < n; j0 += 4 * groups) {
+        __half2 vr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u * groups;
+          vr[u] = j < n ? *reinterpret_cast<const __half2*>(V + kv_off(lo + j) + d0) : __floats2half2_rn(0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u * groups;
+          if (j < n) {
+            const float w = __fmul_rn(sc[j], inv);
+            const float2 vf = __half22float2(vr[u]);
+            o0 = __fadd_rn(o0, __fmul_rn(w, vf.x));
+            o1 = __fadd_rn(o1, __fmul_rn(w, vf.y));
+          }
+        }
       }
     } else {
       for (int j = g; j < n; j += groups) {
@@ -148,12 +172,11 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(const AttnArgs a) {
     red[g * 2 * DP + 2 * dp + 1] = o1;
   }
   __syncthreads();
-  for (int d = tid; d < D; d += 128) {
+  for (int d = tid; d < D; d += kDecThreads) {
     float v = 0.0f;
     for (int gg = 0; gg < groups; ++gg) v = __fadd_rn(v, red[gg * 2 * DP + d]);
     orow[d] = f16_sat(v);
   }
-  pdl_trigger();
 }
 
 // ------------------------------------------------------------------ prefill
@@ -165,6 +188,7 @@ constexpr int kPfKeys = 64;
 __global__ void __launch_bounds__(128) attn_prefill_kernel(const AttnArgs a) {
   extern __shared__ float sm[];
   pdl_wait();
+  pdl_trigger();
   const int qblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int D = a.D;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -257,7 +281,6 @@ __global__ void __launch_bounds__(128) attn_prefill_kernel(const AttnArgs a) {
       if (d < D) orow[d] = f16_sat(o[i][k] * inv);
     }
   }
-  pdl_trigger();
 }
 
 }  // namespace tf

@@ -200,9 +200,11 @@ __device__ __forceinline__ uint32_t dsmem_addr(uint32_t local_smem, uint32_t ran
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem), "r"(rank));
   return r;
 }
+// plain (non-volatile, no memory clobber) so independent loads issue back to back;
+// ordering against the partial-tile writes comes from the cluster barrier
 __device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
   float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
 

@@ -60,6 +60,13 @@ struct GemmArgs {
   const int* qbase_dev;  // cache slot of token t = 0 (device scalar; graph-replayable)
   // EPI_LOGITS
   unsigned long long* keys;  // [m_tok] packed (value, ~id) argmax keys, or null
+  // SWAP only: B operand = LayerNorm of x rows computed in-kernel (ln_x != null);
+  // token t reads x row t * ln_src_stride + ln_src_off (full ln_H-wide row for the
+  // statistics, this CTA's K-slice written into shared memory)
+  const __half* ln_x;
+  int ln_ldx, ln_src_stride, ln_src_off, ln_H;
+  const float* ln_g;
+  const float* ln_b;
 };
 
 constexpr int kTileA = 128;          // MMA M
@@ -77,8 +84,89 @@ __host__ __device__ inline size_t gemm_ring_bytes(int bn, int stages, int splits
   size_t part = splits > 1 ? (size_t)kTileA * bn * 4 : 0;
   return ring > part ? ring : part;
 }
-__host__ inline size_t gemm_smem_bytes(int bn, int stages, int splits) {
-  return 1024 + gemm_ring_bytes(bn, stages, splits) + (2 * stages + 1) * 8 + 16;
+__host__ __device__ inline size_t gemm_ln_bytes(int bn, int kb_per_split) {
+  return (size_t)kb_per_split * bn * kBK * 2;
+}
+__host__ inline size_t gemm_smem_bytes(int bn, int stages, int splits, size_t ln_bytes = 0) {
+  return 1024 + gemm_ring_bytes(bn, stages, splits) + ln_bytes + (2 * stages + 1) * 8 + 16;
+}
+
+// LN-fused B operand: 128 threads normalise the CTA's bn token rows over the full
+// row (same operation order as layernorm_vec_kernel, so results are bit-identical
+// to the stand-alone LN) and write the K-slice [kb0*64, (kb0+nkb)*64) into `bln`
+// as nkb swizzled (128-byte) K-major tiles of bn rows.
+__device__ __forceinline__ void ln_build_b(const GemmArgs& p, int tile_b, int kb0, int nkb, uint8_t* bln) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bn = p.bn, H = p.ln_H;
+  constexpr int NC = 4;  // 16-byte chunks per lane: H <= 1024
+  const int c_lo = kb0 * kBK, c_hi = (kb0 + nkb) * kBK;
+  for (int r = warp; r < bn; r += 4) {
+    const int tok = tile_b * bn + r;
+    const bool valid = tok < p.m_tok;
+    float xv[NC * 8];
+    if (valid) {
+      const __half* xr = p.ln_x + ((size_t)tok * p.ln_src_stride + p.ln_src_off) * p.ln_ldx;
+      uint4 raw[NC];
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        const int c = (lane + 32 * i) * 8;
+        if (c < H) raw[i] = __ldcg(reinterpret_cast<const uint4*>(xr + c));
+      }
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        if ((lane + 32 * i) * 8 < H) {
+          unpack8(raw[i], &xv[8 * i]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) xv[8 * i + e] = 0.0f;
+        }
+      }
+    }
+    float mean = 0.0f, inv = 0.0f;
+    if (valid) {
+      float sum = 0.0f;
+#pragma unroll
+      for (int i = 0; i < NC; ++i)
+        if ((lane + 32 * i) * 8 < H)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) sum = __fadd_rn(sum, xv[8 * i + e]);
+      sum = warp_sum(sum);
+      mean = __fdiv_rn(sum, (float)H);
+      float ss = 0.0f;
+#pragma unroll
+      for (int i = 0; i < NC; ++i)
+        if ((lane + 32 * i) * 8 < H)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float d = __fsub_rn(xv[8 * i + e], mean);
+            ss = __fadd_rn(ss, __fmul_rn(d, d));
+          }
+      ss = warp_sum(ss);
+      inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)H), 1e-5f)));
+    }
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const int c = (lane + 32 * i) * 8;
+      if (c < c_lo || c >= c_hi) continue;
+      float y[8];
+      if (valid && c < H) {
+        const float4 g0 = *reinterpret_cast<const float4*>(p.ln_g + c), g1 = *reinterpret_cast<const float4*>(p.ln_g + c + 4);
+        const float4 b0 = *reinterpret_cast<const float4*>(p.ln_b + c), b1 = *reinterpret_cast<const float4*>(p.ln_b + c + 4);
+        const float gf[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float bf[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          y[e] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[8 * i + e], mean), inv), gf[e]), bf[e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) y[e] = 0.0f;
+      }
+      const int kb = (c - c_lo) / kBK, q = ((c - c_lo) % kBK) / 8;
+      uint8_t* dst = bln + (size_t)kb * bn * kBK * 2 + (r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) * 16);
+      *reinterpret_cast<uint4*>(dst) = pack8(y);
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 template <int MODE, bool SWAP>
@@ -192,7 +280,9 @@ __global__ void __launch_bounds__(128, 1)
                                              ~static_cast<uintptr_t>(1023));
   const int bn = p.bn, stages = p.stages;
   const int stage_bytes = gemm_stage_bytes(bn);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + gemm_ring_bytes(bn, stages, p.splits));
+  const bool ln_mode = SWAP && p.ln_x != nullptr;
+  uint8_t* bln = smem + gemm_ring_bytes(bn, stages, p.splits);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bln + (ln_mode ? gemm_ln_bytes(bn, p.kb_per_split) : 0));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 1);
   __shared__ unsigned long long red[64];
 
@@ -219,19 +309,30 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // let the next kernel in the stream launch now: its prologue (barrier init,
+  // TMEM alloc, weight TMA prefetch) overlaps this kernel; it still waits on
+  // griddepcontrol.wait before touching anything this kernel writes
+  pdl_trigger();
 
+  // ---------------- TMA producer. Weights do not depend on the previous
+  // kernel, so in decode (SWAP) mode the first ring's worth of weight tiles is
+  // requested before waiting on the programmatic launch dependency.
+  const uint32_t tx = ln_mode ? (uint32_t)kABytes : (uint32_t)stage_bytes;
+  const int pre = SWAP ? min(stages, nkb) : 0;
   if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer. Weights do not depend on the previous
-    // kernel, so in decode (SWAP) mode the first ring's worth of weight tiles
-    // is requested before waiting on the programmatic launch dependency.
-    const uint32_t tx = (uint32_t)stage_bytes;
-    const int pre = SWAP ? min(stages, nkb) : 0;
     for (int i = 0; i < pre; ++i) {
       const uint32_t sa = smem_u32(smem + (size_t)i * stage_bytes);
       mbar_expect_tx(full0 + 8 * i, tx);
       tma_load_2d(sa, &tmA, (kb0 + i) * kBK, tile_a * kTileA, full0 + 8 * i);
     }
+  }
+  if (ln_mode) {  // all 128 threads build the normalised B tiles, then go on
     pdl_wait();
+    ln_build_b(p, tile_b, kb0, nkb, bln);
+    __syncthreads();
+  }
+  if (warp == 0 && lane == 0) {
+    if (!ln_mode) pdl_wait();
     for (int i = 0; i < nkb; ++i) {
       const int s = i % stages;
       const uint32_t ph = (uint32_t)(i / stages) & 1u;
@@ -242,7 +343,7 @@ __global__ void __launch_bounds__(128, 1)
         mbar_expect_tx(full0 + 8 * s, tx);
         tma_load_2d(sa, &tmA, (kb0 + i) * kBK, tile_a * kTileA, full0 + 8 * s);
       }
-      tma_load_2d(sb, &tmB, (kb0 + i) * kBK, tile_b * bn, full0 + 8 * s);
+      if (!ln_mode) tma_load_2d(sb, &tmB, (kb0 + i) * kBK, tile_b * bn, full0 + 8 * s);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- single-thread MMA issuer
@@ -254,7 +355,7 @@ __global__ void __launch_bounds__(128, 1)
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
       const uint64_t da = umma_desc_sw128(sa);
-      const uint64_t db = umma_desc_sw128(sa + kABytes);
+      const uint64_t db = umma_desc_sw128(ln_mode ? smem_u32(bln + (size_t)i * bn * kBK * 2) : sa + kABytes);
 #pragma unroll
       for (int k = 0; k < kBK / 16; ++k) {
         // advance 16 f16 = 32 B along K inside the swizzle atom (+2 in 16-B units)
@@ -265,7 +366,6 @@ __global__ void __launch_bounds__(128, 1)
     tc_commit(done_bar);
   }
   __syncwarp();
-  pdl_trigger();
 
   // ---------------- epilogue (all 4 warps)
   pdl_wait();
@@ -300,9 +400,15 @@ __global__ void __launch_bounds__(128, 1)
     const int e_lo = (int)rank * per, e_hi = min(E, e_lo + per);
     const uint32_t local = smem_u32(part);
     for (int e = e_lo + threadIdx.x; e < e_hi; e += 128) {
+      // all S loads in flight, then the sum in split order (deterministic)
+      float part_v[16];
+#pragma unroll
+      for (int sp = 0; sp < 16; ++sp)
+        part_v[sp] = sp < S ? ld_dsmem_f32(dsmem_addr(local + 4u * (uint32_t)e, (uint32_t)sp)) : 0.0f;
       float acc = 0.0f;
-      for (int sp = 0; sp < S; ++sp)
-        acc = __fadd_rn(acc, ld_dsmem_f32(dsmem_addr(local + 4u * (uint32_t)e, (uint32_t)sp)));
+#pragma unroll
+      for (int sp = 0; sp < 16; ++sp)
+        if (sp < S) acc = __fadd_rn(acc, part_v[sp]);
       const int col = e / kTileA, r = e - col * kTileA;
       epi_elem<MODE, SWAP>(p, tile_a * kTileA + r, tile_b * bn + col, acc);
     }

@@ -121,6 +121,7 @@ __device__ __forceinline__ void ln_row_vec(float (&xv)[NC * 8], int H, const flo
 template <int NC>
 __global__ void __launch_bounds__(256) embed_ln_vec_kernel(const EmbedArgs a) {
   pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp;
   if (row >= a.n_tok) return;
@@ -169,12 +170,12 @@ __global__ void __launch_bounds__(256) embed_ln_vec_kernel(const EmbedArgs a) {
   if (a.h != nullptr) ln_row_vec<NC>(xv, a.H, a.ln_g, a.ln_b, a.h + (size_t)row * a.ldx, lane);
   if (lane == 0 && a.tok_out) a.tok_out[row] = id;
   if (a.ids == nullptr && lane == 0) a.keys[row] = 0ull;
-  pdl_trigger();
 }
 
 template <int VPL>
 __global__ void __launch_bounds__(256) embed_ln_kernel(const EmbedArgs a) {
   pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp;
   if (row >= a.n_tok) return;
@@ -210,7 +211,6 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(const EmbedArgs a) {
   if (a.h != nullptr) ln_row_store<VPL>(xv, a.H, a.ln_g, a.ln_b, a.h + (size_t)row * a.ldx, lane);
   if (lane == 0 && a.tok_out) a.tok_out[row] = id;
   if (a.ids == nullptr && lane == 0) a.keys[row] = 0ull;  // consumed: reset for the next argmax
-  pdl_trigger();
 }
 
 struct LnArgs {
@@ -226,6 +226,7 @@ struct LnArgs {
 template <int VPL>
 __global__ void __launch_bounds__(256) layernorm_kernel(const LnArgs a) {
   pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp;
   if (row < a.n_rows) {
@@ -238,12 +239,12 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const LnArgs a) {
     }
     ln_row_store<VPL>(xv, a.H, a.g, a.b, a.h + (size_t)row * a.ldh, lane);
   }
-  pdl_trigger();
 }
 
 template <int NC>
 __global__ void __launch_bounds__(256) layernorm_vec_kernel(const LnArgs a) {
   pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp;
   if (row < a.n_rows) {
@@ -266,7 +267,6 @@ __global__ void __launch_bounds__(256) layernorm_vec_kernel(const LnArgs a) {
     }
     ln_row_vec<NC>(xv, a.H, a.g, a.b, a.h + (size_t)row * a.ldh, lane);
   }
-  pdl_trigger();
 }
 
 // Step bookkeeping after the logits argmax: feed ids, append the generated
@@ -283,6 +283,7 @@ struct CollectArgs {
 
 __global__ void collect_kernel(const CollectArgs a) {
   pdl_wait();
+  pdl_trigger();
   const int step = *a.step_dev;
   for (int b = threadIdx.x; b < a.B; b += blockDim.x) {
     const int tok = (int)argmax_id(a.keys[b]);
@@ -293,7 +294,6 @@ __global__ void collect_kernel(const CollectArgs a) {
     *a.step_dev = step + 1;
     *a.len_dev += a.advance;
   }
-  pdl_trigger();
 }
 
 }  // namespace tf

@@ -199,12 +199,22 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
     p.splits = d.splits;
   } else {
     p.splits = (p.swap && d.epilogue != TF_EPI_LOGITS) ? pick_splits(p.tiles_a * p.tiles_b, p.k_blocks) : 1;
+    if (p.swap && d.ln_x && d.epilogue != TF_EPI_LOGITS) {
+      // fused LN: the CTA's normalised K-slice must fit beside the ring
+      while (gemm_ln_bytes(p.bn, p.k_blocks / p.splits) > 96 * 1024) {
+        int next = p.splits + 1;
+        while (next <= 16 && p.k_blocks % next) ++next;
+        if (next > 16) break;
+        p.splits = next;
+      }
+    }
   }
   TF_REQUIRE(p.splits == 1 || d.epilogue != TF_EPI_LOGITS, TF_ERR_ARG,
              "argmax epilogue does not support split-K");
   const int kb_per = p.k_blocks / p.splits;
   const int stage_bytes = gemm_stage_bytes(p.bn);
-  int st = (int)((kMaxSmem - 4096) / stage_bytes);
+  const size_t ln_bytes = (p.swap && d.ln_x) ? gemm_ln_bytes(p.bn, kb_per) : 0;
+  int st = (int)((kMaxSmem - 4096 - ln_bytes) / stage_bytes);
   if (st > 8) st = 8;
   if (st > kb_per) st = kb_per;
   if (st < 1) st = 1;
@@ -217,8 +227,9 @@ void launch_gemm_t(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& 
                    const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
   ensure_gemm_attr<MODE, SWAP>();
   dim3 grid(p.tiles_a, p.tiles_b, p.splits);
+  const size_t ln_bytes = (SWAP && d.ln_x) ? gemm_ln_bytes(p.bn, p.k_blocks / p.splits) : 0;
   launch_cluster(gemm_tc_kernel<MODE, SWAP>, grid, dim3(128),
-                 gemm_smem_bytes(p.bn, p.stages, p.splits), st, d.pdl != 0, p.splits, ta, tb, args);
+                 gemm_smem_bytes(p.bn, p.stages, p.splits, ln_bytes), st, d.pdl != 0, p.splits, ta, tb, args);
 }
 
 template <int MODE>
@@ -265,6 +276,21 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
   a.T = d.seq_len;
   a.qbase_dev = d.qbase_dev;
   a.keys = d.argmax_keys;
+  if (d.ln_x) {
+    TF_REQUIRE(p.swap, TF_ERR_UNSUPPORTED, "gemm: fused LayerNorm needs the swap-AB (decode) path");
+    TF_REQUIRE(d.ln_gamma && d.ln_beta && d.ln_hidden > 0 && d.ln_hidden <= 1024 && d.ln_hidden % 8 == 0 &&
+                   d.ln_ldx % 8 == 0 && d.ln_hidden <= kext,
+               TF_ERR_ARG, "gemm: bad fused LayerNorm arguments");
+    TF_REQUIRE(gemm_ln_bytes(p.bn, p.k_blocks / p.splits) <= 96 * 1024, TF_ERR_UNSUPPORTED,
+               "gemm: fused LayerNorm tile too large");
+    a.ln_x = static_cast<const __half*>(d.ln_x);
+    a.ln_ldx = d.ln_ldx;
+    a.ln_src_stride = d.ln_src_stride;
+    a.ln_src_off = d.ln_src_off;
+    a.ln_H = d.ln_hidden;
+    a.ln_g = d.ln_gamma;
+    a.ln_b = d.ln_beta;
+  }
   switch (d.epilogue) {
     case TF_EPI_BIAS:
     case TF_EPI_BIAS_GELU:
@@ -374,7 +400,7 @@ void run_ln(const LnArgs& a, cudaStream_t st, bool pdl) {
 void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
   TF_REQUIRE(a.D >= 1 && a.D <= 128, TF_ERR_UNSUPPORTED, "head_dim must be in [1, 128]");
   if (a.T == 1) {
-    const size_t smem = (size_t)(a.D + a.cap + 256) * sizeof(float);
+    const size_t smem = (size_t)(a.D + a.cap + 2 * kDecThreads) * sizeof(float);
     TF_REQUIRE(smem <= kMaxSmem, TF_ERR_UNSUPPORTED, "cache capacity too large for decode kernel");
     static bool attr = false;
     if (!attr) {
@@ -382,7 +408,7 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
       attr = true;
     }
-    launch(attn_decode_kernel, dim3(a.NH, a.B), dim3(128), smem, st, pdl, a);
+    launch(attn_decode_kernel, dim3(a.NH, a.B), dim3(kDecThreads), smem, st, pdl, a);
   } else {
     const size_t smem = (size_t)kPfRows * a.D * sizeof(float) + (size_t)2 * kPfKeys * (a.D + 1) * 2;
     launch(attn_prefill_kernel, dim3((a.T + kPfRows - 1) / kPfRows, a.NH, a.B), dim3(128), smem, st,
@@ -483,10 +509,34 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
   g.n_counters = sd.n_counters;
   g.pdl = pdl ? 1 : 0;
 
+  // decode (every GEMM swap-AB): LayerNorms are fused into the consuming GEMM's
+  // operand build instead of running as separate kernels
+  // measured slower than the stand-alone LN kernel under PDL (the fused build
+  // adds dependent row loads to every GEMM's critical path): opt-in only
+  static const bool fuse_opt = [] {
+    const char* e = getenv("TF_FUSE_LN");
+    return e && e[0] == '1';
+  }();
+  const bool fuse_ln = fuse_opt && M <= 256 && H <= 1024 && H % 8 == 0 && m.ldk_h % 8 == 0;
+  // the lm_head (argmax epilogue, no split-K) fuses only if its full-K tile fits
+  const int lg_rows = (mode == TF_FWD_LOGITS_ALL) ? M : B;
+  const bool fuse_final = fuse_ln && lg_rows <= 256 &&
+                          gemm_ln_bytes(((std::min(lg_rows, 256) + 15) / 16) * 16, pad64(H) / 64) <= 96 * 1024;
+  auto set_ln = [&](tf_gemm_desc& d, const float* gam, const float* bet, int stride, int off) {
+    d.ln_x = x;
+    d.ln_ldx = m.ldk_h;
+    d.ln_src_stride = stride;
+    d.ln_src_off = off;
+    d.ln_hidden = H;
+    d.ln_gamma = gam;
+    d.ln_beta = bet;
+  };
+
   for (int l = 0; l < L; ++l) {
     const tf_layer_weights& w = s.m->layers[l];
     // fused QKV projection, K/V straight into the cache (model.py:464-474)
     tf_gemm_desc q = g;
+    if (fuse_ln) set_ln(q, w.ln1_gamma, w.ln1_beta, 1, 0);
     q.n_feat = 3 * H;
     q.k = H;
     q.act = h;
@@ -557,10 +607,13 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     ln.b = w.ln2_beta;
     ln.h = h;
     ln.ldh = m.ldk_h;
-    run_ln(ln, st, pdl);
-    ++launches;
+    if (!fuse_ln) {
+      run_ln(ln, st, pdl);
+      ++launches;
+    }
     // FFN1 + GELU (model.py:488-490)
     tf_gemm_desc f1 = g;
+    if (fuse_ln) set_ln(f1, w.ln2_gamma, w.ln2_beta, 1, 0);
     f1.n_feat = F;
     f1.k = H;
     f1.act = h;
@@ -603,11 +656,19 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
         nl.src_off = T - 1;
       }
     }
-    run_ln(nl, st, pdl);
-    ++launches;
+    if (l + 1 < L ? !fuse_ln : !fuse_final) {
+      run_ln(nl, st, pdl);
+      ++launches;
+    }
   }
   // lm_head (+ argmax) (model.py:500-504, 594, 652)
   tf_gemm_desc lg = g;
+  if (fuse_final) {
+    if (mode == TF_FWD_LOGITS_ALL)
+      set_ln(lg, m.final_gamma, m.final_beta, 1, 0);
+    else
+      set_ln(lg, m.final_gamma, m.final_beta, T, T - 1);
+  }
   lg.m_tok = (mode == TF_FWD_LOGITS_ALL) ? M : B;
   lg.n_feat = m.vocab;
   lg.k = H;

@@ -158,3 +158,31 @@ def test_embed_gather_sum_bit_exact_and_remap(cuda_device):
     assert torch.equal(used.cpu(), want_ids)
     ref = (tok[want_ids.long()].float() + pos[ps.long()].float()).clamp(-65504, 65504).half()
     assert torch.equal(x.cpu(), ref)  # bit-exact gather-sum
+
+
+@pytest.mark.parametrize("m,n,k", [(32, 2304, 768), (5, 200, 128), (32, 1000, 768)])
+def test_gemm_fused_layernorm_operand(cuda_device, m, n, k):
+    """Swap-AB GEMM whose activation operand is LN(x) built in-kernel equals
+    LN kernel + GEMM (bitwise: same LN operation order)."""
+    x = rand16(m, k, seed=20).to(cuda_device)
+    g = (1 + 0.05 * torch.randn(k)).half().float().to(cuda_device)
+    b = (0.05 * torch.randn(k)).half().float().to(cuda_device)
+    w = rand16(n, ops.pad64(k), scale=0.05, seed=21).to(cuda_device)
+    h = torch.empty_like(x)
+    ops.layernorm(x, k, g, b, h)
+    ref = torch.empty(m, n, dtype=torch.float32, device=cuda_device)
+    ops.gemm(h, w, k, N.EPI_F32, out=ref, force_swap=1)
+    got = torch.empty_like(ref)
+    d = N.GemmDesc()
+    d.m_tok, d.n_feat, d.k = m, n, k
+    d.act, d.lda = x.data_ptr(), x.stride(0)
+    d.wt, d.ldw = w.data_ptr(), w.stride(0)
+    d.epilogue = N.EPI_F32
+    d.out, d.ldo = got.data_ptr(), got.stride(0)
+    d.force_swap = 1
+    d.ln_x, d.ln_ldx, d.ln_src_stride, d.ln_src_off, d.ln_hidden = x.data_ptr(), x.stride(0), 1, 0, k
+    d.ln_gamma, d.ln_beta = g.data_ptr(), b.data_ptr()
+    import ctypes as C
+    N.check(N.lib().tf_gemm(C.byref(d), C.c_void_p(torch.cuda.current_stream().cuda_stream)), "tf_gemm")
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
