@@ -238,25 +238,29 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& p, int ra, int qb, con
     }
     if constexpr (MODE == EPI_LOGITS) {
       if (p.keys != nullptr) {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        // keys of this 16-token chunk staged in smem (the drained ring) as
+        // [16][129] u64; each token column is then reduced by 8 threads over
+        // 16 rows each + 3 shuffle rounds, and one atomicMax per token
+        unsigned long long* kred = reinterpret_cast<unsigned long long*>(red);
+        const int row = threadIdx.x;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          unsigned long long k = fok ? argmax_key(q16(v[j]), (uint32_t)f) : 0ull;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            unsigned long long other = __shfl_xor_sync(0xffffffffu, k, o);
-            k = other > k ? other : k;
-          }
-          if (lane == 0) red[warp * 16 + j] = k;
-        }
+        for (int j = 0; j < 16; ++j)
+          kred[j * 129 + row] = fok ? argmax_key(q16(v[j]), (uint32_t)f) : 0ull;
         __syncthreads();
-        if (threadIdx.x < 16) {
-          const int tok = qb + threadIdx.x;
-          unsigned long long k = red[threadIdx.x];
+        const int j = threadIdx.x >> 3, part = threadIdx.x & 7;
+        unsigned long long best = 0ull;
 #pragma unroll
-          for (int w = 1; w < 4; ++w) k = red[w * 16 + threadIdx.x] > k ? red[w * 16 + threadIdx.x] : k;
-          if (tok < p.m_tok) atomicMax(&p.keys[tok], k);
+        for (int r = 0; r < 16; ++r) {
+          const unsigned long long k = kred[j * 129 + part * 16 + r];
+          best = k > best ? k : best;
         }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+          best = other > best ? other : best;
+        }
+        const int tok = qb + j;
+        if (part == 0 && tok < p.m_tok) atomicMax(&p.keys[tok], best);
         __syncthreads();
       }
     }
@@ -378,7 +382,7 @@ __global__ void __launch_bounds__(128, 1)
   if (p.splits == 1) {
     for (int c = 0; c < bn; c += 16) {
       tmem_ld16(trow + (uint32_t)c, v);
-      epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, red);
+      epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, reinterpret_cast<unsigned long long*>(smem));
     }
   } else {
     // Split-K across the CTAs of one thread-block cluster (grid.z == cluster.z

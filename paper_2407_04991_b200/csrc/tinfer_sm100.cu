@@ -216,6 +216,9 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
   const size_t ln_bytes = (p.swap && d.ln_x) ? gemm_ln_bytes(p.bn, kb_per) : 0;
   int st = (int)((kMaxSmem - 4096 - ln_bytes) / stage_bytes);
   if (st > 8) st = 8;
+  // many independent full-K tiles (lm_head): a shallow ring lets 3 CTAs share
+  // an SM so one CTA's epilogue overlaps the others' weight streaming
+  if (p.swap && p.splits == 1 && p.tiles_a * p.tiles_b > 148 && st > 3) st = 3;
   if (st > kb_per) st = kb_per;
   if (st < 1) st = 1;
   p.stages = st;
