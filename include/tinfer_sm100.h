@@ -153,8 +153,9 @@ typedef struct tf_session_desc {
   void* x; void* h; void* q; void* attn; /* [batch*max_tokens, ldk_h] f16 */
   void* ffn;                             /* [batch*max_tokens, ldk_f] f16 */
   void* logits;                          /* optional [batch*max_tokens, vocab] f16 */
-  float* workspace; size_t workspace_bytes;
-  int* counters; int n_counters;
+  float* workspace; size_t workspace_bytes; /* split-KV decode attention partials:
+                                             * batch*heads*ceil(capacity/64)*66 floats */
+  int* counters; int n_counters;         /* batch*heads zeroed arrival counters */
   unsigned long long* keys;              /* [batch] argmax keys (zeroed) */
   int* len_dev; int* step_dev;           /* device scalars */
   int* out_tokens;                       /* [batch, max_new] */

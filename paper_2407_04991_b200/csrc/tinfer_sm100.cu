@@ -4,6 +4,7 @@
 // entry point replaces.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -402,8 +403,10 @@ void run_ln(const LnArgs& a, cudaStream_t st, bool pdl) {
 
 void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
   TF_REQUIRE(a.D >= 1 && a.D <= 128, TF_ERR_UNSUPPORTED, "head_dim must be in [1, 128]");
-  if (a.T == 1) {
-    const size_t smem = (size_t)(a.D + a.cap + 2 * kDecThreads) * sizeof(float);
+  if (a.T == 1 && a.D == 64 && a.ws && a.cnt && a.max_chunks >= (a.cap + kSplitKeys - 1) / kSplitKeys) {
+    launch(attn_decode_split_kernel, dim3(a.max_chunks, a.NH, a.B), dim3(kSplitThreads), 0, st, pdl, a);
+  } else if (a.T == 1) {
+    const size_t smem = (size_t)(a.D + a.cap + std::max(2 * kDecThreads, kDecWarps * a.D)) * sizeof(float);
     TF_REQUIRE(smem <= kMaxSmem, TF_ERR_UNSUPPORTED, "cache capacity too large for decode kernel");
     static bool attr = false;
     if (!attr) {
@@ -579,6 +582,15 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     if (T == 1 && sd.beam_indir) {
       at.indir = sd.beam_indir;
       at.beam = sd.beam;
+    }
+    if (T == 1 && D == 64) {  // split-KV decode attention when the session provides scratch
+      const int chunks = (sd.capacity + kSplitKeys - 1) / kSplitKeys;
+      const size_t need = (size_t)B * NH * chunks * 66 * sizeof(float);
+      if (sd.workspace && sd.workspace_bytes >= need && sd.counters && sd.n_counters >= B * NH) {
+        at.ws = sd.workspace;
+        at.cnt = sd.counters;
+        at.max_chunks = chunks;
+      }
     }
     run_attention(at, st, pdl);
     ++launches;

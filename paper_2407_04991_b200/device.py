@@ -187,8 +187,12 @@ class Session:
         d.x, d.h, d.q, d.attn = self.x.data_ptr(), self.h.data_ptr(), self.q.data_ptr(), self.attn.data_ptr()
         d.ffn = self.ffn.data_ptr()
         d.logits = self.logits.data_ptr() if logits else None
-        d.workspace, d.workspace_bytes = dm.ws.data_ptr(), dm.ws_bytes
-        d.counters, d.n_counters = dm.counters.data_ptr(), dm.n_counters
+        # split-KV decode attention scratch: per (row, head, 64-slot chunk) {m, z, o[64]}
+        chunks = (capacity + 63) // 64
+        self.att_ws = torch.empty(max(1, batch * dm.NH * chunks * 66), dtype=torch.float32, device=dev)
+        self.att_cnt = torch.zeros(batch * dm.NH, dtype=torch.int32, device=dev)
+        d.workspace, d.workspace_bytes = self.att_ws.data_ptr(), self.att_ws.numel() * 4
+        d.counters, d.n_counters = self.att_cnt.data_ptr(), self.att_cnt.numel()
         d.keys = self.keys.data_ptr()
         d.len_dev, d.step_dev = self.len_dev.data_ptr(), self.step_dev.data_ptr()
         d.out_tokens = self.out_tokens.data_ptr()
