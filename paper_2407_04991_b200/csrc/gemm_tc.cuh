@@ -79,16 +79,19 @@ __host__ __device__ inline int gemm_tmem_cols(int bn) {
 __host__ __device__ inline int gemm_stage_bytes(int bn) { return kABytes + bn * kBK * 2; }
 // ring bytes: the pipeline stages, or the f32 partial tile of the cluster
 // split-K reduction if that is larger (it reuses the drained ring)
-__host__ __device__ inline size_t gemm_ring_bytes(int bn, int stages, int splits) {
+// (non-swap tiles also stage the output tile through it: 128 rows x (bn*4 + 16) B)
+__host__ __device__ inline size_t gemm_ring_bytes(int bn, int stages, int splits, bool swap) {
   size_t ring = (size_t)stages * gemm_stage_bytes(bn);
   size_t part = splits > 1 ? (size_t)kTileA * bn * 4 : 0;
-  return ring > part ? ring : part;
+  size_t out = swap ? 0 : (size_t)kTileA * (bn * 4 + 16);
+  ring = ring > part ? ring : part;
+  return ring > out ? ring : out;
 }
 __host__ __device__ inline size_t gemm_ln_bytes(int bn, int kb_per_split) {
   return (size_t)kb_per_split * bn * kBK * 2;
 }
-__host__ inline size_t gemm_smem_bytes(int bn, int stages, int splits, size_t ln_bytes = 0) {
-  return 1024 + gemm_ring_bytes(bn, stages, splits) + ln_bytes + (2 * stages + 1) * 8 + 16;
+__host__ inline size_t gemm_smem_bytes(int bn, int stages, int splits, bool swap, size_t ln_bytes = 0) {
+  return 1024 + gemm_ring_bytes(bn, stages, splits, swap) + ln_bytes + (2 * stages + 1) * 8 + 16;
 }
 
 // LN-fused B operand: 128 threads normalise the CTA's bn token rows over the full
@@ -267,6 +270,120 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& p, int ra, int qb, con
   }
 }
 
+// ---------------------------------------------------------------- non-swap (prefill) epilogue
+// Thread = output row, so direct stores would hit 32 rows per warp instruction.
+// Instead the tile is staged through the drained ring (row pitch padded by 16 B)
+// after the per-element math, then written out cooperatively: each thread moves
+// 16-byte chunks of one row (8 f16 / 4 f32), consecutive threads consecutive
+// chunks, with the residual read and the Q/K/V routing done per chunk.
+template <int MODE>
+__device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, int tile_b, uint32_t trow,
+                                                 uint8_t* stage) {
+  constexpr bool F32OUT = MODE == EPI_F32;
+  constexpr int ESZ = F32OUT ? 4 : 2;
+  const int bn = p.bn;
+  const int pitch = bn * ESZ + 16;
+  const int row = threadIdx.x;
+  const int tok = tile_a * kTileA + row;
+  float v[16];
+  for (int c = 0; c < bn; c += 16) {
+    tmem_ld16(trow + (uint32_t)c, v);
+    uint8_t* dst = stage + (size_t)row * pitch + (size_t)c * ESZ;
+    if constexpr (F32OUT) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(dst + 16 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+      float y[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int f = min(tile_b * bn + c + j, p.n_feat - 1);
+        if constexpr (MODE == EPI_BIAS || MODE == EPI_QKV) {
+          y[j] = __fadd_rn(v[j], p.bias[f]);
+        } else if constexpr (MODE == EPI_BIAS_GELU) {
+          y[j] = gelu_ref(__fadd_rn(v[j], p.bias[f]));
+        } else if constexpr (MODE == EPI_BIAS_RESID) {
+          y[j] = __fadd_rn(v[j], p.bias[f]);  // rounded to f16 here, residual added below
+        } else {  // EPI_LOGITS
+          y[j] = v[j];
+        }
+      }
+      *reinterpret_cast<uint4*>(dst) = pack8(y);
+      *reinterpret_cast<uint4*>(dst + 16) = pack8(y + 8);
+    }
+  }
+  __syncthreads();
+  const int cpr = bn * ESZ / 16;  // 16-byte chunks per row
+  const int epc = 16 / ESZ;       // elements per chunk
+  for (int idx = threadIdx.x; idx < kTileA * cpr; idx += 128) {
+    const int r = idx / cpr, ch = idx - r * cpr;
+    const int t = tile_a * kTileA + r;
+    const int f0 = tile_b * bn + ch * epc;
+    if (t >= p.m_tok || f0 >= p.n_feat) continue;
+    const uint4 val = *reinterpret_cast<const uint4*>(stage + (size_t)r * pitch + ch * 16);
+    const bool full = f0 + epc <= p.n_feat;
+    if constexpr (F32OUT) {
+      float* o = p.out_f32 + (size_t)t * p.ldo + f0;
+      const float* fv = reinterpret_cast<const float*>(&val);
+      if (full && (p.ldo % 4) == 0) {
+        *reinterpret_cast<uint4*>(o) = val;
+      } else {
+        for (int e = 0; e < epc && f0 + e < p.n_feat; ++e) o[e] = fv[e];
+      }
+    } else if constexpr (MODE == EPI_QKV) {
+      // 8 features never straddle a head (head_dim % 8 == 0) or a q/k/v boundary
+      const int which = f0 / p.H, rr = f0 - which * p.H;
+      __half* dst;
+      if (which == 0) {
+        dst = p.q_out + (size_t)t * p.ldq + rr;
+      } else {
+        const int b = t / p.T, tt = t - b * p.T;
+        const int head = rr / p.D, d = rr - head * p.D;
+        const int slot = *p.qbase_dev + tt;
+        dst = (which == 1 ? p.kc : p.vc) + (((size_t)b * p.NH + head) * p.cap + slot) * p.D + d;
+      }
+      if (full && (p.D % 8) == 0 && (p.ldq % 8) == 0) {
+        *reinterpret_cast<uint4*>(dst) = val;
+      } else {
+        const __half* hv = reinterpret_cast<const __half*>(&val);
+        for (int e = 0; e < epc && f0 + e < p.n_feat; ++e) {
+          const int fe = f0 + e, w2 = fe / p.H, r2 = fe - w2 * p.H;
+          if (w2 == 0) {
+            p.q_out[(size_t)t * p.ldq + r2] = hv[e];
+          } else {
+            const int b = t / p.T, tt = t - b * p.T;
+            const int head = r2 / p.D, d = r2 - head * p.D;
+            (w2 == 1 ? p.kc : p.vc)[(((size_t)b * p.NH + head) * p.cap + *p.qbase_dev + tt) * p.D + d] = hv[e];
+          }
+        }
+      }
+    } else {
+      __half* o = p.out + (size_t)t * p.ldo + f0;
+      uint4 res = val;
+      if constexpr (MODE == EPI_BIAS_RESID) {
+        const __half* rp = p.resid + (size_t)t * p.ldr + f0;
+        float a8[8], r8[8];
+        unpack8(val, a8);
+        if (full && (p.ldr % 8) == 0) {
+          unpack8(*reinterpret_cast<const uint4*>(rp), r8);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) r8[e] = f0 + e < p.n_feat ? __half2float(rp[e]) : 0.0f;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a8[e] = __fadd_rn(r8[e], a8[e]);
+        res = pack8(a8);
+      }
+      if (full && (p.ldo % 8) == 0) {
+        *reinterpret_cast<uint4*>(o) = res;
+      } else {
+        const __half* hv = reinterpret_cast<const __half*>(&res);
+        for (int e = 0; e < epc && f0 + e < p.n_feat; ++e) o[e] = hv[e];
+      }
+    }
+  }
+}
+
 // single-element epilogue for the split-K reduction path (A-tile row ra, Q row qb)
 template <int MODE, bool SWAP>
 __device__ __forceinline__ void epi_elem(const GemmArgs& p, int ra, int qb, float acc) {
@@ -285,7 +402,7 @@ __global__ void __launch_bounds__(128, 1)
   const int bn = p.bn, stages = p.stages;
   const int stage_bytes = gemm_stage_bytes(bn);
   const bool ln_mode = SWAP && p.ln_x != nullptr;
-  uint8_t* bln = smem + gemm_ring_bytes(bn, stages, p.splits);
+  uint8_t* bln = smem + gemm_ring_bytes(bn, stages, p.splits, SWAP);
   uint64_t* bars = reinterpret_cast<uint64_t*>(bln + (ln_mode ? gemm_ln_bytes(bn, p.kb_per_split) : 0));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 1);
   __shared__ unsigned long long red[64];
@@ -379,7 +496,9 @@ __global__ void __launch_bounds__(128, 1)
   const int ra = tile_a * kTileA + row;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   float v[16];
-  if (p.splits == 1) {
+  if (!SWAP && p.splits == 1 && (MODE != EPI_LOGITS || p.keys == nullptr)) {
+    epi_tile_nonswap<MODE>(p, tile_a, tile_b, tmem + (uint32_t)(warp * 32 << 16), smem);
+  } else if (p.splits == 1) {
     for (int c = 0; c < bn; c += 16) {
       tmem_ld16(trow + (uint32_t)c, v);
       epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, reinterpret_cast<unsigned long long*>(smem));

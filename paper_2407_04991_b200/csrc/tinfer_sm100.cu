@@ -216,6 +216,9 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
   const int stage_bytes = gemm_stage_bytes(p.bn);
   const size_t ln_bytes = (p.swap && d.ln_x) ? gemm_ln_bytes(p.bn, kb_per) : 0;
   int st = (int)((kMaxSmem - 4096 - ln_bytes) / stage_bytes);
+  if (!p.swap) {  // leave room for the staged output tile (smem-bytes check below)
+    while (st > 1 && gemm_smem_bytes(p.bn, st, p.splits, false) > kMaxSmem) --st;
+  }
   if (st > 8) st = 8;
   // many independent full-K tiles (lm_head): a shallow ring lets 3 CTAs share
   // an SM so one CTA's epilogue overlaps the others' weight streaming
@@ -233,7 +236,7 @@ void launch_gemm_t(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& 
   dim3 grid(p.tiles_a, p.tiles_b, p.splits);
   const size_t ln_bytes = (SWAP && d.ln_x) ? gemm_ln_bytes(p.bn, p.k_blocks / p.splits) : 0;
   launch_cluster(gemm_tc_kernel<MODE, SWAP>, grid, dim3(128),
-                 gemm_smem_bytes(p.bn, p.stages, p.splits, ln_bytes), st, d.pdl != 0, p.splits, ta, tb, args);
+                 gemm_smem_bytes(p.bn, p.stages, p.splits, SWAP, ln_bytes), st, d.pdl != 0, p.splits, ta, tb, args);
 }
 
 template <int MODE>
@@ -415,6 +418,8 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
       attr = true;
     }
     launch(attn_decode_kernel, dim3(a.NH, a.B), dim3(kDecThreads), smem, st, pdl, a);
+  } else if (a.D == 64 && a.ldq % 8 == 0 && a.ldo % 2 == 0) {
+    launch(attn_prefill_mma_kernel, dim3((a.T + kFaRows - 1) / kFaRows, a.NH, a.B), dim3(128), 0, st, pdl, a);
   } else {
     const size_t smem = (size_t)kPfRows * a.D * sizeof(float) + (size_t)2 * kPfKeys * (a.D + 1) * 2;
     launch(attn_prefill_kernel, dim3((a.T + kPfRows - 1) / kPfRows, a.NH, a.B), dim3(128), smem, st,

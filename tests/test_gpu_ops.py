@@ -30,6 +30,7 @@ def gelu_ref(x):
     (128, 256, 64, 0, 1), (256, 512, 768, 0, 1), (300, 200, 200, 0, 1),
     (4096, 768, 768, 0, 1), (32, 2304, 768, 1, 0), (32, 768, 3072, 1, 0),
     (7, 100, 70, 1, 1), (128, 1000, 256, 1, 4), (256, 768, 768, 1, 0), (16, 64, 32, 1, 1),
+    (512, 2304, 768, 0, 1), (4096, 3072, 768, 0, 1), (300, 1100, 192, 0, 1),  # bn = 256 tiles
 ])
 def test_gemm_f32_matches_torch(cuda_device, m, n, k, swap, splits):
     kp = ops.pad64(k)
