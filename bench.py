@@ -107,6 +107,28 @@ def make_prompts(V, w, rank):
     return out
 
 
+def ncu_traffic(kernel_tag="prof_lm_head"):
+    """dram__bytes_read + dram__bytes_write per launch of the dominant kernel from
+    the committed `ncu --set full` capture summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "r1_ncu_summary.md")
+    if not os.path.exists(path):
+        return None
+    text = open(path).read()
+    at = text.find(kernel_tag)
+    if at < 0:
+        return None
+    block = text[at:at + 2000]
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    for key in ("dram__bytes_read.sum = ", "dram__bytes_write.sum = "):
+        i = block.find(key)
+        if i < 0:
+            return None
+        val, unit = block[i + len(key):].split("\n", 1)[0].split()[:2]
+        total += float(val) * units.get(unit, 1)
+    return total
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -393,7 +415,9 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(st.h2d_bytes), "d2h_bytes_per_step": int(st.d2h_bytes)},
             "gpu_launches": int(run.launches() * args.steps),
             "roofline": {"bound": "hbm", "achieved": kern["gbs"], "peak": hbm_peak, "unit": "GB/s",
-                         "frac": kern["gbs"] / hbm_peak, "traffic": None, "kernel": kern["name"],
+                         "frac": kern["gbs"] / hbm_peak,
+                         "traffic": ncu_traffic() if args.workload == "c2" else None,
+                         "kernel": kern["name"],
                          "bytes_per_launch": kern["bytes"], "launch_us": kern["us"],
                          "peak_kind": peak_kind},
             "decode_step": {"us": t_step * 1e6, "algorithmic_bytes": float(np.mean(step_bytes)),

@@ -45,7 +45,7 @@ if __name__ == "__main__":
     if os.path.exists("gpurun_out/launches.csv"):
         parts += ["## Launch list of one bench step (`ncu --metrics gpu__time_duration.sum --clock-control none`)", "",
                   launches("gpurun_out/launches.csv"), ""]
-    for rep in sorted(p for p in os.listdir("gpurun_out") if p.endswith(".ncu-rep")):
+    for rep in sorted(p for p in os.listdir("gpurun_out") if p.startswith("prof_") and p.endswith(".ncu-rep")):
         parts += [f"## `ncu --set full` {rep}", "", full(os.path.join("gpurun_out", rep)), ""]
     open(dest, "w").write("\n".join(parts))
     print(dest)
