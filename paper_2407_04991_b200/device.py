@@ -206,6 +206,29 @@ class Session:
         self.handle = h
         self.len = 0  # host mirror of the device cache length
 
+    def set_remap(self, table):
+        """Install (or clear, table=None) the prompt-id remap applied by the
+        embedding kernel to prefill ids (int32 old id -> new id, -1 = dropped)."""
+        import numpy as np
+        if table is None:
+            if self.remap is not None:
+                self.desc.remap, self.desc.remap_n = None, 0
+                self.remap = None
+                self._push_desc()
+            return
+        t = torch.from_numpy(np.ascontiguousarray(table, dtype=np.int32)).to(self.k_cache.device)
+        self.remap = t
+        self.desc.remap, self.desc.remap_n, self.desc.unk_id = t.data_ptr(), t.numel(), 0
+        self._push_desc()
+
+    def _push_desc(self):
+        """Re-create the native session with the updated descriptor (buffers kept)."""
+        N.lib().tf_session_destroy(self.handle)
+        h = C.c_void_p()
+        N.check(N.lib().tf_session_create(self.dm.handle, C.byref(self.desc), C.byref(h)),
+                "tf_session_create")
+        self.handle = h
+
     # ------------------------------------------------------------------ steps
     @staticmethod
     def stream():

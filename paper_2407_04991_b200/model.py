@@ -540,7 +540,7 @@ LAST_STATS = GenerateStats()
 
 
 def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens: int,
-                          fused: bool = True) -> list[list[int]]:
+                          fused: bool = True, prompt_vocab_map=None) -> list[list[int]]:
     """KV-cached greedy generation for a group of prompts in lockstep.
 
     Prompts are left-padded; padded slots are masked out of attention. The whole
@@ -548,7 +548,13 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
     steps replayed from one CUDA graph, each feeding the previous step's
     in-kernel argmax; the host syncs once to read the tokens back. Sequences are
     cut after their first eos (done rows keep being fed, as in the reference,
-    model.py:656-661, so the cut is exact)."""
+    model.py:656-661, so the cut is exact).
+
+    ``prompt_vocab_map`` (a ``pruning.PrunedVocabMap``; extension, not in the
+    reference): the prompts are in the ORIGINAL vocabulary of a pruned model and
+    are remapped on the device by the embedding kernel (ids outside the kept set
+    become the model's unk id 0); returned prompts stay as given and
+    generated ids are in the pruned vocabulary."""
     import torch
 
     from . import _native as N
@@ -556,7 +562,17 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
     c = model.config
     if not prompts:
         return []
-    checked = _validate_prompts(c, prompts, max_new_tokens)
+    table = None
+    if prompt_vocab_map is not None:
+        table = prompt_vocab_map.remap_table()
+        for p in prompts:  # original-vocabulary ids: only the sign/length checks apply
+            if len(p) < 1 or any(int(t) < 0 for t in p):
+                raise VocabError("prompt ids must be non-negative and non-empty")
+            if len(p) + max_new_tokens > c.max_position:
+                raise PositionError("prompt + max_new_tokens exceeds max_position")
+        checked = [[int(t) for t in p] for p in prompts]
+    else:
+        checked = _validate_prompts(c, prompts, max_new_tokens)
     seqs = [list(p) for p in checked]
     if max_new_tokens == 0:
         return seqs
@@ -567,6 +583,7 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
     stats = GenerateStats()
     with dm.lock, torch.cuda.device(dm.device):
         s = dm.session(B, cap, max_tokens, max_new_tokens)
+        s.set_remap(table)
         stats.h2d_bytes = s.load_inputs(ids, pos, pads)
         n_pre = s.forward(L, N.FWD_ARGMAX)
         n_dec = s.decode(max_new_tokens - 1)
