@@ -205,6 +205,14 @@ int tf_beam_decode(void* session, const tf_beam_desc* d, int n_steps, int use_gr
  * reports the session's task counts and copies the plan (int4 per task). */
 int tf_debug_mk_trace(void* session, void* trace_buf, int* n_items, int* n_aux, void* plan_out);
 
+/* Diagnostics (host env TF_TRACE=1): kernels launched after a reset store
+ * %globaltimer stamps of up to 8 points per CTA; reset != 0 clears them,
+ * otherwise copies [slot][2048 CTAs][8] u64 (0 = absent; 0 = entry, 1 = past the
+ * PDL wait, 7 = exit, the rest kernel-specific) for up to max_slots slots into
+ * dst and their kernel names into names; returns the slot count (>= 0) or a
+ * negative tf_status. */
+int tf_debug_trace(int reset, unsigned long long* dst, int max_slots, const char** names);
+
 /* Kernels launched by one decode step (for the bench's gpu_launches count). */
 int tf_session_launches_per_step(void* session);
 

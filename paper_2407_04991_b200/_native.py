@@ -128,6 +128,7 @@ SIGNATURES = {
     "tf_beam_select": (C.c_int, [C.c_void_p, C.POINTER(BeamDesc), C.c_void_p]),
     "tf_beam_decode": (C.c_int, [C.c_void_p, C.POINTER(BeamDesc), C.c_int, C.c_int, C.c_void_p]),
     "tf_debug_mk_trace": (C.c_int, [C.c_void_p, C.c_void_p, c_int_p, c_int_p, C.c_void_p]),
+    "tf_debug_trace": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
     "tf_session_launches_per_step": (C.c_int, [C.c_void_p]),
 }
 

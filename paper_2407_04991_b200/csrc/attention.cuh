@@ -37,7 +37,17 @@ struct AttnArgs {
   float* ws;
   int* cnt;
   int max_chunks;
+  int group;  // decode prefetch kernel: 64-slot chunks per CTA
+  int trace;  // diagnostics slot (0 = off)
 };
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
 
 // ------------------------------------------------------------------ decode
 // blockDim = kDecThreads. Dynamic smem: (D + cap + max(2 * kDecThreads, kDecWarps * D)) floats.
@@ -215,7 +225,10 @@ constexpr int kSplitThreads = 128;
 __global__ void __launch_bounds__(kSplitThreads) attn_decode_split_kernel(const AttnArgs a) {
   __shared__ float qs[64], sc[kSplitKeys], red[4 * 64 + 8];
   __shared__ int s_last;
+  TF_TRACE_INIT(tr);
+  if (threadIdx.x == 0) tr.mark(a.trace, 0);
   pdl_wait();
+  if (threadIdx.x == 0) tr.mark(a.trace, 1);
   pdl_trigger();
   constexpr int D = 64;
   const int c = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -328,11 +341,18 @@ __global__ void __launch_bounds__(kSplitThreads) attn_decode_split_kernel(const 
   __threadfence();
   __syncthreads();
   if (tid == 0) {
+    tr.mark(a.trace, 3);
     const int prev = atomicAdd(a.cnt + (size_t)b * a.NH + h, 1);
     s_last = (prev == nch - 1);
   }
   __syncthreads();
-  if (!s_last) return;
+  if (!s_last) {
+    if (tid == 0) {
+      tr.mark(a.trace, 4);
+      tr.flush(a.trace);
+    }
+    return;
+  }
   __threadfence();
   // merge in chunk order: M = max m_c, Z = sum z_c e^(m_c - M), O = sum o_c e^(m_c - M)
   if (tid < D) {
@@ -346,7 +366,219 @@ __global__ void __launch_bounds__(kSplitThreads) attn_decode_split_kernel(const 
     }
     orow[tid] = f16_sat(__fdiv_rn(O, Z));
   }
-  if (tid == 0) a.cnt[(size_t)b * a.NH + h] = 0;  // ready for the next launch / replay
+  if (tid == 0) {
+    a.cnt[(size_t)b * a.NH + h] = 0;  // ready for the next launch / replay
+    tr.mark(a.trace, 7);
+    tr.flush(a.trace);
+  }
+}
+
+
+// ------------------------------------------------------------------ decode, prefetching
+// head_dim 64. CTA (g, h, b) owns chunks [g*G, g*G+G) of the 64-slot chunks of
+// row b's window [start_b, len] (aligned to start_b, as in the split kernel).
+// Every slot but the newest (slot len, written by the QKV GEMM this step) is
+// already in the cache, so the CTA copies its chunks' K/V into shared memory
+// with cp.async BEFORE griddepcontrol.wait: the KV stream overlaps the QKV GEMM
+// instead of following it. After the wait it loads only q and the newest slot.
+// Per-chunk arithmetic and the fixed-order merge are those of
+// attn_decode_split_kernel, so the result does not depend on G (a function of
+// the session capacity) or on the batch. When one CTA owns the whole window
+// the merge is local; otherwise partials go to the workspace and the
+// last-arriving CTA merges them.
+constexpr int kPfKeysPerChunk = 64, kPfChunkBytes = 2 * 64 * 64 * 2;  // K + V, f16
+__host__ __device__ inline size_t attn_pf_smem_bytes(int G) {
+  return (size_t)G * kPfChunkBytes + (size_t)G * 66 * sizeof(float);
+}
+
+__global__ void __launch_bounds__(128) attn_decode_pf_kernel(const AttnArgs a) {
+  extern __shared__ __align__(128) uint8_t pf_smem[];
+  __shared__ __align__(16) float qs[64];
+  __shared__ float sc_all[4 * 64];
+  __shared__ int s_last;
+  constexpr int D = 64;
+  TF_TRACE_INIT(tr);
+  if (threadIdx.x == 0) tr.mark(a.trace, 0);
+  const int G = a.group;
+  __half* kvs = reinterpret_cast<__half*>(pf_smem);                           // [G][K|V][64][64]
+  float* part_s = reinterpret_cast<float*>(pf_smem + (size_t)G * kPfChunkBytes);  // [G][66]
+  const int g = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // the cache length and left pad were written by earlier steps (complete)
+  const int qbase = *a.qbase_dev;
+  const int lo = a.start[b], hi = qbase;  // window [lo, hi]
+  const int n = hi - lo + 1;
+  const int nch = n > 0 ? (n + 63) / 64 : 0;
+  const int ngr = (nch + G - 1) / G;
+  if (g >= (ngr > 0 ? ngr : 1)) {
+    pdl_trigger();
+    return;
+  }
+  const int c0 = g * G, nc = n > 0 ? min(G, nch - c0) : 0;
+  const size_t row_stride = (size_t)a.NH * a.cap * D, head_stride = (size_t)a.cap * D;
+  const int* ind = a.indir ? a.indir + (size_t)b * a.cap : nullptr;
+  const int beam0 = a.indir ? (b / a.beam) * a.beam : b;
+  auto kv_off = [&](int s) -> size_t {
+    const int src = ind ? beam0 + ind[s] : b;
+    return (size_t)src * row_stride + (size_t)h * head_stride + (size_t)s * D;
+  };
+  // ---- before the wait: K/V of every slot < hi in this CTA's chunks
+  for (int seg = tid; seg < nc * 64 * 8; seg += 128) {
+    const int i = seg >> 9, j = (seg >> 3) & 63, part = seg & 7;
+    const int slot = lo + (c0 + i) * 64 + j;
+    if (slot != hi) {  // slots past the window are zero-filled (src-size 0)
+      const bool ok = slot < hi;
+      const size_t off = ok ? kv_off(slot) + part * 8 : 0;
+      __half* kd = kvs + ((size_t)(2 * i) * 64 + j) * 64 + part * 8;
+      __half* vd = kvs + ((size_t)(2 * i + 1) * 64 + j) * 64 + part * 8;
+      cp_async16(smem_u32(kd), a.kc + off, ok);
+      cp_async16(smem_u32(vd), a.vc + off, ok);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) tr.mark(a.trace, 1);
+  __half* orow = a.out + (size_t)b * a.ldo + (size_t)h * D;
+  if (n <= 0) {  // empty window: zeros
+    if (tid < D) orow[tid] = __float2half_rn(0.0f);
+    return;
+  }
+  // ---- after the wait: q and the newest slot
+  if (tid < D) qs[tid] = __half2float(a.q[(size_t)b * a.ldq + (size_t)h * D + tid]);
+  {
+    const int i = (hi - lo) / 64 - c0, j = (hi - lo) % 64;
+    if (i >= 0 && i < nc && tid < 16) {
+      const int part = tid & 7;
+      const size_t off = kv_off(hi) + part * 8;
+      const __half* src = (tid < 8 ? a.kc : a.vc) + off;
+      __half* dst = kvs + ((size_t)(2 * i + (tid < 8 ? 0 : 1)) * 64 + j) * 64 + part * 8;
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+    }
+  }
+  cp_async_commit_wait_all();
+  __syncthreads();
+  if (threadIdx.x == 0) tr.mark(a.trace, 2);
+  const long long clk0 = clock64();
+  // scores: one thread per key. Thread reads its K row in 16-B segments in
+  // the order (s + key) & 7, so the 8 threads of each LDS.128 phase hit
+  // distinct bank groups; 8 independent partial dot products, summed in that
+  // order (fixed by the key's position in its chunk -> batch-invariant)
+  const int n_keys = min(nc * 64, n - c0 * 64);
+  for (int key = tid; key < n_keys; key += 128) {
+    const int i = key >> 6, j = key & 63;
+    const __half* kr = kvs + ((size_t)(2 * i) * 64 + j) * 64;
+    float ps[8];
+#pragma unroll
+    for (int s8 = 0; s8 < 8; ++s8) {
+      const int seg = (s8 + j) & 7;
+      float kf[8];
+      unpack8(*reinterpret_cast<const uint4*>(kr + seg * 8), kf);
+      const float4 qa = *reinterpret_cast<const float4*>(qs + seg * 8);
+      const float4 qb = *reinterpret_cast<const float4*>(qs + seg * 8 + 4);
+      float acc = __fmul_rn(qa.x, kf[0]);
+      acc = __fadd_rn(acc, __fmul_rn(qa.y, kf[1]));
+      acc = __fadd_rn(acc, __fmul_rn(qa.z, kf[2]));
+      acc = __fadd_rn(acc, __fmul_rn(qa.w, kf[3]));
+      acc = __fadd_rn(acc, __fmul_rn(qb.x, kf[4]));
+      acc = __fadd_rn(acc, __fmul_rn(qb.y, kf[5]));
+      acc = __fadd_rn(acc, __fmul_rn(qb.z, kf[6]));
+      acc = __fadd_rn(acc, __fmul_rn(qb.w, kf[7]));
+      ps[s8] = acc;
+    }
+    const float d = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
+                              __fadd_rn(__fadd_rn(ps[4], ps[5]), __fadd_rn(ps[6], ps[7])));
+    sc_all[key] = __fmul_rn(d, a.scale);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tr.mark(a.trace, 4);
+    if (a.trace > 0) tr.t[6] = (unsigned long long)(clock64() - clk0);
+  }
+  // one warp per chunk: chunk max / exp / sum, then o = sum_j e_j v_j with
+  // each lane owning dims (2 lane, 2 lane + 1), keys in order
+  for (int i = warp; i < nc; i += 4) {
+    const int cnt_keys = min(64, n - (c0 + i) * 64);
+    float* sci = sc_all + i * 64;
+    const float s0 = lane < cnt_keys ? sci[lane] : -INFINITY;
+    const float s1 = lane + 32 < cnt_keys ? sci[lane + 32] : -INFINITY;
+    const float m = warp_max(fmaxf(s0, s1));
+    const float e0 = lane < cnt_keys ? expf(__fsub_rn(s0, m)) : 0.0f;
+    const float e1 = lane + 32 < cnt_keys ? expf(__fsub_rn(s1, m)) : 0.0f;
+    const float z = warp_sum(__fadd_rn(e0, e1));
+    sci[lane] = e0;
+    sci[lane + 32] = e1;
+    __syncwarp();
+    const __half* Vs = kvs + (size_t)(2 * i + 1) * 64 * 64;
+    // 4 independent accumulators (keys j % 4), combined pairwise; e_j = 0
+    // past cnt_keys, so the loop runs the whole chunk
+    float o0[4] = {0.f, 0.f, 0.f, 0.f}, o1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int j = 0; j < 64; j += 4) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float2 v = __half22float2(*reinterpret_cast<const __half2*>(Vs + (j + r) * 64 + 2 * lane));
+        const float w = sci[j + r];
+        o0[r] = __fadd_rn(o0[r], __fmul_rn(w, v.x));
+        o1[r] = __fadd_rn(o1[r], __fmul_rn(w, v.y));
+      }
+    }
+    part_s[i * 66 + 2 + 2 * lane] = __fadd_rn(__fadd_rn(o0[0], o0[1]), __fadd_rn(o0[2], o0[3]));
+    part_s[i * 66 + 3 + 2 * lane] = __fadd_rn(__fadd_rn(o1[0], o1[1]), __fadd_rn(o1[2], o1[3]));
+    if (lane == 0) {
+      part_s[i * 66] = m;
+      part_s[i * 66 + 1] = z;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) tr.mark(a.trace, 5);
+  if (threadIdx.x == 0) tr.mark(a.trace, 3);
+  // merge in chunk order: M = max m_c, Z = sum z_c e^(m_c - M), O = sum o_c e^(m_c - M)
+  auto merge = [&](const float* P, int count) {
+    if (tid < D) {
+      float M = -INFINITY;
+      for (int cc = 0; cc < count; ++cc) M = fmaxf(M, P[(size_t)cc * 66]);
+      float Z = 0.0f, O = 0.0f;
+      for (int cc = 0; cc < count; ++cc) {
+        const float f = expf(__fsub_rn(P[(size_t)cc * 66], M));
+        Z = __fadd_rn(Z, __fmul_rn(P[(size_t)cc * 66 + 1], f));
+        O = __fadd_rn(O, __fmul_rn(P[(size_t)cc * 66 + 2 + tid], f));
+      }
+      orow[tid] = f16_sat(__fdiv_rn(O, Z));
+    }
+  };
+  if (ngr == 1) {
+    merge(part_s, nch);
+  } else {
+    float* part = a.ws + (((size_t)b * a.NH + h) * a.max_chunks) * 66;
+    for (int e = tid; e < nc * 66; e += 128) __stcg(part + (size_t)c0 * 66 + e, part_s[e]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const int prev = atomicAdd(a.cnt + (size_t)b * a.NH + h, 1);
+      s_last = (prev == ngr - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      if (tid < D) {
+        float M = -INFINITY;
+        for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(part + (size_t)cc * 66));
+        float Z = 0.0f, O = 0.0f;
+        for (int cc = 0; cc < nch; ++cc) {
+          const float f = expf(__fsub_rn(__ldcg(part + (size_t)cc * 66), M));
+          Z = __fadd_rn(Z, __fmul_rn(__ldcg(part + (size_t)cc * 66 + 1), f));
+          O = __fadd_rn(O, __fmul_rn(__ldcg(part + (size_t)cc * 66 + 2 + tid), f));
+        }
+        orow[tid] = f16_sat(__fdiv_rn(O, Z));
+      }
+      if (tid == 0) a.cnt[(size_t)b * a.NH + h] = 0;
+    }
+  }
+  if (threadIdx.x == 0) {
+    tr.mark(a.trace, 7);
+    tr.flush(a.trace);
+  }
 }
 
 // ------------------------------------------------------------------ prefill, tensor cores
@@ -378,10 +610,6 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
 __device__ __forceinline__ uint32_t pack_h2(float x, float y) {
   __half2 h = __floats2half2_rn(x, y);
   return *reinterpret_cast<uint32_t*>(&h);
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
-               : "memory");
 }
 
 __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const AttnArgs a) {

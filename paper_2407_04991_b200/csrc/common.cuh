@@ -42,6 +42,33 @@ __device__ __forceinline__ uint32_t argmax_id(unsigned long long key) {
   return 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull);
 }
 
+// ---------------------------------------------------------------- tracing
+// Diagnostics only (TF_TRACE=1 on the host): kernels launched with a non-zero
+// trace slot keep %globaltimer stamps in registers (TraceRec::mark) and store
+// them once per CTA at exit (flush); the host reduces over CTAs. Points are
+// kernel-specific; all kernels use 0 = entry, 1 = past griddepcontrol.wait,
+// 7 = exit.
+constexpr int kTraceSlots = 256, kTraceCtas = 2048;
+// [slot][cta][8] stamps (plain stores, no same-address atomics), 0 = absent
+__device__ unsigned long long* g_trace_buf;
+struct TraceRec {
+  unsigned long long t[8];
+  __device__ __forceinline__ void mark(int tr, int i) {
+    if (tr > 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t[i]));
+  }
+  __device__ __forceinline__ void flush(int tr) {
+    const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (tr > 0 && g_trace_buf != nullptr && cta < (unsigned)kTraceCtas) {
+      unsigned long long* p = g_trace_buf + ((size_t)(tr - 1) * kTraceCtas + cta) * 8;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) p[i] = t[i];
+    }
+  }
+};
+#define TF_TRACE_INIT(rec) \
+  TraceRec rec;           \
+  _Pragma("unroll") for (int _i = 0; _i < 8; ++_i) rec.t[_i] = 0ull
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -194,6 +221,39 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+// bulk copy shared::cta -> shared::cluster (a peer CTA's smem), completing
+// `bytes` transaction bytes on the peer's mbarrier
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
+                                                  uint32_t mbar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_cluster),
+      "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// non-.aligned forms: threads of a warp may reach them at different points
+__device__ __forceinline__ void cluster_arrive_any() {
+  asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_any() {
+  asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+}
 // address of the same smem offset in CTA `rank` of this cluster
 __device__ __forceinline__ uint32_t dsmem_addr(uint32_t local_smem, uint32_t rank) {
   uint32_t r;
@@ -205,6 +265,12 @@ __device__ __forceinline__ uint32_t dsmem_addr(uint32_t local_smem, uint32_t ran
 __device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
   float v;
   asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ float4 ld_dsmem_f32x4(uint32_t addr) {
+  float4 v;
+  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
 

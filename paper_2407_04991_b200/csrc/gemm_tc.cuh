@@ -67,6 +67,7 @@ struct GemmArgs {
   int ln_ldx, ln_src_stride, ln_src_off, ln_H;
   const float* ln_g;
   const float* ln_b;
+  int trace;  // diagnostics slot (0 = off)
 };
 
 constexpr int kTileA = 128;          // MMA M
@@ -90,8 +91,19 @@ __host__ __device__ inline size_t gemm_ring_bytes(int bn, int stages, int splits
 __host__ __device__ inline size_t gemm_ln_bytes(int bn, int kb_per_split) {
   return (size_t)kb_per_split * bn * kBK * 2;
 }
+// push-based split-K reduction (SWAP, splits > 1, bn <= 128): every CTA owns a
+// receive buffer for the S-1 peer slices of its 1/S share of the tile
+__host__ __device__ inline bool gemm_push_reduce(int bn, int splits, bool swap) {
+  return swap && splits > 1 && bn <= 128;
+}
+__host__ __device__ inline size_t gemm_recv_bytes(int bn, int splits, bool swap) {
+  if (!gemm_push_reduce(bn, splits, swap)) return 0;
+  const int U = (kTileA / 4) * bn, per = (U + splits - 1) / splits;
+  return (size_t)splits * per * 16;
+}
 __host__ inline size_t gemm_smem_bytes(int bn, int stages, int splits, bool swap, size_t ln_bytes = 0) {
-  return 1024 + gemm_ring_bytes(bn, stages, splits, swap) + ln_bytes + (2 * stages + 1) * 8 + 16;
+  return 1024 + gemm_ring_bytes(bn, stages, splits, swap) + ln_bytes + gemm_recv_bytes(bn, splits, swap) +
+         (2 * stages + 2) * 8 + 16;
 }
 
 // LN-fused B operand: 128 threads normalise the CTA's bn token rows over the full
@@ -384,12 +396,106 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
   }
 }
 
-// single-element epilogue for the split-K reduction path (A-tile row ra, Q row qb)
+// ---- split-K reduction epilogue, 4 rows of one tile column per unit.
+// Unit u of tile (tile_a, tile_b): column u / 32, rows 4 * (u % 32) .. +3.
+// SWAP: rows are features, the column is a token; otherwise the reverse.
+struct EpiPre4 {
+  float b[4];  // bias
+  float x[4];  // residual
+};
+
+template <bool SWAP>
+__device__ __forceinline__ void unit_coords(int tile_a, int tile_b, int bn, int u, int& tok, int& f, int& step) {
+  const int col = tile_b * bn + u / 32, r = tile_a * kTileA + (u % 32) * 4;
+  tok = SWAP ? col : r;
+  f = SWAP ? r : col;
+  step = SWAP ? 1 : 0;  // the 4 rows advance the feature (SWAP) or the token
+}
+
 template <int MODE, bool SWAP>
-__device__ __forceinline__ void epi_elem(const GemmArgs& p, int ra, int qb, float acc) {
-  const int tok = SWAP ? qb : ra;
-  const int f = SWAP ? ra : qb;
-  if (tok < p.m_tok && f < p.n_feat) epi_store<MODE, SWAP>(p, tok, f, acc);
+__device__ __forceinline__ void epi_pre4(const GemmArgs& p, int tile_a, int tile_b, int u, EpiPre4& q) {
+  int tok, f, st;
+  unit_coords<SWAP>(tile_a, tile_b, p.bn, u, tok, f, st);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int tj = tok + (st ? 0 : j), fj = f + (st ? j : 0);
+    const bool ok = tj < p.m_tok && fj < p.n_feat;
+    if constexpr (MODE == EPI_BIAS || MODE == EPI_BIAS_GELU || MODE == EPI_BIAS_RESID || MODE == EPI_QKV)
+      q.b[j] = ok ? p.bias[fj] : 0.0f;
+    if constexpr (MODE == EPI_BIAS_RESID)
+      q.x[j] = ok ? __half2float(p.resid[(size_t)tj * p.ldr + fj]) : 0.0f;
+  }
+}
+
+template <int MODE, bool SWAP>
+__device__ __forceinline__ void epi_fin4(const GemmArgs& p, int tile_a, int tile_b, int u, const float (&acc)[4],
+                                         const EpiPre4& q) {
+  int tok, f, st;
+  unit_coords<SWAP>(tile_a, tile_b, p.bn, u, tok, f, st);
+  if constexpr (MODE == EPI_F32) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int tj = tok + (st ? 0 : j), fj = f + (st ? j : 0);
+      if (tj < p.m_tok && fj < p.n_feat) p.out_f32[(size_t)tj * p.ldo + fj] = acc[j];
+    }
+    return;
+  }
+  __half val[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if constexpr (MODE == EPI_BIAS || MODE == EPI_QKV) {
+      val[j] = f16_sat(__fadd_rn(acc[j], q.b[j]));
+    } else if constexpr (MODE == EPI_BIAS_GELU) {
+      val[j] = f16_sat(gelu_ref(__fadd_rn(acc[j], q.b[j])));
+    } else if constexpr (MODE == EPI_BIAS_RESID) {
+      val[j] = f16_sat(__fadd_rn(q.x[j], q16(__fadd_rn(acc[j], q.b[j]))));
+    } else {
+      val[j] = f16_sat(acc[j]);
+    }
+  }
+  // destination of the 4 values: contiguous when they run along features
+  __half* dst = nullptr;
+  if constexpr (MODE == EPI_QKV) {
+    if (st && tok < p.m_tok && f + 3 < p.n_feat && p.H % 4 == 0 && p.D % 4 == 0) {
+      const int which = f / p.H, r = f - which * p.H;
+      if (which == 0) {
+        dst = p.q_out + (size_t)tok * p.ldq + r;
+      } else {
+        const int b = tok / p.T, t = tok - b * p.T;
+        const int head = r / p.D, d = r - head * p.D;
+        const int slot = *p.qbase_dev + t;
+        dst = (which == 1 ? p.kc : p.vc) + (((size_t)b * p.NH + head) * p.cap + slot) * p.D + d;
+      }
+    }
+  } else {
+    if (st && tok < p.m_tok && f + 3 < p.n_feat && p.out) dst = p.out + (size_t)tok * p.ldo + f;
+  }
+  if (dst != nullptr && (reinterpret_cast<uintptr_t>(dst) & 7u) == 0) {
+    __half2 lo = __halves2half2(val[0], val[1]), hi = __halves2half2(val[2], val[3]);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t*>(&lo);
+    w.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(dst) = w;
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int tj = tok + (st ? 0 : j), fj = f + (st ? j : 0);
+    if (tj >= p.m_tok || fj >= p.n_feat) continue;
+    if constexpr (MODE == EPI_QKV) {
+      const int which = fj / p.H, r = fj - which * p.H;
+      if (which == 0) {
+        p.q_out[(size_t)tj * p.ldq + r] = val[j];
+      } else {
+        const int b = tj / p.T, t = tj - b * p.T;
+        const int head = r / p.D, d = r - head * p.D;
+        const int slot = *p.qbase_dev + t;
+        (which == 1 ? p.kc : p.vc)[(((size_t)b * p.NH + head) * p.cap + slot) * p.D + d] = val[j];
+      }
+    } else if (p.out) {
+      p.out[(size_t)tj * p.ldo + fj] = val[j];
+    }
+  }
 }
 
 template <int MODE, bool SWAP>
@@ -403,8 +509,10 @@ __global__ void __launch_bounds__(128, 1)
   const int stage_bytes = gemm_stage_bytes(bn);
   const bool ln_mode = SWAP && p.ln_x != nullptr;
   uint8_t* bln = smem + gemm_ring_bytes(bn, stages, p.splits, SWAP);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bln + (ln_mode ? gemm_ln_bytes(bn, p.kb_per_split) : 0));
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 1);
+  uint8_t* recv = bln + (ln_mode ? gemm_ln_bytes(bn, p.kb_per_split) : 0);
+  const bool push = gemm_push_reduce(bn, p.splits, SWAP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(recv + gemm_recv_bytes(bn, p.splits, SWAP));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 2);
   __shared__ unsigned long long red[64];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -412,8 +520,10 @@ __global__ void __launch_bounds__(128, 1)
   const int kb0 = split * p.kb_per_split;
   const int nkb = min(p.kb_per_split, p.k_blocks - kb0);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + stages),
-                 done_bar = smem_u32(bars + 2 * stages);
+                 done_bar = smem_u32(bars + 2 * stages), recv_bar = smem_u32(bars + 2 * stages + 1);
   const uint32_t ncols = (uint32_t)gemm_tmem_cols(bn);
+  TF_TRACE_INIT(tr);
+  if (threadIdx.x == 0) tr.mark(p.trace, 0);
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmA);
@@ -423,12 +533,16 @@ __global__ void __launch_bounds__(128, 1)
       mbar_init(empty0 + 8 * s, 1);
     }
     mbar_init(done_bar, 1);
+    mbar_init(recv_bar, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(smem_u32(tmem_slot), ncols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // push reduction: peers may signal this CTA's recv_bar only after it is
+  // initialised; the matching wait sits right before the first push
+  if (push) cluster_arrive_relaxed();
   const uint32_t tmem = *tmem_slot;
   // let the next kernel in the stream launch now: its prologue (barrier init,
   // TMEM alloc, weight TMA prefetch) overlaps this kernel; it still waits on
@@ -454,6 +568,7 @@ __global__ void __launch_bounds__(128, 1)
   }
   if (warp == 0 && lane == 0) {
     if (!ln_mode) pdl_wait();
+    tr.mark(p.trace, 1);
     for (int i = 0; i < nkb; ++i) {
       const int s = i % stages;
       const uint32_t ph = (uint32_t)(i / stages) & 1u;
@@ -492,6 +607,7 @@ __global__ void __launch_bounds__(128, 1)
   pdl_wait();
   mbar_wait(done_bar, 0);
   tc_fence_after();
+  if (threadIdx.x == 0) tr.mark(p.trace, 2);
   const int row = warp * 32 + lane;  // TMEM lane == row of the A tile
   const int ra = tile_a * kTileA + row;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
@@ -502,6 +618,69 @@ __global__ void __launch_bounds__(128, 1)
     for (int c = 0; c < bn; c += 16) {
       tmem_ld16(trow + (uint32_t)c, v);
       epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, reinterpret_cast<unsigned long long*>(smem));
+    }
+  } else if (push) {
+    // Split-K across the CTAs of one cluster, push form. Each CTA parks its f32
+    // partial tile ([column][128 rows], in the drained ring), then one thread
+    // bulk-copies the slice owned by every peer r (units [r*per, r*per+per),
+    // 16 B per unit) into r's receive buffer at row `rank`, completing bytes
+    // on r's recv_bar. Each CTA waits only for its own S-1 incoming slices and
+    // reduces them from local smem in split order 0..S-1 (deterministic; the
+    // same sums as the pull form). No cluster barrier on the data path; the
+    // CTA only waits for its outgoing copies to finish reading before exit.
+    float* part = reinterpret_cast<float*>(smem);
+    for (int c = 0; c < bn; c += 16) {
+      tmem_ld16(trow + (uint32_t)c, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) part[(c + j) * kTileA + row] = v[j];
+    }
+    fence_proxy_async_smem();  // generic smem writes -> visible to the bulk-copy engine
+    const uint32_t rank = cluster_ctarank();
+    const int S = p.splits;
+    const int U = (kTileA / 4) * bn;
+    const int per = (U + S - 1) / S;
+    const int u_lo = (int)rank * per, u_hi = min(U, u_lo + per);
+    cluster_wait();  // every peer's recv_bar is initialised
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tr.mark(p.trace, 3);
+      const int mine = max(0, u_hi - u_lo);
+      mbar_expect_tx(recv_bar, (uint32_t)((S - 1) * mine * 16));
+      const uint32_t src0 = smem_u32(part), rcv0 = smem_u32(recv);
+      for (int r = 0; r < S; ++r) {
+        if (r == (int)rank) continue;
+        const int r_lo = r * per, r_n = min(U, r_lo + per) - r_lo;
+        if (r_n <= 0) continue;
+        bulk_copy_to_peer(dsmem_addr(rcv0 + (uint32_t)(rank * per * 16), (uint32_t)r),
+                          src0 + (uint32_t)(r_lo * 16), (uint32_t)(r_n * 16), dsmem_addr(recv_bar, (uint32_t)r));
+      }
+      bulk_commit();
+    }
+    EpiPre4 pre;
+    int u = u_lo + (int)threadIdx.x;
+    if (u < u_hi) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
+    mbar_wait(recv_bar, 0);
+    if (threadIdx.x == 0) tr.mark(p.trace, 4);
+    const float4* own = reinterpret_cast<const float4*>(part);
+    const float4* rin = reinterpret_cast<const float4*>(recv);
+    for (bool first = true; u < u_hi; u += 128, first = false) {
+      if (!first) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int sp = 0; sp < 16; ++sp)
+        if (sp < S) {
+          const float4 pv = sp == (int)rank ? own[u] : rin[sp * per + (u - u_lo)];
+          acc[0] = __fadd_rn(acc[0], pv.x);
+          acc[1] = __fadd_rn(acc[1], pv.y);
+          acc[2] = __fadd_rn(acc[2], pv.z);
+          acc[3] = __fadd_rn(acc[3], pv.w);
+        }
+      if (threadIdx.x == 0 && first) tr.mark(p.trace, 5);
+      epi_fin4<MODE, SWAP>(p, tile_a, tile_b, u, acc, pre);
+    }
+    if (threadIdx.x == 0) {
+      tr.mark(p.trace, 6);
+      bulk_wait_read_all();  // outgoing slices read before this smem is released
     }
   } else {
     // Split-K across the CTAs of one thread-block cluster (grid.z == cluster.z
@@ -515,30 +694,57 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
       for (int j = 0; j < 16; ++j) part[(c + j) * kTileA + row] = v[j];
     }
-    cluster_sync();
+    // Work unit = 4 adjacent rows of one column of the tile (16 B of every
+    // partial); CTA `rank` reduces a contiguous 1/S of the units. The epilogue
+    // operands of the first unit (bias, residual) are loaded before the
+    // cluster barrier so their latency overlaps the wait for the slowest split.
     const uint32_t rank = cluster_ctarank();
     const int S = p.splits;
-    const int E = kTileA * bn;
-    const int per = (E + S - 1) / S;
-    const int e_lo = (int)rank * per, e_hi = min(E, e_lo + per);
+    const int U = (kTileA / 4) * bn;
+    const int per = (U + S - 1) / S;
+    const int u_lo = (int)rank * per, u_hi = min(U, u_lo + per);
+    EpiPre4 pre;
+    int u = u_lo + (int)threadIdx.x;
+    if (threadIdx.x == 0) tr.mark(p.trace, 3);
+    cluster_arrive();  // release: this CTA's partial tile is complete
+    if (u < u_hi) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
+    cluster_wait();
+    if (threadIdx.x == 0) tr.mark(p.trace, 4);
     const uint32_t local = smem_u32(part);
-    for (int e = e_lo + threadIdx.x; e < e_hi; e += 128) {
+    // the last DSMEM read of this thread is followed by the arrive that lets the
+    // other CTAs exit; the epilogue stores of the last unit overlap that barrier
+    const int n_units = u < u_hi ? (u_hi - 1 - u) / 128 + 1 : 0;
+    int it = 0;
+    if (n_units == 0) cluster_arrive_any();
+    for (bool first = true; u < u_hi; u += 128, first = false, ++it) {
+      if (!first) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
       // all S loads in flight, then the sum in split order (deterministic)
-      float part_v[16];
+      float4 pv[16];
 #pragma unroll
       for (int sp = 0; sp < 16; ++sp)
-        part_v[sp] = sp < S ? ld_dsmem_f32(dsmem_addr(local + 4u * (uint32_t)e, (uint32_t)sp)) : 0.0f;
-      float acc = 0.0f;
+        if (sp < S) pv[sp] = ld_dsmem_f32x4(dsmem_addr(local + 16u * (uint32_t)u, (uint32_t)sp));
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
       for (int sp = 0; sp < 16; ++sp)
-        if (sp < S) acc = __fadd_rn(acc, part_v[sp]);
-      const int col = e / kTileA, r = e - col * kTileA;
-      epi_elem<MODE, SWAP>(p, tile_a * kTileA + r, tile_b * bn + col, acc);
+        if (sp < S) {
+          acc[0] = __fadd_rn(acc[0], pv[sp].x);
+          acc[1] = __fadd_rn(acc[1], pv[sp].y);
+          acc[2] = __fadd_rn(acc[2], pv[sp].z);
+          acc[3] = __fadd_rn(acc[3], pv[sp].w);
+        }
+      if (threadIdx.x == 0 && first) tr.mark(p.trace, 5);
+      if (it == n_units - 1) cluster_arrive_any();
+      epi_fin4<MODE, SWAP>(p, tile_a, tile_b, u, acc, pre);
     }
-    cluster_sync();  // partial tiles stay alive until every CTA has read them
+    if (threadIdx.x == 0) tr.mark(p.trace, 6);
+    cluster_wait_any();  // partial tiles stay alive until every CTA has read them
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) {
+    tr.mark(p.trace, 7);
+    tr.flush(p.trace);
+  }
   if (warp == 2) tmem_dealloc(tmem, ncols);
 }
 

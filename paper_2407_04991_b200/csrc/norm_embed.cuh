@@ -221,6 +221,7 @@ struct LnArgs {
   const float* b;
   __half* h;  // [n_rows, ldh]
   int ldh;
+  int trace;  // diagnostics slot (0 = off)
 };
 
 template <int VPL>
@@ -243,7 +244,10 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const LnArgs a) {
 
 template <int NC>
 __global__ void __launch_bounds__(256) layernorm_vec_kernel(const LnArgs a) {
+  TF_TRACE_INIT(tr);
+  if (threadIdx.x == 0) tr.mark(a.trace, 0);
   pdl_wait();
+  if (threadIdx.x == 0) tr.mark(a.trace, 1);
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp;
@@ -266,6 +270,13 @@ __global__ void __launch_bounds__(256) layernorm_vec_kernel(const LnArgs a) {
       }
     }
     ln_row_vec<NC>(xv, a.H, a.g, a.b, a.h + (size_t)row * a.ldh, lane);
+  }
+  if (a.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tr.mark(a.trace, 7);
+      tr.flush(a.trace);
+    }
   }
 }
 

@@ -140,6 +140,22 @@ int num_sms() {
   return g_num_sms;
 }
 
+// ------------------------------------------------------------------ tracing (diagnostics)
+bool trace_on() {
+  static const bool on = [] {
+    const char* e = getenv("TF_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+int g_trace_n = 0;
+const char* g_trace_names[kTraceSlots];
+int trace_next(const char* name) {
+  if (!trace_on() || g_trace_n >= kTraceSlots) return 0;
+  g_trace_names[g_trace_n] = name;
+  return ++g_trace_n;
+}
+
 // dynamic smem budget: 227 KB per CTA minus room for the kernels' static smem
 constexpr size_t kMaxSmem = 227 * 1024 - 1024;
 
@@ -200,6 +216,19 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
     p.splits = d.splits;
   } else {
     p.splits = (p.swap && d.epilogue != TF_EPI_LOGITS) ? pick_splits(p.tiles_a * p.tiles_b, p.k_blocks) : 1;
+    static const int kb_target = [] {  // diagnostics: TF_KB_PER=n -> fewest splits with <= n K-blocks each
+      const char* e = getenv("TF_KB_PER");
+      return e ? atoi(e) : 0;
+    }();
+    if (kb_target > 0 && p.swap && d.epilogue != TF_EPI_LOGITS && !d.ln_x) {
+      int best = p.k_blocks <= 16 ? p.k_blocks : 16;
+      for (int dd = 1; dd <= 16 && dd <= p.k_blocks; ++dd)
+        if (p.k_blocks % dd == 0 && p.k_blocks / dd <= kb_target) {
+          best = dd;
+          break;
+        }
+      p.splits = best;
+    }
     if (p.swap && d.ln_x && d.epilogue != TF_EPI_LOGITS) {
       // fused LN: the CTA's normalised K-slice must fit beside the ring
       while (gemm_ln_bytes(p.bn, p.k_blocks / p.splits) > 96 * 1024) {
@@ -215,7 +244,7 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
   const int kb_per = p.k_blocks / p.splits;
   const int stage_bytes = gemm_stage_bytes(p.bn);
   const size_t ln_bytes = (p.swap && d.ln_x) ? gemm_ln_bytes(p.bn, kb_per) : 0;
-  int st = (int)((kMaxSmem - 4096 - ln_bytes) / stage_bytes);
+  int st = (int)((kMaxSmem - 4096 - ln_bytes - gemm_recv_bytes(p.bn, p.splits, p.swap)) / stage_bytes);
   if (!p.swap) {  // leave room for the staged output tile (smem-bytes check below)
     while (st > 1 && gemm_smem_bytes(p.bn, st, p.splits, false) > kMaxSmem) --st;
   }
@@ -283,6 +312,8 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
   a.T = d.seq_len;
   a.qbase_dev = d.qbase_dev;
   a.keys = d.argmax_keys;
+  static const char* kGemmNames[] = {"gemm_f32", "gemm_bias", "gemm_gelu", "gemm_resid", "gemm_qkv", "gemm_logits"};
+  a.trace = trace_next(d.epilogue >= 0 && d.epilogue < 6 ? kGemmNames[d.epilogue] : "gemm");
   if (d.ln_x) {
     TF_REQUIRE(p.swap, TF_ERR_UNSUPPORTED, "gemm: fused LayerNorm needs the swap-AB (decode) path");
     TF_REQUIRE(d.ln_gamma && d.ln_beta && d.ln_hidden > 0 && d.ln_hidden <= 1024 && d.ln_hidden % 8 == 0 &&
@@ -378,7 +409,9 @@ void run_embed(const EmbedArgs& a, cudaStream_t st, bool pdl) {
   }
 }
 
-void run_ln(const LnArgs& a, cudaStream_t st, bool pdl) {
+void run_ln(const LnArgs& a0, cudaStream_t st, bool pdl) {
+  LnArgs a = a0;
+  a.trace = trace_next("layernorm");
   const dim3 grid((a.n_rows + 7) / 8);
   if (vec_ok(a.H, a.ldx, a.ldh) && a.H <= 2048) {
     const int nc = (a.H / 8 + 31) / 32;
@@ -406,8 +439,31 @@ void run_ln(const LnArgs& a, cudaStream_t st, bool pdl) {
 
 void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
   TF_REQUIRE(a.D >= 1 && a.D <= 128, TF_ERR_UNSUPPORTED, "head_dim must be in [1, 128]");
-  if (a.T == 1 && a.D == 64 && a.ws && a.cnt && a.max_chunks >= (a.cap + kSplitKeys - 1) / kSplitKeys) {
-    launch(attn_decode_split_kernel, dim3(a.max_chunks, a.NH, a.B), dim3(kSplitThreads), 0, st, pdl, a);
+  static const int pf_mode = [] {  // TF_ATTN_PF=0 selects the split kernel (A/B diagnostics)
+    const char* e = getenv("TF_ATTN_PF");
+    return e ? atoi(e) : 1;
+  }();
+  if (a.T == 1 && a.D == 64 && a.ws && a.cnt && a.max_chunks >= (a.cap + kSplitKeys - 1) / kSplitKeys &&
+      pf_mode) {
+    // chunks per CTA: the whole window when it is <= 4 chunks (local merge),
+    // else groups of <= 4 (64 KB of K/V each) merged through the workspace
+    const int nch = a.max_chunks;
+    const int ngr = (nch + 3) / 4;
+    AttnArgs t = a;
+    t.group = (nch + ngr - 1) / ngr;
+    t.trace = trace_next("attn_decode_pf");
+    const size_t smem = attn_pf_smem_bytes(t.group);
+    static bool attr = false;
+    if (!attr) {
+      TF_CHECK_CUDA(cudaFuncSetAttribute(attn_decode_pf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)attn_pf_smem_bytes(4)));
+      attr = true;
+    }
+    launch(attn_decode_pf_kernel, dim3(ngr, a.NH, a.B), dim3(128), smem, st, pdl, t);
+  } else if (a.T == 1 && a.D == 64 && a.ws && a.cnt && a.max_chunks >= (a.cap + kSplitKeys - 1) / kSplitKeys) {
+    AttnArgs t = a;
+    t.trace = trace_next("attn_decode_split");
+    launch(attn_decode_split_kernel, dim3(a.max_chunks, a.NH, a.B), dim3(kSplitThreads), 0, st, pdl, t);
   } else if (a.T == 1) {
     const size_t smem = (size_t)(a.D + a.cap + std::max(2 * kDecThreads, kDecWarps * a.D)) * sizeof(float);
     TF_REQUIRE(smem <= kMaxSmem, TF_ERR_UNSUPPORTED, "cache capacity too large for decode kernel");
@@ -1231,6 +1287,31 @@ int tf_debug_mk_trace(void* session, void* trace_buf, int* n_items, int* n_aux, 
       }
     }
   });
+}
+
+int tf_debug_trace(int reset, unsigned long long* dst, int max_slots, const char** names) {
+  // dst: [slot][kTraceCtas][8] raw per-CTA stamps (0 = CTA absent)
+  int n = 0;
+  static unsigned long long* buf = nullptr;
+  const size_t bytes = sizeof(unsigned long long) * (size_t)kTraceSlots * kTraceCtas * 8;
+  const int rc = guarded([&] {
+    if (reset) {
+      if (!buf) {
+        TF_CHECK_CUDA(cudaMalloc(&buf, bytes));
+        TF_CHECK_CUDA(cudaMemcpyToSymbol(g_trace_buf, &buf, sizeof(buf)));
+      }
+      TF_CHECK_CUDA(cudaMemset(buf, 0, bytes));
+      g_trace_n = 0;
+      return;
+    }
+    n = std::min(g_trace_n, max_slots);
+    if (dst && buf && n > 0)
+      TF_CHECK_CUDA(cudaMemcpy(dst, buf, sizeof(unsigned long long) * (size_t)n * kTraceCtas * 8,
+                               cudaMemcpyDeviceToHost));
+    if (names)
+      for (int i = 0; i < n; ++i) names[i] = g_trace_names[i];
+  });
+  return rc != TF_OK ? -rc : n;
 }
 
 int tf_session_launches_per_step(void* session) {

@@ -1,59 +1,79 @@
-"""CUPTI trace of graph-replayed C2 decode steps: per-kernel device durations and
-inter-kernel gaps (torch.profiler collects every kernel in the process)."""
-import os, sys, json, collections
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
-import paper_2407_04991_b200 as P
-from paper_2407_04991_b200 import model as PM, _native as N
-from paper_2407_04991_b200.pruning import prune_position_embedding
-from oracle import tinfer_oracle as O
+"""Per-kernel timeline of one decode step (diagnostics; needs TF_TRACE=1).
 
-B = int(os.environ.get("B", 32)); SRC, NEW = 128, 64
-cfg = P.ModelConfig(40000, 768, 12, 12, 64, 3072, 1024, P.DType.F16, 1, 2)
-m = prune_position_embedding(P.init_random(cfg, 42), 512)
-dm = m.device_model()
-prompts = O.synthetic_prompts(40000, B, SRC)
-ids, pos, pads, _ = PM._left_pad(m.config, prompts)
-s = dm.session(B, SRC + NEW, SRC, NEW)
-use_graph = int(os.environ.get("GRAPH", 1))
-for _ in range(3):
-    s.load_inputs(ids, pos, pads); s.forward(SRC, N.FWD_ARGMAX); s.decode(NEW - 1, use_graph=bool(use_graph))
-torch.cuda.synchronize()
-s.load_inputs(ids, pos, pads); s.forward(SRC, N.FWD_ARGMAX); s.decode(20, use_graph=bool(use_graph))
-torch.cuda.synchronize()
-from torch.profiler import profile, ProfilerActivity
-with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    s.decode(4, use_graph=bool(use_graph))
+Runs a workload's prefill, warms the decode path, then launches ONE decode step
+without a graph (same kernels, same PDL chaining) with trace slots enabled and
+prints, per kernel, each trace point's latest CTA time relative to the previous
+kernel's last exit (the critical-path view). GEMM points: 1 past the PDL wait,
+2 MMA done, 3 partial tile parked, 4 past the cluster barrier, 5 first unit
+reduced, 6 stores issued, 7 exit. Usage: TF_TRACE=1 python tools/trace_step.py [workload] [rows]"""
+
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("TF_TRACE", "1")
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2407_04991_b200 import _native as N  # noqa: E402
+
+NP = 16
+
+
+def main():
+    wname = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    nrows = int(sys.argv[2]) if len(sys.argv) > 2 else 14
+    w = bench.WORKLOADS[wname]
+    model = bench.build_model(w)
+    prompts = bench.make_prompts(model.config.vocab_size, w, 0)
+    run = bench.Runner(model, prompts, w)
+    lib = N.lib()
+    run.stage()
+    run.sess.forward(run.ids.shape[1], N.FWD_ARGMAX)
+    run.sess.decode(8, use_graph=False)
     torch.cuda.synchronize()
-evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
-evs.sort(key=lambda e: e.time_range.start)
-# one step = the last 87 kernels
-per = collections.OrderedDict()
-rows = []
-prev_end = None
-for e in evs:
-    st, en = e.time_range.start, e.time_range.end
-    gap = (st - prev_end) if prev_end is not None else 0
-    prev_end = en
-    rows.append((e.name[:60], en - st, gap))
-n = len(rows)
-print("kernels traced", n)
-step = rows[-(n // 4):]
-tot = sum(r[1] for r in step); gaps = sum(r[2] for r in step)
-print(f"one step: {len(step)} kernels, busy {tot:.1f} us, gaps {gaps:.1f} us, span {tot+gaps:.1f} us")
-agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
-for name, d, g in step:
-    a = agg[name]; a[0] += 1; a[1] += d; a[2] += g
-for k, (c, d, g) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-    print(f"n={c:3d} busy {d:8.1f} us ({d/c:6.2f}/launch) gaps-before {g:7.1f} us  {k}")
-# critical-path attribution: end_i - end_{i-1}
-ends = []
-for e in evs:
-    ends.append((e.name[:60], e.time_range.start, e.time_range.end))
-ends = ends[-(n // 4):]
-inc = collections.defaultdict(lambda: [0, 0.0])
-for i in range(1, len(ends)):
-    a = inc[ends[i][0]]; a[0] += 1; a[1] += ends[i][2] - ends[i - 1][2]
-print("critical-path increments (end_i - end_{i-1}):")
-for k, (c, d) in sorted(inc.items(), key=lambda kv: -kv[1][1]):
-    print(f"  n={c:3d} {d:8.1f} us ({d/c:6.2f}/launch)  {k}")
+    for rep in range(4):
+        lib.tf_debug_trace(1, None, 0, None)
+        run.sess.decode(1, use_graph=False)
+        torch.cuda.synchronize()
+        raw = np.zeros((256, 2048, 8), dtype=np.uint64)
+        names = (C.c_char_p * 256)()
+        n = lib.tf_debug_trace(0, raw.ctypes.data, 256, names)
+    r = raw[:n].astype(np.float64)
+    r[r == 0] = np.nan
+    t = np.full((n, NP), np.nan)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        t[:, :8] = np.nanmax(r, axis=1)
+        t[:, 8:] = np.nanmin(r, axis=1)
+    nm = [names[i].decode() for i in range(n)]
+    base = np.nanmin(t[:, 8])
+    print(f"{'#':>3} {'kernel':<18} {'entry':>7} " + " ".join(f"{'p' + str(i):>6}" for i in range(0, 8)) + f" {'incr':>6}")
+    prev = None
+    tot = {}
+    for i in range(n):
+        ref = prev if prev is not None else t[i, 8]
+        rel = [(t[i, k] - ref) / 1e3 for k in range(0, 8)]
+        incr = (t[i, 7] - ref) / 1e3
+        if i < nrows:
+            print(f"{i:3d} {nm[i]:<18} {(t[i, 8] - base) / 1e3:7.2f} " + " ".join(f"{v:6.2f}" for v in rel)
+                  + f" {incr:6.2f}")
+            mins = [(t[i, 8 + k] - ref) / 1e3 for k in range(0, 8)]
+            print(f"{'':3} {'  (min over CTAs)':<18} {'':7} " + " ".join(f"{v:6.2f}" for v in mins))
+        tot.setdefault(nm[i], []).append(incr)
+        if nm[i] == "attn_decode_pf" and i < nrows:
+            print(f"      scores: SM cycles max {t[i, 6]:.0f} min {t[i, 14]:.0f}; globaltimer p2->p4 "
+                  f"{(t[i, 4] - t[i, 2]) / 1e3:.2f} us (max)")
+        prev = t[i, 7]
+    print("\ncritical-path increment (exit_i - exit_{i-1}) per kernel type, us:")
+    for k, v in tot.items():
+        print(f"  {k:<18} n={len(v):3d} mean {np.nanmean(v):6.2f} total {np.nansum(v):7.1f}")
+    print(f"step (first entry -> last exit): {(t[-1, 7] - base) / 1e3:.1f} us (traced kernels only)")
+
+
+if __name__ == "__main__":
+    main()
