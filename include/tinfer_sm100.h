@@ -87,7 +87,10 @@ typedef struct tf_gemm_desc {
   int* counters; int n_counters;            /* reserved                              */
   int force_swap;                /* -1 auto (swap-AB when m_tok <= 256), 0, 1      */
   int splits;                    /* 0 auto; else divides ceil(k/64), <= 16 (cluster) */
-  int pdl;                       /* launch with programmatic dependent launch       */
+  int pdl;                       /* programmatic dependent launch: 0 off, 1 on (the
+                                    next kernel may launch once this one is set up),
+                                    2 on, next kernel released only after this
+                                    kernel's own dependency wait                   */
   /* optional fused LayerNorm of the activation operand (swap-AB only): act is
    * ignored and row t of the operand is q16(LN(ln_x[t*ln_src_stride+ln_src_off]))
    * over ln_hidden features (tensor.py:153-160); ln_hidden <= 1024, % 8 == 0 */

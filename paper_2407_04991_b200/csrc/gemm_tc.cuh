@@ -68,6 +68,7 @@ struct GemmArgs {
   const float* ln_g;
   const float* ln_b;
   int trace;  // diagnostics slot (0 = off)
+  int late_trigger;  // release the next kernel only after this kernel's PDL wait
 };
 
 constexpr int kTileA = 128;          // MMA M
@@ -429,7 +430,7 @@ __device__ __forceinline__ void epi_pre4(const GemmArgs& p, int tile_a, int tile
 
 template <int MODE, bool SWAP>
 __device__ __forceinline__ void epi_fin4(const GemmArgs& p, int tile_a, int tile_b, int u, const float (&acc)[4],
-                                         const EpiPre4& q) {
+                                         const EpiPre4& q, int qslot) {
   int tok, f, st;
   unit_coords<SWAP>(tile_a, tile_b, p.bn, u, tok, f, st);
   if constexpr (MODE == EPI_F32) {
@@ -463,7 +464,7 @@ __device__ __forceinline__ void epi_fin4(const GemmArgs& p, int tile_a, int tile
       } else {
         const int b = tok / p.T, t = tok - b * p.T;
         const int head = r / p.D, d = r - head * p.D;
-        const int slot = *p.qbase_dev + t;
+        const int slot = qslot + t;
         dst = (which == 1 ? p.kc : p.vc) + (((size_t)b * p.NH + head) * p.cap + slot) * p.D + d;
       }
     }
@@ -489,7 +490,7 @@ __device__ __forceinline__ void epi_fin4(const GemmArgs& p, int tile_a, int tile
       } else {
         const int b = tj / p.T, t = tj - b * p.T;
         const int head = r / p.D, d = r - head * p.D;
-        const int slot = *p.qbase_dev + t;
+        const int slot = qslot + t;
         (which == 1 ? p.kc : p.vc)[(((size_t)b * p.NH + head) * p.cap + slot) * p.D + d] = val[j];
       }
     } else if (p.out) {
@@ -546,8 +547,11 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t tmem = *tmem_slot;
   // let the next kernel in the stream launch now: its prologue (barrier init,
   // TMEM alloc, weight TMA prefetch) overlaps this kernel; it still waits on
-  // griddepcontrol.wait before touching anything this kernel writes
-  pdl_trigger();
+  // griddepcontrol.wait before touching anything this kernel writes. With
+  // late_trigger the release waits for this kernel's own dependency instead
+  // (so a heavy prefetching successor does not compete with this kernel's
+  // weight prefetch).
+  if (!p.late_trigger) pdl_trigger();
 
   // ---------------- TMA producer. Weights do not depend on the previous
   // kernel, so in decode (SWAP) mode the first ring's worth of weight tiles is
@@ -605,6 +609,9 @@ __global__ void __launch_bounds__(128, 1)
 
   // ---------------- epilogue (all 4 warps)
   pdl_wait();
+  if (p.late_trigger) pdl_trigger();
+  // cache slot of token t = 0 (EPI_QKV): one load per thread, overlapping the MMA
+  const int qslot = (MODE == EPI_QKV && p.qbase_dev != nullptr) ? *p.qbase_dev : 0;
   mbar_wait(done_bar, 0);
   tc_fence_after();
   if (threadIdx.x == 0) tr.mark(p.trace, 2);
@@ -656,15 +663,20 @@ __global__ void __launch_bounds__(128, 1)
       }
       bulk_commit();
     }
-    EpiPre4 pre;
+    // epilogue operands of this thread's first two units, loaded while the
+    // peer slices are in flight
+    EpiPre4 pre, pre2;
     int u = u_lo + (int)threadIdx.x;
     if (u < u_hi) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
+    if (u + 128 < u_hi) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u + 128, pre2);
     mbar_wait(recv_bar, 0);
     if (threadIdx.x == 0) tr.mark(p.trace, 4);
     const float4* own = reinterpret_cast<const float4*>(part);
     const float4* rin = reinterpret_cast<const float4*>(recv);
-    for (bool first = true; u < u_hi; u += 128, first = false) {
-      if (!first) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
+    for (int it = 0; u < u_hi; u += 128, ++it) {
+      const bool first = it == 0;
+      if (it == 1) pre = pre2;
+      if (it >= 2) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
       float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
       for (int sp = 0; sp < 16; ++sp)
@@ -676,7 +688,7 @@ __global__ void __launch_bounds__(128, 1)
           acc[3] = __fadd_rn(acc[3], pv.w);
         }
       if (threadIdx.x == 0 && first) tr.mark(p.trace, 5);
-      epi_fin4<MODE, SWAP>(p, tile_a, tile_b, u, acc, pre);
+      epi_fin4<MODE, SWAP>(p, tile_a, tile_b, u, acc, pre, qslot);
     }
     if (threadIdx.x == 0) {
       tr.mark(p.trace, 6);
@@ -734,7 +746,7 @@ __global__ void __launch_bounds__(128, 1)
         }
       if (threadIdx.x == 0 && first) tr.mark(p.trace, 5);
       if (it == n_units - 1) cluster_arrive_any();
-      epi_fin4<MODE, SWAP>(p, tile_a, tile_b, u, acc, pre);
+      epi_fin4<MODE, SWAP>(p, tile_a, tile_b, u, acc, pre, qslot);
     }
     if (threadIdx.x == 0) tr.mark(p.trace, 6);
     cluster_wait_any();  // partial tiles stay alive until every CTA has read them

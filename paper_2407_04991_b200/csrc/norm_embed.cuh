@@ -71,9 +71,8 @@ __device__ __forceinline__ void ln_row_store(const float (&xv)[VPL], int H, cons
 // c8 = lane + 32*i; every load of the row (x, gamma, beta) is issued before the
 // first use so one row costs ~one memory round trip.
 template <int NC>
-__device__ __forceinline__ void ln_row_vec(float (&xv)[NC * 8], int H, const float* g,
-                                           const float* b, __half* hrow, int lane) {
-  float4 gv[NC * 2], bv[NC * 2];
+__device__ __forceinline__ void ln_load_gb(int H, const float* g, const float* b, int lane, float4 (&gv)[NC * 2],
+                                           float4 (&bv)[NC * 2]) {
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
     const int c = (lane + 32 * i) * 8;
@@ -84,6 +83,11 @@ __device__ __forceinline__ void ln_row_vec(float (&xv)[NC * 8], int H, const flo
       bv[2 * i + 1] = *reinterpret_cast<const float4*>(b + c + 4);
     }
   }
+}
+
+template <int NC>
+__device__ __forceinline__ void ln_row_apply(float (&xv)[NC * 8], int H, const float4 (&gv)[NC * 2],
+                                             const float4 (&bv)[NC * 2], __half* hrow, int lane) {
   float s = 0.0f;
 #pragma unroll
   for (int i = 0; i < NC; ++i)
@@ -116,6 +120,14 @@ __device__ __forceinline__ void ln_row_vec(float (&xv)[NC * 8], int H, const flo
       *reinterpret_cast<uint4*>(hrow + c) = pack8(y);
     }
   }
+}
+
+template <int NC>
+__device__ __forceinline__ void ln_row_vec(float (&xv)[NC * 8], int H, const float* g, const float* b, __half* hrow,
+                                           int lane) {
+  float4 gv[NC * 2], bv[NC * 2];
+  ln_load_gb<NC>(H, g, b, lane, gv, bv);
+  ln_row_apply<NC>(xv, H, gv, bv, hrow, lane);
 }
 
 template <int NC>
@@ -246,10 +258,13 @@ template <int NC>
 __global__ void __launch_bounds__(256) layernorm_vec_kernel(const LnArgs a) {
   TF_TRACE_INIT(tr);
   if (threadIdx.x == 0) tr.mark(a.trace, 0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // gamma / beta are weights: loaded before the dependency wait
+  float4 gv[NC * 2], bv[NC * 2];
+  ln_load_gb<NC>(a.H, a.g, a.b, lane, gv, bv);
   pdl_wait();
   if (threadIdx.x == 0) tr.mark(a.trace, 1);
   pdl_trigger();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp;
   if (row < a.n_rows) {
     const __half* xr = a.x + ((size_t)row * a.src_stride + a.src_off) * a.ldx;
@@ -269,7 +284,7 @@ __global__ void __launch_bounds__(256) layernorm_vec_kernel(const LnArgs a) {
         for (int e = 0; e < 8; ++e) xv[8 * i + e] = 0.0f;
       }
     }
-    ln_row_vec<NC>(xv, a.H, a.g, a.b, a.h + (size_t)row * a.ldh, lane);
+    ln_row_apply<NC>(xv, a.H, gv, bv, a.h + (size_t)row * a.ldh, lane);
   }
   if (a.trace) {
     __syncthreads();

@@ -130,6 +130,25 @@ void launch(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool
   launch_cluster(kern, grid, block, smem, st, pdl, 1, args...);
 }
 
+// max shared-memory carveout, once per kernel (see set_max_carveout)
+bool carveout_on() {
+  static const bool on = [] {  // TF_CARVEOUT=0 disables (A/B diagnostics)
+    const char* e = getenv("TF_CARVEOUT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename Kern, typename... Args>
+void launch_mc(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl, Args... args) {
+  static bool done = false;  // one flag per kernel instantiation
+  if (!done && carveout_on()) {
+    TF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared));
+    done = true;
+  }
+  launch_cluster(kern, grid, block, smem, st, pdl, 1, args...);
+}
+
 int g_num_sms = 0;
 int num_sms() {
   if (g_num_sms == 0) {
@@ -159,6 +178,17 @@ int trace_next(const char* name) {
 // dynamic smem budget: 227 KB per CTA minus room for the kernels' static smem
 constexpr size_t kMaxSmem = 227 * 1024 - 1024;
 
+// Every SM keeps the maximum shared-memory carveout, whatever kernel runs on
+// it: with programmatic dependent launch the next kernel's CTAs are placed
+// while the current kernel's are resident, and an SM configured for a small
+// carveout cannot take them until it drains.
+template <typename K>
+void set_max_carveout(K kern) {
+  if (carveout_on())
+    TF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared));
+}
+
 template <int MODE, bool SWAP>
 void ensure_gemm_attr() {
   static bool done = false;
@@ -167,6 +197,7 @@ void ensure_gemm_attr() {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
     TF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<MODE, SWAP>,
                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    set_max_carveout(gemm_tc_kernel<MODE, SWAP>);
     done = true;
   }
 }
@@ -312,6 +343,7 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
   a.T = d.seq_len;
   a.qbase_dev = d.qbase_dev;
   a.keys = d.argmax_keys;
+  a.late_trigger = d.pdl == 2 ? 1 : 0;
   static const char* kGemmNames[] = {"gemm_f32", "gemm_bias", "gemm_gelu", "gemm_resid", "gemm_qkv", "gemm_logits"};
   a.trace = trace_next(d.epilogue >= 0 && d.epilogue < 6 ? kGemmNames[d.epilogue] : "gemm");
   if (d.ln_x) {
@@ -388,23 +420,23 @@ void run_embed(const EmbedArgs& a, cudaStream_t st, bool pdl) {
   if (vec_ok(a.H, a.ldw, a.ldx) && a.H <= 2048) {
     const int nc = (a.H / 8 + 31) / 32;
     switch (nc) {
-      case 1: launch(embed_ln_vec_kernel<1>, grid, dim3(256), 0, st, pdl, a); return;
-      case 2: launch(embed_ln_vec_kernel<2>, grid, dim3(256), 0, st, pdl, a); return;
-      case 3: launch(embed_ln_vec_kernel<3>, grid, dim3(256), 0, st, pdl, a); return;
-      case 4: launch(embed_ln_vec_kernel<4>, grid, dim3(256), 0, st, pdl, a); return;
-      case 6: launch(embed_ln_vec_kernel<6>, grid, dim3(256), 0, st, pdl, a); return;
-      case 8: launch(embed_ln_vec_kernel<8>, grid, dim3(256), 0, st, pdl, a); return;
+      case 1: launch_mc(embed_ln_vec_kernel<1>, grid, dim3(256), 0, st, pdl, a); return;
+      case 2: launch_mc(embed_ln_vec_kernel<2>, grid, dim3(256), 0, st, pdl, a); return;
+      case 3: launch_mc(embed_ln_vec_kernel<3>, grid, dim3(256), 0, st, pdl, a); return;
+      case 4: launch_mc(embed_ln_vec_kernel<4>, grid, dim3(256), 0, st, pdl, a); return;
+      case 6: launch_mc(embed_ln_vec_kernel<6>, grid, dim3(256), 0, st, pdl, a); return;
+      case 8: launch_mc(embed_ln_vec_kernel<8>, grid, dim3(256), 0, st, pdl, a); return;
       default: break;
     }
   }
   switch (vpl_for(a.H)) {
-    case 4: launch(embed_ln_kernel<4>, grid, dim3(256), 0, st, pdl, a); break;
-    case 8: launch(embed_ln_kernel<8>, grid, dim3(256), 0, st, pdl, a); break;
-    case 16: launch(embed_ln_kernel<16>, grid, dim3(256), 0, st, pdl, a); break;
-    case 24: launch(embed_ln_kernel<24>, grid, dim3(256), 0, st, pdl, a); break;
-    case 32: launch(embed_ln_kernel<32>, grid, dim3(256), 0, st, pdl, a); break;
-    case 48: launch(embed_ln_kernel<48>, grid, dim3(256), 0, st, pdl, a); break;
-    case 64: launch(embed_ln_kernel<64>, grid, dim3(256), 0, st, pdl, a); break;
+    case 4: launch_mc(embed_ln_kernel<4>, grid, dim3(256), 0, st, pdl, a); break;
+    case 8: launch_mc(embed_ln_kernel<8>, grid, dim3(256), 0, st, pdl, a); break;
+    case 16: launch_mc(embed_ln_kernel<16>, grid, dim3(256), 0, st, pdl, a); break;
+    case 24: launch_mc(embed_ln_kernel<24>, grid, dim3(256), 0, st, pdl, a); break;
+    case 32: launch_mc(embed_ln_kernel<32>, grid, dim3(256), 0, st, pdl, a); break;
+    case 48: launch_mc(embed_ln_kernel<48>, grid, dim3(256), 0, st, pdl, a); break;
+    case 64: launch_mc(embed_ln_kernel<64>, grid, dim3(256), 0, st, pdl, a); break;
     default: throw TfError{TF_ERR_UNSUPPORTED, "hidden size > 2048 unsupported"};
   }
 }
@@ -416,23 +448,23 @@ void run_ln(const LnArgs& a0, cudaStream_t st, bool pdl) {
   if (vec_ok(a.H, a.ldx, a.ldh) && a.H <= 2048) {
     const int nc = (a.H / 8 + 31) / 32;
     switch (nc) {
-      case 1: launch(layernorm_vec_kernel<1>, grid, dim3(256), 0, st, pdl, a); return;
-      case 2: launch(layernorm_vec_kernel<2>, grid, dim3(256), 0, st, pdl, a); return;
-      case 3: launch(layernorm_vec_kernel<3>, grid, dim3(256), 0, st, pdl, a); return;
-      case 4: launch(layernorm_vec_kernel<4>, grid, dim3(256), 0, st, pdl, a); return;
-      case 6: launch(layernorm_vec_kernel<6>, grid, dim3(256), 0, st, pdl, a); return;
-      case 8: launch(layernorm_vec_kernel<8>, grid, dim3(256), 0, st, pdl, a); return;
+      case 1: launch_mc(layernorm_vec_kernel<1>, grid, dim3(256), 0, st, pdl, a); return;
+      case 2: launch_mc(layernorm_vec_kernel<2>, grid, dim3(256), 0, st, pdl, a); return;
+      case 3: launch_mc(layernorm_vec_kernel<3>, grid, dim3(256), 0, st, pdl, a); return;
+      case 4: launch_mc(layernorm_vec_kernel<4>, grid, dim3(256), 0, st, pdl, a); return;
+      case 6: launch_mc(layernorm_vec_kernel<6>, grid, dim3(256), 0, st, pdl, a); return;
+      case 8: launch_mc(layernorm_vec_kernel<8>, grid, dim3(256), 0, st, pdl, a); return;
       default: break;
     }
   }
   switch (vpl_for(a.H)) {
-    case 4: launch(layernorm_kernel<4>, grid, dim3(256), 0, st, pdl, a); break;
-    case 8: launch(layernorm_kernel<8>, grid, dim3(256), 0, st, pdl, a); break;
-    case 16: launch(layernorm_kernel<16>, grid, dim3(256), 0, st, pdl, a); break;
-    case 24: launch(layernorm_kernel<24>, grid, dim3(256), 0, st, pdl, a); break;
-    case 32: launch(layernorm_kernel<32>, grid, dim3(256), 0, st, pdl, a); break;
-    case 48: launch(layernorm_kernel<48>, grid, dim3(256), 0, st, pdl, a); break;
-    case 64: launch(layernorm_kernel<64>, grid, dim3(256), 0, st, pdl, a); break;
+    case 4: launch_mc(layernorm_kernel<4>, grid, dim3(256), 0, st, pdl, a); break;
+    case 8: launch_mc(layernorm_kernel<8>, grid, dim3(256), 0, st, pdl, a); break;
+    case 16: launch_mc(layernorm_kernel<16>, grid, dim3(256), 0, st, pdl, a); break;
+    case 24: launch_mc(layernorm_kernel<24>, grid, dim3(256), 0, st, pdl, a); break;
+    case 32: launch_mc(layernorm_kernel<32>, grid, dim3(256), 0, st, pdl, a); break;
+    case 48: launch_mc(layernorm_kernel<48>, grid, dim3(256), 0, st, pdl, a); break;
+    case 64: launch_mc(layernorm_kernel<64>, grid, dim3(256), 0, st, pdl, a); break;
     default: throw TfError{TF_ERR_UNSUPPORTED, "hidden size > 2048 unsupported"};
   }
 }
@@ -457,6 +489,7 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
     if (!attr) {
       TF_CHECK_CUDA(cudaFuncSetAttribute(attn_decode_pf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)attn_pf_smem_bytes(4)));
+      set_max_carveout(attn_decode_pf_kernel);
       attr = true;
     }
     launch(attn_decode_pf_kernel, dim3(ngr, a.NH, a.B), dim3(128), smem, st, pdl, t);
@@ -510,6 +543,7 @@ struct Session {
   tf_session_desc d;
   MkState mk;
   cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t graph_multi = nullptr;  // TF_GRAPH_STEPS decode steps
   cudaGraphExec_t beam_graph = nullptr;
   tf_beam_desc beam_key{};  // descriptor the beam graph was captured with
   int graph_launches = 0;
@@ -622,6 +656,13 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     q.cap = sd.capacity;
     q.seq_len = T;
     q.qbase_dev = sd.len_dev;
+    static const bool qkv_late = [] {  // TF_QKV_LATE=0 disables (A/B diagnostics)
+      const char* e = getenv("TF_QKV_LATE");
+      return !(e && e[0] == '0');
+    }();
+    // decode: attention (next) prefetches the whole KV window; release it only
+    // once the QKV weights are in (after this GEMM's own dependency wait)
+    if (pdl && T == 1 && qkv_late) q.pdl = 2;
     run_gemm(q, st);
     ++launches;
     // attention over slots [pad_b, len + t] (model.py:475-478)
@@ -773,9 +814,9 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     // only advance the cache length: reuse collect with no token output
     CollectArgs c2 = c;
     c2.B = 0;
-    launch(collect_kernel, dim3(1), dim3(32), 0, st, pdl, c2);
+    launch_mc(collect_kernel, dim3(1), dim3(32), 0, st, pdl, c2);
   } else {
-    launch(collect_kernel, dim3(1), dim3(256), 0, st, pdl, c);
+    launch_mc(collect_kernel, dim3(1), dim3(256), 0, st, pdl, c);
   }
   ++launches;
   return launches;
@@ -1166,6 +1207,7 @@ int tf_session_destroy(void* session) {
   return guarded([&] {
     Session* s = static_cast<Session*>(session);
     if (s && s->graph) cudaGraphExecDestroy(s->graph);
+    if (s && s->graph_multi) cudaGraphExecDestroy(s->graph_multi);
     if (s && s->beam_graph) cudaGraphExecDestroy(s->beam_graph);
     if (s && s->mk.mem) cudaFree(s->mk.mem);
     delete s;
@@ -1197,28 +1239,42 @@ int tf_decode(void* session, int n_steps, int use_graph, void* stream) {
         s.launches_last = forward(s, nullptr, nullptr, 1, TF_FWD_ARGMAX, true, st);
       return;
     }
-    if (!s.graph) {
-      // capture one decode step on a private stream; every per-step quantity
-      // (cache length, fed ids, output column) lives in device memory
+    // capture k decode steps on a private stream; every per-step quantity
+    // (cache length, fed ids, output column) lives in device memory, so one
+    // graph replays any step. Steps inside a graph are chained with PDL like
+    // the kernels of a step (each step's embed kernel waits before releasing
+    // its successor, which keeps whole steps ordered).
+    auto capture = [&](int k, cudaGraphExec_t* out) {
       cudaStream_t cs;
       TF_CHECK_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
       cudaGraph_t g;
       TF_CHECK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
       int launches = 0;
       try {
-        launches = forward(s, nullptr, nullptr, 1, TF_FWD_ARGMAX, true, cs);
+        for (int i = 0; i < k; ++i) launches = forward(s, nullptr, nullptr, 1, TF_FWD_ARGMAX, true, cs);
       } catch (...) {
         cudaStreamEndCapture(cs, &g);
         cudaStreamDestroy(cs);
         throw;
       }
       TF_CHECK_CUDA(cudaStreamEndCapture(cs, &g));
-      TF_CHECK_CUDA(cudaGraphInstantiate(&s.graph, g, 0));
+      TF_CHECK_CUDA(cudaGraphInstantiate(out, g, 0));
       TF_CHECK_CUDA(cudaGraphDestroy(g));
       TF_CHECK_CUDA(cudaStreamDestroy(cs));
-      s.graph_launches = launches;
+      return launches;
+    };
+    static const int multi = [] {  // steps per multi-step graph (TF_GRAPH_STEPS, 1 disables)
+      const char* e = getenv("TF_GRAPH_STEPS");
+      const int v = e ? atoi(e) : 8;
+      return v < 1 ? 1 : v;
+    }();
+    if (!s.graph) s.graph_launches = capture(1, &s.graph);
+    int left = n_steps;
+    if (multi > 1 && left >= multi) {
+      if (!s.graph_multi) capture(multi, &s.graph_multi);
+      for (; left >= multi; left -= multi) TF_CHECK_CUDA(cudaGraphLaunch(s.graph_multi, st));
     }
-    for (int i = 0; i < n_steps; ++i) TF_CHECK_CUDA(cudaGraphLaunch(s.graph, st));
+    for (; left > 0; --left) TF_CHECK_CUDA(cudaGraphLaunch(s.graph, st));
     s.launches_last = s.graph_launches;
   });
 }

@@ -35,13 +35,30 @@ def main():
     run.sess.forward(run.ids.shape[1], N.FWD_ARGMAX)
     run.sess.decode(8, use_graph=False)
     torch.cuda.synchronize()
-    for rep in range(4):
+    reps = int(os.environ.get("TRACE_REPS", "10"))
+    agg = {}
+    step_us = []
+    for rep in range(reps):
         lib.tf_debug_trace(1, None, 0, None)
         run.sess.decode(1, use_graph=False)
         torch.cuda.synchronize()
         raw = np.zeros((256, 2048, 8), dtype=np.uint64)
         names = (C.c_char_p * 256)()
         n = lib.tf_debug_trace(0, raw.ctypes.data, 256, names)
+        r = raw[:n].astype(np.float64)
+        r[r == 0] = np.nan
+        import warnings
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            mx = np.nanmax(r[:, :, 7], axis=1)
+            mn0 = np.nanmin(r[:, :, 0], axis=1)
+        for i in range(n):
+            prev = mx[i - 1] if i > 0 else mn0[0]
+            agg.setdefault(names[i].decode(), []).append((mx[i] - prev) / 1e3)
+        step_us.append((mx[n - 1] - mn0[0]) / 1e3)
+    print(f"mean over {reps} traced steps: step {np.mean(step_us):.1f} us (median {np.median(step_us):.1f})")
+    for k, v in agg.items():
+        print(f"  {k:<18} mean incr {np.nanmean(v):6.2f} us  x{len(v) // reps:3d}/step = {np.nansum(v) / reps:7.1f} us")
     r = raw[:n].astype(np.float64)
     r[r == 0] = np.nan
     t = np.full((n, NP), np.nan)
