@@ -89,8 +89,10 @@ __host__ __device__ inline size_t gemm_ring_bytes(int bn, int stages, int splits
   ring = ring > part ? ring : part;
   return ring > out ? ring : out;
 }
-__host__ __device__ inline size_t gemm_ln_bytes(int bn, int kb_per_split) {
-  return (size_t)kb_per_split * bn * kBK * 2;
+// LN-fused B operand: the normalised K-slice (kb_per_split tiles) plus the TMA
+// staging of the full source rows (k_blocks tiles of 64 columns)
+__host__ __device__ inline size_t gemm_ln_bytes(int bn, int kb_per_split, int k_blocks) {
+  return (size_t)(kb_per_split + k_blocks) * bn * kBK * 2;
 }
 // push-based split-K reduction (SWAP, splits > 1, bn <= 128): every CTA owns a
 // receive buffer for the S-1 peer slices of its 1/S share of the tile
@@ -104,62 +106,54 @@ __host__ __device__ inline size_t gemm_recv_bytes(int bn, int splits, bool swap)
 }
 __host__ inline size_t gemm_smem_bytes(int bn, int stages, int splits, bool swap, size_t ln_bytes = 0) {
   return 1024 + gemm_ring_bytes(bn, stages, splits, swap) + ln_bytes + gemm_recv_bytes(bn, splits, swap) +
-         (2 * stages + 2) * 8 + 16;
+         (2 * stages + 3) * 8 + 16;
 }
 
-// LN-fused B operand: 128 threads normalise the CTA's bn token rows over the full
-// row (same operation order as layernorm_vec_kernel, so results are bit-identical
-// to the stand-alone LN) and write the K-slice [kb0*64, (kb0+nkb)*64) into `bln`
-// as nkb swizzled (128-byte) K-major tiles of bn rows.
-__device__ __forceinline__ void ln_build_b(const GemmArgs& p, int tile_b, int kb0, int nkb, uint8_t* bln) {
+// LN-fused B operand: the CTA's bn source rows were staged in smem by TMA
+// (k_blocks swizzled 64-column tiles at `stg`); each warp normalises whole rows
+// (same operation order as layernorm_vec_kernel -> bit-identical to the
+// stand-alone LN) and writes the K-slice [kb0*64, (kb0+nkb)*64) into `bln` as
+// nkb swizzled (128-byte) K-major tiles of bn rows. (Plain loads of the rows
+// by every CTA of a launch hit the same L2 lines from 100+ SMs and serialise;
+// TMA does not.)
+__device__ __forceinline__ void ln_build_b(const GemmArgs& p, int tile_b, int kb0, int nkb, uint8_t* bln,
+                                           const uint8_t* stg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bn = p.bn, H = p.ln_H;
   constexpr int NC = 4;  // 16-byte chunks per lane: H <= 1024
   const int c_lo = kb0 * kBK, c_hi = (kb0 + nkb) * kBK;
   for (int r = warp; r < bn; r += 4) {
-    const int tok = tile_b * bn + r;
-    const bool valid = tok < p.m_tok;
+    const bool valid = tile_b * bn + r < p.m_tok;
     float xv[NC * 8];
-    if (valid) {
-      const __half* xr = p.ln_x + ((size_t)tok * p.ln_src_stride + p.ln_src_off) * p.ln_ldx;
-      uint4 raw[NC];
 #pragma unroll
-      for (int i = 0; i < NC; ++i) {
-        const int c = (lane + 32 * i) * 8;
-        if (c < H) raw[i] = __ldcg(reinterpret_cast<const uint4*>(xr + c));
+    for (int i = 0; i < NC; ++i) {
+      const int q = lane + 32 * i;
+      if (q * 8 < H) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(stg + (size_t)(q >> 3) * bn * 128 + r * 128 +
+                                                          (((q & 7) ^ (r & 7)) * 16));
+        unpack8(raw, &xv[8 * i]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xv[8 * i + e] = 0.0f;
       }
+    }
+    float sum = 0.0f;
 #pragma unroll
-      for (int i = 0; i < NC; ++i) {
-        if ((lane + 32 * i) * 8 < H) {
-          unpack8(raw[i], &xv[8 * i]);
-        } else {
+    for (int i = 0; i < NC; ++i)
+      if ((lane + 32 * i) * 8 < H)
 #pragma unroll
-          for (int e = 0; e < 8; ++e) xv[8 * i + e] = 0.0f;
+        for (int e = 0; e < 8; ++e) sum = __fadd_rn(sum, xv[8 * i + e]);
+    const float mean = __fdiv_rn(warp_sum(sum), (float)H);
+    float ss = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+      if ((lane + 32 * i) * 8 < H)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float d = __fsub_rn(xv[8 * i + e], mean);
+          ss = __fadd_rn(ss, __fmul_rn(d, d));
         }
-      }
-    }
-    float mean = 0.0f, inv = 0.0f;
-    if (valid) {
-      float sum = 0.0f;
-#pragma unroll
-      for (int i = 0; i < NC; ++i)
-        if ((lane + 32 * i) * 8 < H)
-#pragma unroll
-          for (int e = 0; e < 8; ++e) sum = __fadd_rn(sum, xv[8 * i + e]);
-      sum = warp_sum(sum);
-      mean = __fdiv_rn(sum, (float)H);
-      float ss = 0.0f;
-#pragma unroll
-      for (int i = 0; i < NC; ++i)
-        if ((lane + 32 * i) * 8 < H)
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float d = __fsub_rn(xv[8 * i + e], mean);
-            ss = __fadd_rn(ss, __fmul_rn(d, d));
-          }
-      ss = warp_sum(ss);
-      inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)H), 1e-5f)));
-    }
+    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(warp_sum(ss), (float)H), 1e-5f)));
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
       const int c = (lane + 32 * i) * 8;
@@ -510,10 +504,11 @@ __global__ void __launch_bounds__(128, 1)
   const int stage_bytes = gemm_stage_bytes(bn);
   const bool ln_mode = SWAP && p.ln_x != nullptr;
   uint8_t* bln = smem + gemm_ring_bytes(bn, stages, p.splits, SWAP);
-  uint8_t* recv = bln + (ln_mode ? gemm_ln_bytes(bn, p.kb_per_split) : 0);
+  uint8_t* recv = bln + (ln_mode ? gemm_ln_bytes(bn, p.kb_per_split, p.k_blocks) : 0);
+  uint8_t* stg = bln + (size_t)p.kb_per_split * bn * kBK * 2;  // LN source rows (ln_mode)
   const bool push = gemm_push_reduce(bn, p.splits, SWAP);
   uint64_t* bars = reinterpret_cast<uint64_t*>(recv + gemm_recv_bytes(bn, p.splits, SWAP));
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 3);
   __shared__ unsigned long long red[64];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -521,7 +516,8 @@ __global__ void __launch_bounds__(128, 1)
   const int kb0 = split * p.kb_per_split;
   const int nkb = min(p.kb_per_split, p.k_blocks - kb0);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + stages),
-                 done_bar = smem_u32(bars + 2 * stages), recv_bar = smem_u32(bars + 2 * stages + 1);
+                 done_bar = smem_u32(bars + 2 * stages), recv_bar = smem_u32(bars + 2 * stages + 1),
+                 ln_bar = smem_u32(bars + 2 * stages + 2);
   const uint32_t ncols = (uint32_t)gemm_tmem_cols(bn);
   TF_TRACE_INIT(tr);
   if (threadIdx.x == 0) tr.mark(p.trace, 0);
@@ -535,6 +531,7 @@ __global__ void __launch_bounds__(128, 1)
     }
     mbar_init(done_bar, 1);
     mbar_init(recv_bar, 1);
+    mbar_init(ln_bar, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(smem_u32(tmem_slot), ncols);
@@ -565,9 +562,15 @@ __global__ void __launch_bounds__(128, 1)
       tma_load_2d(sa, &tmA, (kb0 + i) * kBK, tile_a * kTileA, full0 + 8 * i);
     }
   }
-  if (ln_mode) {  // all 128 threads build the normalised B tiles, then go on
+  if (ln_mode) {  // stage the source rows by TMA, then all 128 threads build the normalised B tiles
     pdl_wait();
-    ln_build_b(p, tile_b, kb0, nkb, bln);
+    if (warp == 0 && lane == 0) {
+      mbar_expect_tx(ln_bar, (uint32_t)(p.k_blocks * bn * kBK * 2));
+      for (int kb = 0; kb < p.k_blocks; ++kb)
+        tma_load_2d(smem_u32(stg + (size_t)kb * bn * kBK * 2), &tmB, kb * kBK, tile_b * bn, ln_bar);
+    }
+    mbar_wait(ln_bar, 0);
+    ln_build_b(p, tile_b, kb0, nkb, bln, stg);
     __syncthreads();
   }
   if (warp == 0 && lane == 0) {

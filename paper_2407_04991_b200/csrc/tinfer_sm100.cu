@@ -262,7 +262,7 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
     }
     if (p.swap && d.ln_x && d.epilogue != TF_EPI_LOGITS) {
       // fused LN: the CTA's normalised K-slice must fit beside the ring
-      while (gemm_ln_bytes(p.bn, p.k_blocks / p.splits) > 96 * 1024) {
+      while (gemm_ln_bytes(p.bn, p.k_blocks / p.splits, p.k_blocks) > 128 * 1024) {
         int next = p.splits + 1;
         while (next <= 16 && p.k_blocks % next) ++next;
         if (next > 16) break;
@@ -274,7 +274,7 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
              "argmax epilogue does not support split-K");
   const int kb_per = p.k_blocks / p.splits;
   const int stage_bytes = gemm_stage_bytes(p.bn);
-  const size_t ln_bytes = (p.swap && d.ln_x) ? gemm_ln_bytes(p.bn, kb_per) : 0;
+  const size_t ln_bytes = (p.swap && d.ln_x) ? gemm_ln_bytes(p.bn, kb_per, p.k_blocks) : 0;
   int st = (int)((kMaxSmem - 4096 - ln_bytes - gemm_recv_bytes(p.bn, p.splits, p.swap)) / stage_bytes);
   if (!p.swap) {  // leave room for the staged output tile (smem-bytes check below)
     while (st > 1 && gemm_smem_bytes(p.bn, st, p.splits, false) > kMaxSmem) --st;
@@ -294,7 +294,7 @@ void launch_gemm_t(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& 
                    const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
   ensure_gemm_attr<MODE, SWAP>();
   dim3 grid(p.tiles_a, p.tiles_b, p.splits);
-  const size_t ln_bytes = (SWAP && d.ln_x) ? gemm_ln_bytes(p.bn, p.k_blocks / p.splits) : 0;
+  const size_t ln_bytes = (SWAP && d.ln_x) ? gemm_ln_bytes(p.bn, p.k_blocks / p.splits, p.k_blocks) : 0;
   launch_cluster(gemm_tc_kernel<MODE, SWAP>, grid, dim3(128),
                  gemm_smem_bytes(p.bn, p.stages, p.splits, SWAP, ln_bytes), st, d.pdl != 0, p.splits, ta, tb, args);
 }
@@ -351,7 +351,7 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
     TF_REQUIRE(d.ln_gamma && d.ln_beta && d.ln_hidden > 0 && d.ln_hidden <= 1024 && d.ln_hidden % 8 == 0 &&
                    d.ln_ldx % 8 == 0 && d.ln_hidden <= kext,
                TF_ERR_ARG, "gemm: bad fused LayerNorm arguments");
-    TF_REQUIRE(gemm_ln_bytes(p.bn, p.k_blocks / p.splits) <= 96 * 1024, TF_ERR_UNSUPPORTED,
+    TF_REQUIRE(gemm_ln_bytes(p.bn, p.k_blocks / p.splits, p.k_blocks) <= 128 * 1024, TF_ERR_UNSUPPORTED,
                "gemm: fused LayerNorm tile too large");
     a.ln_x = static_cast<const __half*>(d.ln_x);
     a.ln_ldx = d.ln_ldx;
@@ -386,7 +386,11 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
   }
   const void* P = p.swap ? d.wt : d.act;
   const void* Q = p.swap ? d.act : d.wt;
-  const int ldp = p.swap ? d.ldw : d.lda, ldq = p.swap ? d.lda : d.ldw;
+  int ldp = p.swap ? d.ldw : d.lda, ldq = p.swap ? d.lda : d.ldw;
+  if (d.ln_x) {  // fused LN: the B map stages the (strided) LN source rows instead
+    Q = static_cast<const __half*>(d.ln_x) + (size_t)d.ln_src_off * d.ln_ldx;
+    ldq = d.ln_ldx * d.ln_src_stride;
+  }
   const CUtensorMap ta = make_kmajor_map(P, a.rows_a, kext, ldp, kTileA);
   const CUtensorMap tb = make_kmajor_map(Q, a.rows_b, kext, ldq, p.bn);
   switch (d.epilogue) {
@@ -618,11 +622,12 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     const char* e = getenv("TF_FUSE_LN");
     return e && e[0] == '1';
   }();
-  const bool fuse_ln = fuse_opt && M <= 256 && H <= 1024 && H % 8 == 0 && m.ldk_h % 8 == 0;
+  const bool fuse_ln = fuse_opt && M <= 64 && H <= 1024 && H % 8 == 0 && m.ldk_h % 8 == 0;
   // the lm_head (argmax epilogue, no split-K) fuses only if its full-K tile fits
   const int lg_rows = (mode == TF_FWD_LOGITS_ALL) ? M : B;
   const bool fuse_final = fuse_ln && lg_rows <= 256 &&
-                          gemm_ln_bytes(((std::min(lg_rows, 256) + 15) / 16) * 16, pad64(H) / 64) <= 96 * 1024;
+                          gemm_ln_bytes(((std::min(lg_rows, 256) + 15) / 16) * 16, pad64(H) / 64, pad64(H) / 64) <=
+                              128 * 1024;
   auto set_ln = [&](tf_gemm_desc& d, const float* gam, const float* bet, int stride, int off) {
     d.ln_x = x;
     d.ln_ldx = m.ldk_h;
