@@ -39,6 +39,10 @@ struct AttnArgs {
   int max_chunks;
   int group;  // decode prefetch kernel: 64-slot chunks per CTA
   int trace;  // diagnostics slot (0 = off)
+  // decode prefetch kernel: the next layer's caches (same layout); each CTA
+  // streams its own window of them HBM -> L2 (null = off)
+  const __half* pf_kc;
+  const __half* pf_vc;
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
@@ -436,6 +440,12 @@ __global__ void __launch_bounds__(128) attn_decode_pf_kernel(const AttnArgs a) {
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
+  if (a.pf_kc != nullptr && ind == nullptr && tid < 2 && nc > 0) {
+    // next layer's copy of this CTA's window (contiguous slots of one (b, h))
+    const int s0 = lo + c0 * 64, s1 = min(lo + (c0 + nc) * 64, hi + 1);
+    const size_t off = kv_off(s0);
+    l2_prefetch_bulk((tid == 0 ? a.pf_kc : a.pf_vc) + off, (uint32_t)((s1 - s0) * D * 2));
+  }
   pdl_trigger();
   pdl_wait();
   if (threadIdx.x == 0) tr.mark(a.trace, 1);

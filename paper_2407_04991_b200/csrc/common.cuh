@@ -138,6 +138,29 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   return p;
 }
 
+// Fire-and-forget HBM -> L2 prefetch of [p, p + bytes) (16-B aligned, multiple
+// of 16). Used to stream the next layer's weights / KV slots into L2 while the
+// current layer's latency-bound kernels run.
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// This CTA's share (by linear block id) of a flat prefetch range, in <= 32 KB pieces.
+__device__ __forceinline__ void l2_prefetch_share(const void* base, unsigned long long bytes) {
+  if (base == nullptr || bytes == 0) return;
+  const unsigned long long nblk = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+  const unsigned long long bid =
+      blockIdx.x + (unsigned long long)gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z);
+  const unsigned long long per = ((bytes + nblk - 1) / nblk + 255) & ~255ull;
+  const unsigned long long lo = bid * per;
+  if (lo >= bytes) return;
+  const unsigned long long hi = lo + per < bytes ? lo + per : bytes;
+  const uint8_t* b = static_cast<const uint8_t*>(base);
+  for (unsigned long long o = lo; o < hi; o += 32768) {
+    const unsigned long long n = hi - o < 32768 ? hi - o : 32768;
+    l2_prefetch_bulk(b + o, (uint32_t)(n & ~15ull));
+  }
+}
+
 // ---------------------------------------------------------------- PDL
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {

@@ -25,6 +25,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "norm_embed.cuh"
 
 namespace tf {
 
@@ -69,6 +70,24 @@ struct GemmArgs {
   const float* ln_b;
   int trace;  // diagnostics slot (0 = off)
   int late_trigger;  // release the next kernel only after this kernel's PDL wait
+  // decode: activation-independent bytes of a later kernel (the next layer's
+  // copy of this weight matrix) streamed HBM -> L2 by this launch's CTAs
+  const void* l2pf;
+  unsigned long long l2pf_bytes;
+  // decode EPI_BIAS_RESID (swap, split-K): LayerNorm of the finished rows fused
+  // into the epilogue. Every CTA adds the number of features it stored for each
+  // token to lnf_cnt[token]; the CTA that completes a row (count == n_feat)
+  // normalises it (out row -> lnf_h row, same arithmetic as the stand-alone LN
+  // kernel) and resets the counter.
+  // ln_x set + ln_coop: the LayerNorm of the operand rows is computed
+  // cooperatively by the split-K cluster (each CTA loads and normalises only its
+  // own K slice; row statistics are exchanged over DSMEM), see ln_coop_build
+  int ln_coop;
+  int* lnf_cnt;
+  const float* lnf_g;
+  const float* lnf_b;
+  __half* lnf_h;
+  int lnf_ldh;
 };
 
 constexpr int kTileA = 128;          // MMA M
@@ -93,6 +112,15 @@ __host__ __device__ inline size_t gemm_ring_bytes(int bn, int stages, int splits
 // staging of the full source rows (k_blocks tiles of 64 columns)
 __host__ __device__ inline size_t gemm_ln_bytes(int bn, int kb_per_split, int k_blocks) {
   return (size_t)(kb_per_split + k_blocks) * bn * kBK * 2;
+}
+// cooperative LN operand: the CTA's K slice of the rows (kb_per_split tiles),
+// then f32 scratch: 2 exchange rounds [splits][bn], segment partials
+// [bn][ceil(kb_per_split*8/4)], mean / inv [bn] each, gamma / beta of the
+// slice [kb_per_split * 64] each
+__host__ __device__ inline int gemm_ln_coop_seg(int bn, int kb_per_split) { return bn * ((kb_per_split * 8 + 3) / 4); }
+__host__ __device__ inline size_t gemm_ln_coop_bytes(int bn, int kb_per_split, int splits) {
+  return (size_t)kb_per_split * bn * kBK * 2 +
+         (size_t)(2 * splits * bn + gemm_ln_coop_seg(bn, kb_per_split) + 2 * bn + 2 * kb_per_split * kBK) * 4;
 }
 // push-based split-K reduction (SWAP, splits > 1, bn <= 128): every CTA owns a
 // receive buffer for the S-1 peer slices of its 1/S share of the tile
@@ -493,6 +521,174 @@ __device__ __forceinline__ void epi_fin4(const GemmArgs& p, int tile_a, int tile
   }
 }
 
+// Fused LayerNorm tail of a split-K swap epilogue (see GemmArgs::lnf_cnt).
+// [u_lo, u_hi): this CTA's reduction units (unit u = token column u / 32,
+// features 4 * (u % 32) .. +3 of the tile). s_rows: >= bn ints of free smem
+// (the drained ring; written only after this CTA's partial tile is released).
+__device__ __forceinline__ void gemm_ln_tail(const GemmArgs& p, int tile_a, int tile_b, int u_lo, int u_hi,
+                                             int* s_rows) {
+  __shared__ int s_nrows;
+  __threadfence();  // release this CTA's x stores before its counter updates
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int nl = 0;
+    if (u_lo < u_hi) {
+      for (int c = u_lo / 32; c <= (u_hi - 1) / 32; ++c) {
+        const int tok = tile_b * p.bn + c;
+        if (tok >= p.m_tok) continue;
+        int n = 0;
+        for (int u = max(u_lo, c * 32); u < min(u_hi, c * 32 + 32); ++u)
+          n += max(0, min(4, p.n_feat - (tile_a * kTileA + (u % 32) * 4)));
+        if (n == 0) continue;
+        const int prev = atomicAdd(p.lnf_cnt + tok, n);
+        if (prev + n == p.n_feat) s_rows[nl++] = tok;
+      }
+    }
+    s_nrows = nl;
+  }
+  __syncthreads();
+  const int nl = s_nrows;
+  if (nl == 0) return;
+  __threadfence();  // acquire: every other CTA's stores of these rows
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NC = 4;  // H <= 1024; chunks past H are skipped (same sums as NC = ceil(H/256))
+  float4 gv[NC * 2], bv[NC * 2];
+  ln_load_gb<NC>(p.n_feat, p.lnf_g, p.lnf_b, lane, gv, bv);
+  for (int i = warp; i < nl; i += 4) {
+    const int tok = s_rows[i];
+    const __half* xr = p.out + (size_t)tok * p.ldo;
+    uint4 raw[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int c = (lane + 32 * j) * 8;
+      if (c < p.n_feat) raw[j] = __ldcg(reinterpret_cast<const uint4*>(xr + c));
+    }
+    float xv[NC * 8];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      if ((lane + 32 * j) * 8 < p.n_feat) {
+        unpack8(raw[j], &xv[8 * j]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xv[8 * j + e] = 0.0f;
+      }
+    }
+    ln_row_apply<NC>(xv, p.n_feat, gv, bv, p.lnf_h + (size_t)tok * p.lnf_ldh, lane);
+    if (lane == 0) p.lnf_cnt[tok] = 0;
+  }
+}
+
+__device__ __forceinline__ void st_dsmem_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
+// Cooperative LayerNorm of the B operand across the split-K cluster. The CTA
+// holds its K slice [kb0*64, (kb0+nkb)*64) of bn rows as swizzled tiles at
+// `bln`; the S CTAs of the cluster together hold the whole rows. Two exchange
+// rounds (row sums, then sums of squared deviations from the mean), each a
+// per-CTA partial written into every peer's `red` slot [rank][row] over DSMEM
+// and summed in rank order after a cluster barrier (deterministic), give the
+// reference's two-pass statistics (tensor.py:153-160: mean; c = x - mean;
+// var = mean(c*c); c * (1/sqrt(var + 1e-5)) * g + b); the CTA then normalises
+// its slice in place (f16, rows past m_tok zero). Cluster-barrier protocol on
+// entry: with `pending_arrive` the caller has already arrived once (push
+// reduction); on exit with `rearm` one arrive is left pending for the caller.
+__device__ __forceinline__ void ln_coop_build(const GemmArgs& p, int tile_b, int nkb, uint8_t* bln, float* sc,
+                                              bool pending_arrive, bool rearm) {
+  const int bn = p.bn, S = p.splits, tid = threadIdx.x;
+  const float H = (float)p.ln_H;
+  float* red0 = sc;                   // [S][bn]
+  float* red1 = red0 + S * bn;        // [S][bn]
+  float* seg = red1 + S * bn;         // [bn][nsr]
+  float* mean_s = seg + bn * ((nkb * 8 + 3) / 4);  // [bn]
+  float* inv_s = mean_s + bn;         // [bn]
+  const float* g_s = inv_s + bn;      // [nkb*64] gamma of the slice (staged by the caller)
+  const float* b_s = g_s + nkb * kBK;  // [nkb*64]
+  const uint32_t rank = S > 1 ? cluster_ctarank() : 0u;
+  const int C = nkb * 8;  // 16-byte chunks of one row in this slice
+  auto chunk_addr = [&](int r, int c) {
+    return bln + (size_t)(c >> 3) * bn * 128 + r * 128 + ((((c & 7) ^ (r & 7))) * 16);
+  };
+  // per-(row, segment) partials over fixed 4-chunk (32-feature) segments, then
+  // the per-row total in segment order (independent of bn: batch-invariant),
+  // then one write per peer
+  const int nsr = (C + 3) / 4;
+  auto round = [&](float* red, bool second) {
+    for (int idx = tid; idx < bn * nsr; idx += 128) {
+      const int r = idx / nsr, sg = idx - r * nsr;
+      const float m = second ? mean_s[r] : 0.0f;
+      float acc = 0.0f;
+      for (int c = 4 * sg; c < min(C, 4 * sg + 4); ++c) {
+        float xv[8];
+        unpack8(*reinterpret_cast<const uint4*>(chunk_addr(r, c)), xv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (second) {
+            const float d = __fsub_rn(xv[e], m);
+            acc = __fadd_rn(acc, __fmul_rn(d, d));
+          } else {
+            acc = __fadd_rn(acc, xv[e]);
+          }
+        }
+      }
+      seg[idx] = acc;
+    }
+    __syncthreads();
+    for (int r = tid; r < bn; r += 128) {
+      float tot = 0.0f;
+      for (int sg = 0; sg < nsr; ++sg) tot = __fadd_rn(tot, seg[r * nsr + sg]);
+      if (S > 1) {
+        const uint32_t a = smem_u32(red + (int)rank * bn + r);
+        for (int pr = 0; pr < S; ++pr) st_dsmem_f32(dsmem_addr(a, (uint32_t)pr), tot);
+      } else {
+        red[r] = tot;
+      }
+    }
+    __syncthreads();
+  };
+  if (S > 1) {
+    if (!pending_arrive) cluster_arrive_relaxed();
+    cluster_wait();  // every peer is running before its smem is written
+  }
+  round(red0, false);
+  if (S > 1) {
+    cluster_arrive();
+    cluster_wait();
+  }
+  for (int r = tid; r < bn; r += 128) {
+    float s = 0.0f;
+    for (int pr = 0; pr < S; ++pr) s = __fadd_rn(s, red0[pr * bn + r]);
+    mean_s[r] = __fdiv_rn(s, H);
+  }
+  __syncthreads();
+  round(red1, true);
+  if (S > 1) {
+    cluster_arrive();
+    cluster_wait();
+  }
+  for (int r = tid; r < bn; r += 128) {
+    float s = 0.0f;
+    for (int pr = 0; pr < S; ++pr) s = __fadd_rn(s, red1[pr * bn + r]);
+    inv_s[r] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(s, H), 1e-5f)));
+  }
+  __syncthreads();
+  for (int idx = tid; idx < bn * C; idx += 128) {
+    const int r = idx / C, c = idx - r * C;
+    uint8_t* a = chunk_addr(r, c);
+    float xv[8], y[8];
+    unpack8(*reinterpret_cast<const uint4*>(a), xv);
+    const bool valid = tile_b * bn + r < p.m_tok;
+    const float m = mean_s[r], iv = inv_s[r];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      y[e] = valid ? __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[e], m), iv), g_s[c * 8 + e]), b_s[c * 8 + e]) : 0.0f;
+    *reinterpret_cast<uint4*>(a) = pack8(y);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (S > 1 && rearm) cluster_arrive_relaxed();
+  __syncthreads();
+}
+
 template <int MODE, bool SWAP>
 __global__ void __launch_bounds__(128, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -504,7 +700,11 @@ __global__ void __launch_bounds__(128, 1)
   const int stage_bytes = gemm_stage_bytes(bn);
   const bool ln_mode = SWAP && p.ln_x != nullptr;
   uint8_t* bln = smem + gemm_ring_bytes(bn, stages, p.splits, SWAP);
-  uint8_t* recv = bln + (ln_mode ? gemm_ln_bytes(bn, p.kb_per_split, p.k_blocks) : 0);
+  const bool coop = ln_mode && p.ln_coop != 0;
+  uint8_t* recv = bln + (ln_mode ? (coop ? gemm_ln_coop_bytes(bn, p.kb_per_split, p.splits)
+                                         : gemm_ln_bytes(bn, p.kb_per_split, p.k_blocks))
+                                 : 0);
+  float* ln_sc = reinterpret_cast<float*>(bln + (size_t)p.kb_per_split * bn * kBK * 2);  // coop scratch
   uint8_t* stg = bln + (size_t)p.kb_per_split * bn * kBK * 2;  // LN source rows (ln_mode)
   const bool push = gemm_push_reduce(bn, p.splits, SWAP);
   uint64_t* bars = reinterpret_cast<uint64_t*>(recv + gemm_recv_bytes(bn, p.splits, SWAP));
@@ -562,7 +762,25 @@ __global__ void __launch_bounds__(128, 1)
       tma_load_2d(sa, &tmA, (kb0 + i) * kBK, tile_a * kTileA, full0 + 8 * i);
     }
   }
-  if (ln_mode) {  // stage the source rows by TMA, then all 128 threads build the normalised B tiles
+  if (warp == 3 && lane == 0) l2_prefetch_share(p.l2pf, p.l2pf_bytes);
+  if (coop) {
+    // gamma / beta of this CTA's K slice are weights: staged before the wait
+    float* g_s = ln_sc + 2 * p.splits * bn + gemm_ln_coop_seg(bn, p.kb_per_split) + 2 * bn;
+    for (int i = threadIdx.x; i < nkb * kBK; i += 128) {
+      const int f = kb0 * kBK + i;
+      g_s[i] = f < p.ln_H ? p.ln_g[f] : 0.0f;
+      g_s[nkb * kBK + i] = f < p.ln_H ? p.ln_b[f] : 0.0f;
+    }
+    pdl_wait();
+    if (warp == 0 && lane == 0) {
+      mbar_expect_tx(ln_bar, (uint32_t)(nkb * bn * kBK * 2));
+      for (int kb = 0; kb < nkb; ++kb)
+        tma_load_2d(smem_u32(bln + (size_t)kb * bn * kBK * 2), &tmB, (kb0 + kb) * kBK, tile_b * bn, ln_bar);
+    }
+    mbar_wait(ln_bar, 0);
+    __syncthreads();  // g_s / b_s visible
+    ln_coop_build(p, tile_b, nkb, bln, ln_sc, push, push);
+  } else if (ln_mode) {  // stage the source rows by TMA, then all 128 threads build the normalised B tiles
     pdl_wait();
     if (warp == 0 && lane == 0) {
       mbar_expect_tx(ln_bar, (uint32_t)(p.k_blocks * bn * kBK * 2));
@@ -753,6 +971,13 @@ __global__ void __launch_bounds__(128, 1)
     }
     if (threadIdx.x == 0) tr.mark(p.trace, 6);
     cluster_wait_any();  // partial tiles stay alive until every CTA has read them
+  }
+  if constexpr (MODE == EPI_BIAS_RESID && SWAP) {
+    if (p.lnf_cnt != nullptr && p.splits > 1) {
+      const int S = p.splits, U = (kTileA / 4) * bn, per = (U + S - 1) / S;
+      const int r = (int)cluster_ctarank();
+      gemm_ln_tail(p, tile_a, tile_b, r * per, min(U, r * per + per), reinterpret_cast<int*>(smem));
+    }
   }
   tc_fence_before();
   __syncthreads();

@@ -18,6 +18,7 @@
 #include "decode_mk.cuh"
 #include "common.cuh"
 #include "gemm_tc.cuh"
+#include "dgemm.cuh"
 #include "norm_embed.cuh"
 
 using namespace tf;
@@ -224,7 +225,7 @@ int pick_splits(int tiles, int k_blocks) {
   return best;
 }
 
-GemmPlan plan_gemm(const tf_gemm_desc& d) {
+GemmPlan plan_gemm(const tf_gemm_desc& d, bool ln_coop = false) {
   GemmPlan p{};
   p.k_blocks = (d.k + 63) / 64;
   p.swap = d.force_swap >= 0 ? d.force_swap != 0 : d.m_tok <= 256;
@@ -260,7 +261,7 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
         }
       p.splits = best;
     }
-    if (p.swap && d.ln_x && d.epilogue != TF_EPI_LOGITS) {
+    if (p.swap && d.ln_x && d.epilogue != TF_EPI_LOGITS && !ln_coop) {
       // fused LN: the CTA's normalised K-slice must fit beside the ring
       while (gemm_ln_bytes(p.bn, p.k_blocks / p.splits, p.k_blocks) > 128 * 1024) {
         int next = p.splits + 1;
@@ -274,7 +275,9 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
              "argmax epilogue does not support split-K");
   const int kb_per = p.k_blocks / p.splits;
   const int stage_bytes = gemm_stage_bytes(p.bn);
-  const size_t ln_bytes = (p.swap && d.ln_x) ? gemm_ln_bytes(p.bn, kb_per, p.k_blocks) : 0;
+  const size_t ln_bytes = (p.swap && d.ln_x) ? (ln_coop ? gemm_ln_coop_bytes(p.bn, kb_per, p.splits)
+                                                        : gemm_ln_bytes(p.bn, kb_per, p.k_blocks))
+                                             : 0;
   int st = (int)((kMaxSmem - 4096 - ln_bytes - gemm_recv_bytes(p.bn, p.splits, p.swap)) / stage_bytes);
   if (!p.swap) {  // leave room for the staged output tile (smem-bytes check below)
     while (st > 1 && gemm_smem_bytes(p.bn, st, p.splits, false) > kMaxSmem) --st;
@@ -294,7 +297,10 @@ void launch_gemm_t(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& 
                    const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
   ensure_gemm_attr<MODE, SWAP>();
   dim3 grid(p.tiles_a, p.tiles_b, p.splits);
-  const size_t ln_bytes = (SWAP && d.ln_x) ? gemm_ln_bytes(p.bn, p.k_blocks / p.splits, p.k_blocks) : 0;
+  const size_t ln_bytes =
+      (SWAP && d.ln_x) ? (args.ln_coop ? gemm_ln_coop_bytes(p.bn, p.k_blocks / p.splits, p.splits)
+                                       : gemm_ln_bytes(p.bn, p.k_blocks / p.splits, p.k_blocks))
+                       : 0;
   launch_cluster(gemm_tc_kernel<MODE, SWAP>, grid, dim3(128),
                  gemm_smem_bytes(p.bn, p.stages, p.splits, SWAP, ln_bytes), st, d.pdl != 0, p.splits, ta, tb, args);
 }
@@ -308,10 +314,28 @@ void launch_gemm_mode(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMa
     launch_gemm_t<MODE, false>(d, p, ta, tb, args, st);
 }
 
-void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
+// runtime-internal GEMM options (not part of the operator ABI)
+struct GemmExtra {
+  const void* l2pf = nullptr;  // HBM -> L2 prefetch range (next layer's operand)
+  unsigned long long l2pf_bytes = 0;
+  int ln_coop = 0;  // with desc.ln_x: cooperative cluster LayerNorm (gemm_tc.cuh ln_coop_build)
+  int* lnf_cnt = nullptr;  // fused LN of the finished rows (EPI_BIAS_RESID, swap, split-K)
+  const float* lnf_g = nullptr;
+  const float* lnf_b = nullptr;
+  void* lnf_h = nullptr;
+  int lnf_ldh = 0;
+};
+
+bool gemm_fuses_ln(const tf_gemm_desc& d) {
+  const GemmPlan p = plan_gemm(d);
+  return p.swap && p.splits > 1 && d.epilogue == TF_EPI_BIAS_RESID && d.n_feat <= 1024 && d.n_feat % 8 == 0 &&
+         d.ldo % 8 == 0;
+}
+
+void run_gemm(const tf_gemm_desc& d, cudaStream_t st, const GemmExtra& ex = GemmExtra{}) {
   TF_REQUIRE(d.m_tok > 0 && d.n_feat > 0 && d.k > 0, TF_ERR_SHAPE, "gemm: empty shape");
   TF_REQUIRE(d.act && d.wt, TF_ERR_ARG, "gemm: null operand");
-  const GemmPlan p = plan_gemm(d);
+  const GemmPlan p = plan_gemm(d, d.ln_x != nullptr && ex.ln_coop != 0);
   const int kext = p.k_blocks * 64;
   TF_REQUIRE(d.lda >= kext && d.ldw >= kext, TF_ERR_SHAPE,
              "gemm: leading dimensions must cover K padded to a multiple of 64");
@@ -344,6 +368,17 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
   a.qbase_dev = d.qbase_dev;
   a.keys = d.argmax_keys;
   a.late_trigger = d.pdl == 2 ? 1 : 0;
+  a.l2pf = ex.l2pf;
+  a.l2pf_bytes = ex.l2pf_bytes;
+  if (ex.lnf_cnt) {
+    TF_REQUIRE(gemm_fuses_ln(d) && ex.lnf_g && ex.lnf_b && ex.lnf_h && ex.lnf_ldh % 8 == 0, TF_ERR_ARG,
+               "gemm: fused epilogue LayerNorm not applicable");
+    a.lnf_cnt = ex.lnf_cnt;
+    a.lnf_g = ex.lnf_g;
+    a.lnf_b = ex.lnf_b;
+    a.lnf_h = static_cast<__half*>(ex.lnf_h);
+    a.lnf_ldh = ex.lnf_ldh;
+  }
   static const char* kGemmNames[] = {"gemm_f32", "gemm_bias", "gemm_gelu", "gemm_resid", "gemm_qkv", "gemm_logits"};
   a.trace = trace_next(d.epilogue >= 0 && d.epilogue < 6 ? kGemmNames[d.epilogue] : "gemm");
   if (d.ln_x) {
@@ -351,8 +386,11 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
     TF_REQUIRE(d.ln_gamma && d.ln_beta && d.ln_hidden > 0 && d.ln_hidden <= 1024 && d.ln_hidden % 8 == 0 &&
                    d.ln_ldx % 8 == 0 && d.ln_hidden <= kext,
                TF_ERR_ARG, "gemm: bad fused LayerNorm arguments");
-    TF_REQUIRE(gemm_ln_bytes(p.bn, p.k_blocks / p.splits, p.k_blocks) <= 128 * 1024, TF_ERR_UNSUPPORTED,
-               "gemm: fused LayerNorm tile too large");
+    TF_REQUIRE(ex.ln_coop || gemm_ln_bytes(p.bn, p.k_blocks / p.splits, p.k_blocks) <= 128 * 1024,
+               TF_ERR_UNSUPPORTED, "gemm: fused LayerNorm tile too large");
+    TF_REQUIRE(!ex.ln_coop || (d.ln_hidden == d.k && p.splits <= 16), TF_ERR_ARG,
+               "gemm: cooperative LayerNorm needs K == hidden");
+    a.ln_coop = ex.ln_coop;
     a.ln_x = static_cast<const __half*>(d.ln_x);
     a.ln_ldx = d.ln_ldx;
     a.ln_src_stride = d.ln_src_stride;
@@ -400,6 +438,119 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st) {
     case TF_EPI_BIAS_RESID: launch_gemm_mode<EPI_BIAS_RESID>(d, p, ta, tb, a, st); break;
     case TF_EPI_QKV: launch_gemm_mode<EPI_QKV>(d, p, ta, tb, a, st); break;
     case TF_EPI_LOGITS: launch_gemm_mode<EPI_LOGITS>(d, p, ta, tb, a, st); break;
+  }
+}
+
+// ------------------------------------------------------------------ small-batch decode GEMM
+struct DgPlan {
+  int bn, nkb, splits, tiles_f;
+};
+
+int dg_kb_max() {  // K blocks per CTA (TF_DG_KB, diagnostics)
+  static const int v = [] {
+    const char* e = getenv("TF_DG_KB");
+    return e ? std::max(1, atoi(e)) : 12;
+  }();
+  return v;
+}
+
+// dgemm_kernel applies when the whole batch fits one 16..64-row operand tile and
+// the CTA's K slice (<= dg_kb_max blocks, K split <= 4 ways) fits shared memory
+bool dg_plan(int m_tok, int n_feat, int k, DgPlan& pl) {
+  if (m_tok < 1 || m_tok > 64) return false;
+  pl.bn = std::max(16, (m_tok + 15) / 16 * 16);
+  const int kb = (k + 63) / 64;
+  int S = 1;
+  while (S <= 4 && (kb % S != 0 || kb / S > dg_kb_max())) ++S;
+  if (S > 4) return false;
+  pl.splits = S;
+  pl.nkb = kb / S;
+  pl.tiles_f = (n_feat + kDgRows - 1) / kDgRows;
+  return dg_smem_bytes(pl.bn, pl.nkb) <= kMaxSmem;
+}
+
+template <int MODE, int NC>
+void launch_dg(const DgPlan& pl, const CUtensorMap& tw, const CUtensorMap& ta, const DgArgs& a, cudaStream_t st,
+               bool pdl) {
+  static bool done = false;
+  if (!done) {
+    TF_CHECK_CUDA(cudaFuncSetAttribute(dgemm_kernel<MODE, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kMaxSmem));
+    set_max_carveout(dgemm_kernel<MODE, NC>);
+    done = true;
+  }
+  launch_cluster(dgemm_kernel<MODE, NC>, dim3(pl.tiles_f, 1, pl.splits), dim3(kDgThreads),
+                 dg_smem_bytes(pl.bn, pl.nkb), st, pdl, pl.splits, tw, ta, a);
+}
+
+template <int MODE>
+void launch_dg_ln(const DgPlan& pl, const CUtensorMap& tw, const CUtensorMap& ta, const DgArgs& a, cudaStream_t st,
+                  bool pdl) {
+  if (a.ln_g == nullptr) return launch_dg<MODE, 0>(pl, tw, ta, a, st, pdl);
+  switch ((a.ln_H / 8 + 31) / 32) {
+    case 1: return launch_dg<MODE, 1>(pl, tw, ta, a, st, pdl);
+    case 2: return launch_dg<MODE, 2>(pl, tw, ta, a, st, pdl);
+    case 3: return launch_dg<MODE, 3>(pl, tw, ta, a, st, pdl);
+    case 4: return launch_dg<MODE, 4>(pl, tw, ta, a, st, pdl);
+    default: throw TfError{TF_ERR_UNSUPPORTED, "dgemm: fused LayerNorm needs hidden <= 1024"};
+  }
+}
+
+// d: the usual GEMM descriptor (swap-AB decode shape, T == 1 for EPI_QKV);
+// ln_g/ln_b: fused LayerNorm of the operand rows (d.k == hidden) or null
+void run_dgemm(const tf_gemm_desc& d, const DgPlan& pl, const float* ln_g, const float* ln_b, const GemmExtra& ex,
+               cudaStream_t st) {
+  const int kext = pl.nkb * pl.splits * 64;
+  TF_REQUIRE(d.lda >= kext && d.ldw >= kext && d.lda % 8 == 0 && d.ldw % 8 == 0 && d.ldo % 8 == 0, TF_ERR_SHAPE,
+             "dgemm: leading dimensions");
+  TF_REQUIRE(pl.splits == 1 || (d.epilogue != TF_EPI_QKV && d.n_feat % 4 == 0), TF_ERR_ARG, "dgemm: split epilogue");
+  TF_REQUIRE(d.n_feat % 8 == 0, TF_ERR_SHAPE, "dgemm: features must be a multiple of 8");
+  TF_REQUIRE(ln_g == nullptr || (d.k % 8 == 0 && d.k <= 1024 && pl.splits == 1), TF_ERR_ARG,
+             "dgemm: fused LayerNorm needs the whole row in one CTA");
+  DgArgs a{};
+  a.m_tok = d.m_tok;
+  a.n_feat = d.n_feat;
+  a.bn = pl.bn;
+  a.nkb = pl.nkb;
+  a.splits = pl.splits;
+  a.bias = d.bias;
+  a.out = static_cast<__half*>(d.out);
+  a.ldo = d.ldo;
+  a.resid = static_cast<const __half*>(d.resid);
+  a.ldr = d.ldr;
+  a.q_out = static_cast<__half*>(d.q_out);
+  a.ldq = d.ldq;
+  a.kc = static_cast<__half*>(d.k_cache);
+  a.vc = static_cast<__half*>(d.v_cache);
+  a.H = d.hidden;
+  a.NH = d.heads;
+  a.D = d.head_dim;
+  a.cap = d.cap;
+  a.qbase_dev = d.qbase_dev;
+  a.ln_g = ln_g;
+  a.ln_b = ln_b;
+  a.ln_H = d.k;
+  a.l2pf = ex.l2pf;
+  a.l2pf_bytes = ex.l2pf_bytes;
+  const CUtensorMap tw = make_kmajor_map(d.wt, d.n_feat, kext, d.ldw, kDgRows);
+  const CUtensorMap ta = make_kmajor_map(d.act, d.m_tok, kext, d.lda, pl.bn);
+  const bool pdl = d.pdl != 0;
+  switch (d.epilogue) {
+    case TF_EPI_QKV:
+      TF_REQUIRE(d.head_dim % 8 == 0 && d.seq_len == 1, TF_ERR_ARG, "dgemm: qkv routing");
+      a.trace = trace_next("dg_qkv");
+      launch_dg_ln<EPI_QKV>(pl, tw, ta, a, st, pdl);
+      break;
+    case TF_EPI_BIAS_RESID:
+      a.trace = trace_next("dg_resid");
+      launch_dg<EPI_BIAS_RESID, 0>(pl, tw, ta, a, st, pdl);
+      break;
+    case TF_EPI_BIAS_GELU:
+      a.trace = trace_next("dg_gelu");
+      launch_dg_ln<EPI_BIAS_GELU>(pl, tw, ta, a, st, pdl);
+      break;
+    default:
+      throw TfError{TF_ERR_UNSUPPORTED, "dgemm: epilogue"};
   }
 }
 
@@ -638,6 +789,72 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     d.ln_beta = bet;
   };
 
+  // decode: every kernel of layer l streams the next layer's copy of its own
+  // operand (weights; the attention its KV window) HBM -> L2, so the chain of
+  // latency-bound kernels reads L2 while HBM runs a layer ahead. The last
+  // layer's GEMMs stream a quarter of the lm_head each instead.
+  static const bool l2pf_on = [] {  // TF_L2PF=0 disables (A/B diagnostics)
+    const char* e = getenv("TF_L2PF");
+    return !(e && e[0] == '0');
+  }();
+  const bool l2pf = l2pf_on && T == 1;
+  const unsigned long long lm_bytes = (unsigned long long)m.vocab * m.ldk_h * 2;
+  const unsigned long long lm_q = ((lm_bytes / 4) + 255) & ~255ull;
+  auto pf_next = [&](int l, int which) {
+    GemmExtra ex;
+    const void*& ptr = ex.l2pf;
+    unsigned long long& bytes = ex.l2pf_bytes;
+    if (!l2pf) return ex;
+    if (l + 1 < L) {
+      const tf_layer_weights& n = s.m->layers[l + 1];
+      switch (which) {
+        case 0: ptr = n.wqkv_t; bytes = 3ull * H * m.ldk_h * 2; break;
+        case 1: ptr = n.wo_t; bytes = (unsigned long long)H * m.ldk_h * 2; break;
+        case 2: ptr = n.w1_t; bytes = (unsigned long long)F * m.ldk_h * 2; break;
+        default: ptr = n.w2_t; bytes = (unsigned long long)H * m.ldk_f * 2; break;
+      }
+    } else {
+      const unsigned long long lo = which * lm_q;
+      if (lo >= lm_bytes) return ex;
+      ptr = static_cast<const uint8_t*>(m.lm_head_t) + lo;
+      bytes = std::min(lm_q, lm_bytes - lo);
+    }
+    return ex;
+  };
+  // decode: the LayerNorms after the two residual GEMMs run in those GEMMs'
+  // epilogues (last CTA to finish a row normalises it) instead of as kernels
+  // (measured slower than the LN launch it replaces: opt-in TF_LN_EPI=1)
+  static const bool lnf_on = [] {
+    const char* e = getenv("TF_LN_EPI");
+    return e && e[0] == '1';
+  }();
+  int* ln_cnt = (lnf_on && T == 1 && !fuse_ln && sd.counters && sd.n_counters >= B * NH + M)
+                    ? sd.counters + B * NH
+                    : nullptr;
+
+  // small-batch decode: narrow-tile whole-K GEMMs with the LayerNorms fused
+  // into the QKV / FFN1 operand (dgemm.cuh). Opt-in (TF_DGEMM=1): the whole-K
+  // MMA chain (~35 cycles per tcgen05.mma issue) and the per-CTA LayerNorm of
+  // all rows cost more than the split-K reduction they remove.
+  static const bool dg_on = [] {
+    const char* e = getenv("TF_DGEMM");
+    return e && e[0] == '1';
+  }();
+  DgPlan pq{}, po{}, p1{}, p2{};
+  const bool dg = dg_on && T == 1 && !fuse_ln && D % 8 == 0 && H % 8 == 0 && H <= 1024 &&
+                  dg_plan(M, 3 * H, H, pq) && dg_plan(M, H, H, po) && dg_plan(M, F, H, p1) && dg_plan(M, H, F, p2) &&
+                  pq.splits == 1 && p1.splits == 1;
+  if (dg) ln_cnt = nullptr;
+  // decode: attn_norm / ffn_norm computed by the consuming QKV / FFN1 split-K
+  // cluster (cooperative LN, gemm_tc.cuh) instead of stand-alone launches.
+  // Opt-in (TF_LN_COOP=1): measured slower in the PDL-chained step
+  static const bool coop_on = [] {
+    const char* e = getenv("TF_LN_COOP");
+    return e && e[0] == '1';
+  }();
+  const bool coop = coop_on && !dg && !fuse_ln && T == 1 && M <= 256 && H <= 1024 && H % 8 == 0 && m.ldk_h % 8 == 0;
+  if (coop) ln_cnt = nullptr;
+
   for (int l = 0; l < L; ++l) {
     const tf_layer_weights& w = s.m->layers[l];
     // fused QKV projection, K/V straight into the cache (model.py:464-474)
@@ -661,6 +878,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     q.cap = sd.capacity;
     q.seq_len = T;
     q.qbase_dev = sd.len_dev;
+    if (coop) set_ln(q, w.ln1_gamma, w.ln1_beta, 1, 0);
     static const bool qkv_late = [] {  // TF_QKV_LATE=0 disables (A/B diagnostics)
       const char* e = getenv("TF_QKV_LATE");
       return !(e && e[0] == '0');
@@ -668,7 +886,14 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     // decode: attention (next) prefetches the whole KV window; release it only
     // once the QKV weights are in (after this GEMM's own dependency wait)
     if (pdl && T == 1 && qkv_late) q.pdl = 2;
-    run_gemm(q, st);
+    if (dg) {
+      q.act = x;  // attn_norm (model.py:460-462) runs on the operand inside the GEMM
+      run_dgemm(q, pq, w.ln1_gamma, w.ln1_beta, pf_next(l, 0), st);
+    } else {
+      GemmExtra qex = pf_next(l, 0);
+      qex.ln_coop = coop ? 1 : 0;
+      run_gemm(q, st, qex);
+    }
     ++launches;
     // attention over slots [pad_b, len + t] (model.py:475-478)
     AttnArgs at{};
@@ -698,6 +923,10 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
         at.cnt = sd.counters;
         at.max_chunks = chunks;
       }
+      if (l2pf && l + 1 < L) {
+        at.pf_kc = static_cast<const __half*>(sd.k_cache) + (l + 1) * layer_cache;
+        at.pf_vc = static_cast<const __half*>(sd.v_cache) + (l + 1) * layer_cache;
+      }
     }
     run_attention(at, st, pdl);
     ++launches;
@@ -715,7 +944,19 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     o.ldo = m.ldk_h;
     o.resid = x;
     o.ldr = m.ldk_h;
-    run_gemm(o, st);
+    GemmExtra oex = pf_next(l, 1);
+    const bool o_ln = ln_cnt && gemm_fuses_ln(o);
+    if (o_ln) {
+      oex.lnf_cnt = ln_cnt;
+      oex.lnf_g = w.ln2_gamma;
+      oex.lnf_b = w.ln2_beta;
+      oex.lnf_h = h;
+      oex.lnf_ldh = m.ldk_h;
+    }
+    if (dg)
+      run_dgemm(o, po, nullptr, nullptr, oex, st);
+    else
+      run_gemm(o, st, oex);
     ++launches;
     // ffn_norm (model.py:484-486)
     LnArgs ln{};
@@ -729,7 +970,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     ln.b = w.ln2_beta;
     ln.h = h;
     ln.ldh = m.ldk_h;
-    if (!fuse_ln) {
+    if (!fuse_ln && !o_ln && !dg && !coop) {
       run_ln(ln, st, pdl);
       ++launches;
     }
@@ -746,7 +987,17 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     f1.bias = w.b1;
     f1.out = sd.ffn;
     f1.ldo = m.ldk_f;
-    run_gemm(f1, st);
+    if (dg) {
+      f1.act = x;  // ffn_norm (model.py:484-486) inside the GEMM
+      run_dgemm(f1, p1, w.ln2_gamma, w.ln2_beta, pf_next(l, 2), st);
+    } else {
+      GemmExtra f1ex = pf_next(l, 2);
+      if (coop) {
+        set_ln(f1, w.ln2_gamma, w.ln2_beta, 1, 0);
+        f1ex.ln_coop = 1;
+      }
+      run_gemm(f1, st, f1ex);
+    }
     ++launches;
     // FFN2 + residual (model.py:491-494)
     tf_gemm_desc f2 = g;
@@ -762,8 +1013,6 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     f2.ldo = m.ldk_h;
     f2.resid = x;
     f2.ldr = m.ldk_h;
-    run_gemm(f2, st);
-    ++launches;
     // next layer's attn_norm, or final_norm (model.py:460-462, 497-498)
     LnArgs nl = ln;
     if (l + 1 < L) {
@@ -778,6 +1027,22 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
         nl.src_off = T - 1;
       }
     }
+    GemmExtra f2ex = pf_next(l, 3);
+    const bool f2_ln = ln_cnt && gemm_fuses_ln(f2);
+    if (f2_ln) {  // T == 1: every row is the last position
+      f2ex.lnf_cnt = ln_cnt;
+      f2ex.lnf_g = nl.g;
+      f2ex.lnf_b = nl.b;
+      f2ex.lnf_h = h;
+      f2ex.lnf_ldh = m.ldk_h;
+    }
+    if (dg)
+      run_dgemm(f2, p2, nullptr, nullptr, f2ex, st);
+    else
+      run_gemm(f2, st, f2ex);
+    ++launches;
+    if (f2_ln) continue;
+    if ((dg || coop) && l + 1 < L) continue;  // the next QKV normalises its own operand
     if (l + 1 < L ? !fuse_ln : !fuse_final) {
       run_ln(nl, st, pdl);
       ++launches;
