@@ -74,16 +74,15 @@ struct GemmArgs {
   // copy of this weight matrix) streamed HBM -> L2 by this launch's CTAs
   const void* l2pf;
   unsigned long long l2pf_bytes;
-  // decode EPI_BIAS_RESID (swap, split-K): LayerNorm of the finished rows fused
-  // into the epilogue. Every CTA adds the number of features it stored for each
-  // token to lnf_cnt[token]; the CTA that completes a row (count == n_feat)
-  // normalises it (out row -> lnf_h row, same arithmetic as the stand-alone LN
-  // kernel) and resets the counter.
   // ln_x set + ln_coop: the LayerNorm of the operand rows is computed
   // cooperatively by the split-K cluster (each CTA loads and normalises only its
   // own K slice; row statistics are exchanged over DSMEM), see ln_coop_build
   int ln_coop;
-  int* lnf_cnt;
+  // decode EPI_BIAS_RESID with the whole output row in one cluster (grid =
+  // cluster = tiles_a x 1 x 2): split-K pair reduction plus the LayerNorm of
+  // the new residual rows over DSMEM (gemm_rowln_epilogue); writes out (x) and
+  // lnf_h = q16(LN(x)) with lnf_g / lnf_b
+  int row_ln;
   const float* lnf_g;
   const float* lnf_b;
   __half* lnf_h;
@@ -521,63 +520,6 @@ __device__ __forceinline__ void epi_fin4(const GemmArgs& p, int tile_a, int tile
   }
 }
 
-// Fused LayerNorm tail of a split-K swap epilogue (see GemmArgs::lnf_cnt).
-// [u_lo, u_hi): this CTA's reduction units (unit u = token column u / 32,
-// features 4 * (u % 32) .. +3 of the tile). s_rows: >= bn ints of free smem
-// (the drained ring; written only after this CTA's partial tile is released).
-__device__ __forceinline__ void gemm_ln_tail(const GemmArgs& p, int tile_a, int tile_b, int u_lo, int u_hi,
-                                             int* s_rows) {
-  __shared__ int s_nrows;
-  __threadfence();  // release this CTA's x stores before its counter updates
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int nl = 0;
-    if (u_lo < u_hi) {
-      for (int c = u_lo / 32; c <= (u_hi - 1) / 32; ++c) {
-        const int tok = tile_b * p.bn + c;
-        if (tok >= p.m_tok) continue;
-        int n = 0;
-        for (int u = max(u_lo, c * 32); u < min(u_hi, c * 32 + 32); ++u)
-          n += max(0, min(4, p.n_feat - (tile_a * kTileA + (u % 32) * 4)));
-        if (n == 0) continue;
-        const int prev = atomicAdd(p.lnf_cnt + tok, n);
-        if (prev + n == p.n_feat) s_rows[nl++] = tok;
-      }
-    }
-    s_nrows = nl;
-  }
-  __syncthreads();
-  const int nl = s_nrows;
-  if (nl == 0) return;
-  __threadfence();  // acquire: every other CTA's stores of these rows
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NC = 4;  // H <= 1024; chunks past H are skipped (same sums as NC = ceil(H/256))
-  float4 gv[NC * 2], bv[NC * 2];
-  ln_load_gb<NC>(p.n_feat, p.lnf_g, p.lnf_b, lane, gv, bv);
-  for (int i = warp; i < nl; i += 4) {
-    const int tok = s_rows[i];
-    const __half* xr = p.out + (size_t)tok * p.ldo;
-    uint4 raw[NC];
-#pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      const int c = (lane + 32 * j) * 8;
-      if (c < p.n_feat) raw[j] = __ldcg(reinterpret_cast<const uint4*>(xr + c));
-    }
-    float xv[NC * 8];
-#pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      if ((lane + 32 * j) * 8 < p.n_feat) {
-        unpack8(raw[j], &xv[8 * j]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) xv[8 * j + e] = 0.0f;
-      }
-    }
-    ln_row_apply<NC>(xv, p.n_feat, gv, bv, p.lnf_h + (size_t)tok * p.lnf_ldh, lane);
-    if (lane == 0) p.lnf_cnt[tok] = 0;
-  }
-}
-
 __device__ __forceinline__ void st_dsmem_f32(uint32_t addr, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
@@ -689,7 +631,112 @@ __device__ __forceinline__ void ln_coop_build(const GemmArgs& p, int tile_b, int
   __syncthreads();
 }
 
-template <int MODE, bool SWAP>
+// Scratch the row-LN epilogue needs in the drained ring: the parked partial
+// tile [bn][128] f32, the finished values [bn/2][128] f32, exchange slots
+// [2][TA][bn/2], warp partials [2][4][bn/2], mean / inv [bn/2].
+__host__ __device__ inline size_t gemm_rowln_scratch_bytes(int bn, int tiles_a) {
+  const int bh = bn / 2;
+  return (size_t)kTileA * bn * 4 + (size_t)kTileA * bh * 4 + (size_t)(2 * tiles_a * bh + 10 * bh) * 4;
+}
+
+// Row-LN epilogue (see GemmArgs::row_ln). The cluster is the whole grid: CTA
+// (x, z) holds the f32 partial of features [128x, 128x+128) over K half z.
+// CTA (x, z) finalises tokens [z*bn/2, (z+1)*bn/2): acc = p0 + p1 (split
+// order), v = q16(x + q16(acc + b)) (model.py:478-482 / 491-494, bit-identical
+// to the other epilogues), then the LayerNorm of each token row over the TA
+// CTAs that share z (tensor.py:153-160 two-pass form: per-CTA column sums ->
+// every peer over DSMEM -> summed in CTA order after a cluster barrier; then the
+// same for the squared deviations). Deterministic; per-token, so batch-invariant.
+// Loops are kept rolled: the executed path stays short for the i-cache.
+__device__ __noinline__ void gemm_rowln_epilogue(const GemmArgs& p, uint32_t trow, uint8_t* smem) {
+  const int TA = gridDim.x, x = blockIdx.x, z = blockIdx.z;
+  const int bn = p.bn, bh = bn / 2, t0 = z * bh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int f = x * kTileA + tid;
+  const bool fok = f < p.n_feat;
+  const float H = (float)p.n_feat;
+  float* part = reinterpret_cast<float*>(smem);  // [bn][128]
+  float* vals = part + kTileA * bn;              // [bh][128]
+  float* red = vals + kTileA * bh;               // [2][TA][bh]
+  float* wsum = red + 2 * TA * bh;               // [2][4][bh]
+  float* mean = wsum + 8 * bh;                   // [bh]
+  float* inv = mean + bh;                        // [bh]
+  for (int c = 0; c < bn; c += 16) {
+    float v[16];
+    tmem_ld16(trow + (uint32_t)c, v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) part[(c + j) * kTileA + tid] = v[j];
+  }
+  const float bias = fok ? p.bias[f] : 0.0f;
+  cluster_arrive();
+  cluster_wait();  // every partial tile parked
+  const uint32_t loc = smem_u32(part) + (uint32_t)((t0 * kTileA + tid) * 4);
+  const uint32_t a0 = dsmem_addr(loc, (uint32_t)x), a1 = dsmem_addr(loc, (uint32_t)(x + TA));
+#pragma unroll 4
+  for (int t = 0; t < bh; ++t) {
+    const int tok = t0 + t;
+    const float p0 = ld_dsmem_f32(a0 + (uint32_t)(t * kTileA * 4));
+    const float p1 = ld_dsmem_f32(a1 + (uint32_t)(t * kTileA * 4));
+    const float xo = (fok && tok < p.m_tok) ? __half2float(p.resid[(size_t)tok * p.ldr + f]) : 0.0f;
+    const float acc = __fadd_rn(__fadd_rn(0.0f, p0), p1);
+    vals[t * kTileA + tid] = (fok && tok < p.m_tok) ? q16(__fadd_rn(xo, q16(__fadd_rn(acc, bias)))) : 0.0f;
+  }
+  for (int rnd = 0; rnd < 2; ++rnd) {
+    float* w = wsum + rnd * 4 * bh;
+    float* rr = red + rnd * TA * bh;
+    for (int t = 0; t < bh; ++t) {
+      const float v = vals[t * kTileA + tid];
+      float q = v;
+      if (rnd == 1) {
+        const float d = fok ? __fsub_rn(v, mean[t]) : 0.0f;
+        q = __fmul_rn(d, d);
+      }
+      q = warp_sum(q);
+      if (lane == 0) w[warp * bh + t] = q;
+    }
+    __syncthreads();
+    if (tid < bh) {
+      const float tot = __fadd_rn(__fadd_rn(__fadd_rn(w[tid], w[bh + tid]), w[2 * bh + tid]), w[3 * bh + tid]);
+      const uint32_t ad = smem_u32(rr + x * bh + tid);
+      for (int xx = 0; xx < TA; ++xx) st_dsmem_f32(dsmem_addr(ad, (uint32_t)(xx + TA * z)), tot);
+    }
+    cluster_arrive();
+    cluster_wait();
+    if (tid < bh) {
+      float s = 0.0f;
+      for (int xx = 0; xx < TA; ++xx) s = __fadd_rn(s, rr[xx * bh + tid]);
+      if (rnd == 0)
+        mean[tid] = __fdiv_rn(s, H);
+      else
+        inv[tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(s, H), 1e-5f)));
+    }
+    __syncthreads();
+  }
+  if (fok) {
+    const float gam = p.lnf_g[f], bet = p.lnf_b[f];
+    for (int t = 0; t < bh; ++t) {
+      const int tok = t0 + t;
+      if (tok >= p.m_tok) break;
+      const float v = vals[t * kTileA + tid];
+      p.out[(size_t)tok * p.ldo + f] = __float2half_rn(v);
+      p.lnf_h[(size_t)tok * p.lnf_ldh + f] =
+          f16_sat(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v, mean[t]), inv[t]), gam), bet));
+    }
+  }
+}
+
+// Reduction / epilogue path of a launch (template parameter, so every
+// instantiation carries only the code it executes: decode kernels are
+// i-cache-bound when they carry all paths)
+enum GemmRed : int {
+  RED_ONE = 0,    // splits == 1 (full-K tile; non-swap staged epilogue or per-chunk stores)
+  RED_PUSH = 1,   // split-K cluster, push form (swap, bn <= 128)
+  RED_PULL = 2,   // split-K cluster, pull form
+  RED_ROWLN = 3,  // whole-row cluster + fused LayerNorm (EPI_BIAS_RESID, swap)
+};
+// LayerNorm of the B operand built in-kernel: 0 none, 1 full-row staging
+// (ln_build_b), 2 cluster-cooperative (ln_coop_build)
+template <int MODE, bool SWAP, int RED, int LNV>
 __global__ void __launch_bounds__(128, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs p) {
@@ -698,15 +745,15 @@ __global__ void __launch_bounds__(128, 1)
                                              ~static_cast<uintptr_t>(1023));
   const int bn = p.bn, stages = p.stages;
   const int stage_bytes = gemm_stage_bytes(bn);
-  const bool ln_mode = SWAP && p.ln_x != nullptr;
+  constexpr bool ln_mode = SWAP && LNV != 0;
   uint8_t* bln = smem + gemm_ring_bytes(bn, stages, p.splits, SWAP);
-  const bool coop = ln_mode && p.ln_coop != 0;
+  constexpr bool coop = ln_mode && LNV == 2;
   uint8_t* recv = bln + (ln_mode ? (coop ? gemm_ln_coop_bytes(bn, p.kb_per_split, p.splits)
                                          : gemm_ln_bytes(bn, p.kb_per_split, p.k_blocks))
                                  : 0);
   float* ln_sc = reinterpret_cast<float*>(bln + (size_t)p.kb_per_split * bn * kBK * 2);  // coop scratch
   uint8_t* stg = bln + (size_t)p.kb_per_split * bn * kBK * 2;  // LN source rows (ln_mode)
-  const bool push = gemm_push_reduce(bn, p.splits, SWAP);
+  constexpr bool push = RED == RED_PUSH;
   uint64_t* bars = reinterpret_cast<uint64_t*>(recv + gemm_recv_bytes(bn, p.splits, SWAP));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 3);
   __shared__ unsigned long long red[64];
@@ -740,7 +787,7 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   // push reduction: peers may signal this CTA's recv_bar only after it is
   // initialised; the matching wait sits right before the first push
-  if (push) cluster_arrive_relaxed();
+  if constexpr (push) cluster_arrive_relaxed();
   const uint32_t tmem = *tmem_slot;
   // let the next kernel in the stream launch now: its prologue (barrier init,
   // TMEM alloc, weight TMA prefetch) overlaps this kernel; it still waits on
@@ -763,7 +810,7 @@ __global__ void __launch_bounds__(128, 1)
     }
   }
   if (warp == 3 && lane == 0) l2_prefetch_share(p.l2pf, p.l2pf_bytes);
-  if (coop) {
+  if constexpr (coop) {
     // gamma / beta of this CTA's K slice are weights: staged before the wait
     float* g_s = ln_sc + 2 * p.splits * bn + gemm_ln_coop_seg(bn, p.kb_per_split) + 2 * bn;
     for (int i = threadIdx.x; i < nkb * kBK; i += 128) {
@@ -780,7 +827,7 @@ __global__ void __launch_bounds__(128, 1)
     mbar_wait(ln_bar, 0);
     __syncthreads();  // g_s / b_s visible
     ln_coop_build(p, tile_b, nkb, bln, ln_sc, push, push);
-  } else if (ln_mode) {  // stage the source rows by TMA, then all 128 threads build the normalised B tiles
+  } else if constexpr (ln_mode) {  // stage the source rows by TMA, then all 128 threads build the normalised B tiles
     pdl_wait();
     if (warp == 0 && lane == 0) {
       mbar_expect_tx(ln_bar, (uint32_t)(p.k_blocks * bn * kBK * 2));
@@ -840,14 +887,23 @@ __global__ void __launch_bounds__(128, 1)
   const int ra = tile_a * kTileA + row;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   float v[16];
-  if (!SWAP && p.splits == 1 && (MODE != EPI_LOGITS || p.keys == nullptr)) {
-    epi_tile_nonswap<MODE>(p, tile_a, tile_b, tmem + (uint32_t)(warp * 32 << 16), smem);
-  } else if (p.splits == 1) {
+  if constexpr (RED == RED_ROWLN) {
+    if constexpr (MODE == EPI_BIAS_RESID && SWAP) gemm_rowln_epilogue(p, trow, smem);
+  } else if constexpr (RED == RED_ONE && !SWAP) {
+    if (MODE != EPI_LOGITS || p.keys == nullptr) {
+      epi_tile_nonswap<MODE>(p, tile_a, tile_b, tmem + (uint32_t)(warp * 32 << 16), smem);
+    } else {
+      for (int c = 0; c < bn; c += 16) {
+        tmem_ld16(trow + (uint32_t)c, v);
+        epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, reinterpret_cast<unsigned long long*>(smem));
+      }
+    }
+  } else if constexpr (RED == RED_ONE) {
     for (int c = 0; c < bn; c += 16) {
       tmem_ld16(trow + (uint32_t)c, v);
       epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, reinterpret_cast<unsigned long long*>(smem));
     }
-  } else if (push) {
+  } else if constexpr (RED == RED_PUSH) {
     // Split-K across the CTAs of one cluster, push form. Each CTA parks its f32
     // partial tile ([column][128 rows], in the drained ring), then one thread
     // bulk-copies the slice owned by every peer r (units [r*per, r*per+per),
@@ -916,6 +972,7 @@ __global__ void __launch_bounds__(128, 1)
       bulk_wait_read_all();  // outgoing slices read before this smem is released
     }
   } else {
+    static_assert(RED == RED_PULL, "reduction path");
     // Split-K across the CTAs of one thread-block cluster (grid.z == cluster.z
     // == splits). Each CTA parks its f32 partial tile in its own (drained)
     // pipeline smem as [column][128 rows]; after a cluster barrier every CTA
@@ -971,13 +1028,6 @@ __global__ void __launch_bounds__(128, 1)
     }
     if (threadIdx.x == 0) tr.mark(p.trace, 6);
     cluster_wait_any();  // partial tiles stay alive until every CTA has read them
-  }
-  if constexpr (MODE == EPI_BIAS_RESID && SWAP) {
-    if (p.lnf_cnt != nullptr && p.splits > 1) {
-      const int S = p.splits, U = (kTileA / 4) * bn, per = (U + S - 1) / S;
-      const int r = (int)cluster_ctarank();
-      gemm_ln_tail(p, tile_a, tile_b, r * per, min(U, r * per + per), reinterpret_cast<int*>(smem));
-    }
   }
   tc_fence_before();
   __syncthreads();

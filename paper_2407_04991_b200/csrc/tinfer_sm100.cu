@@ -99,6 +99,31 @@ CUtensorMap make_kmajor_map(const void* ptr, int rows, int k_extent, int ld, int
 
 // ------------------------------------------------------------------ launch helper
 template <typename Kern, typename... Args>
+void launch_cluster3(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl, dim3 cluster,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  attr[n].id = cudaLaunchAttributeClusterDimension;
+  attr[n].val.clusterDim.x = cluster.x;
+  attr[n].val.clusterDim.y = cluster.y;
+  attr[n].val.clusterDim.z = cluster.z;
+  ++n;
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  TF_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
+template <typename Kern, typename... Args>
 void launch_cluster(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
                     int cluster_z, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -190,15 +215,15 @@ void set_max_carveout(K kern) {
                                        (int)cudaSharedmemCarveoutMaxShared));
 }
 
-template <int MODE, bool SWAP>
+template <int MODE, bool SWAP, int RED, int LNV>
 void ensure_gemm_attr() {
   static bool done = false;
   if (!done) {
-    TF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<MODE, SWAP>,
+    TF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<MODE, SWAP, RED, LNV>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
-    TF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<MODE, SWAP>,
+    TF_CHECK_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<MODE, SWAP, RED, LNV>,
                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    set_max_carveout(gemm_tc_kernel<MODE, SWAP>);
+    set_max_carveout(gemm_tc_kernel<MODE, SWAP, RED, LNV>);
     done = true;
   }
 }
@@ -213,14 +238,17 @@ struct GemmPlan {
 // batch, so decode results are batch-invariant. Splits form one cluster per
 // tile: up to 8 (portable) when there are many tiles, up to 16 (non-portable,
 // one cluster per GPC) when a few tiles must cover the machine.
+// The largest split count whose grid stays within 128 CTAs: every cluster is
+// then co-resident in one wave (a 144-CTA grid of 6-CTA clusters measured a
+// second wave at batch 128: FFN1 22 -> 13 us).
 int pick_splits(int tiles, int k_blocks) {
   const int target = 128;
   const int cap = tiles >= 16 ? 8 : 16;
   int best = 1;
   for (int d = 1; d <= k_blocks && d <= cap; ++d) {
     if (k_blocks % d) continue;
+    if (tiles * d > target) break;
     best = d;
-    if (tiles * d >= target) break;
   }
   return best;
 }
@@ -292,17 +320,56 @@ GemmPlan plan_gemm(const tf_gemm_desc& d, bool ln_coop = false) {
   return p;
 }
 
+template <int MODE, bool SWAP, int RED, int LNV>
+void launch_gemm_v(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& ta, const CUtensorMap& tb,
+                   const GemmArgs& args, cudaStream_t st) {
+  ensure_gemm_attr<MODE, SWAP, RED, LNV>();
+  dim3 grid(p.tiles_a, p.tiles_b, p.splits);
+  const size_t ln_bytes =
+      LNV == 2 ? gemm_ln_coop_bytes(p.bn, p.k_blocks / p.splits, p.splits)
+               : (LNV == 1 ? gemm_ln_bytes(p.bn, p.k_blocks / p.splits, p.k_blocks) : 0);
+  const size_t smem = gemm_smem_bytes(p.bn, p.stages, p.splits, SWAP, ln_bytes);
+  if (RED == RED_ROWLN)
+    launch_cluster3(gemm_tc_kernel<MODE, SWAP, RED, LNV>, grid, dim3(128), smem, st, d.pdl != 0, grid, ta, tb, args);
+  else
+    launch_cluster(gemm_tc_kernel<MODE, SWAP, RED, LNV>, grid, dim3(128), smem, st, d.pdl != 0, p.splits, ta, tb,
+                   args);
+}
+
+// One kernel instantiation per (epilogue, operand order, reduction path,
+// operand LayerNorm): each carries only the code it executes.
 template <int MODE, bool SWAP>
 void launch_gemm_t(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& ta,
                    const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
-  ensure_gemm_attr<MODE, SWAP>();
-  dim3 grid(p.tiles_a, p.tiles_b, p.splits);
-  const size_t ln_bytes =
-      (SWAP && d.ln_x) ? (args.ln_coop ? gemm_ln_coop_bytes(p.bn, p.k_blocks / p.splits, p.splits)
-                                       : gemm_ln_bytes(p.bn, p.k_blocks / p.splits, p.k_blocks))
-                       : 0;
-  launch_cluster(gemm_tc_kernel<MODE, SWAP>, grid, dim3(128),
-                 gemm_smem_bytes(p.bn, p.stages, p.splits, SWAP, ln_bytes), st, d.pdl != 0, p.splits, ta, tb, args);
+  const int red = args.row_ln ? RED_ROWLN
+                              : (p.splits == 1 ? RED_ONE : (gemm_push_reduce(p.bn, p.splits, SWAP) ? RED_PUSH : RED_PULL));
+  const int lnv = (SWAP && d.ln_x) ? (args.ln_coop ? 2 : 1) : 0;
+  if constexpr (!SWAP) {
+    if (red == RED_ONE) return launch_gemm_v<MODE, false, RED_ONE, 0>(d, p, ta, tb, args, st);
+    return launch_gemm_v<MODE, false, RED_PULL, 0>(d, p, ta, tb, args, st);
+  } else {
+    if (red == RED_ROWLN) {
+      if constexpr (MODE == EPI_BIAS_RESID) return launch_gemm_v<MODE, true, RED_ROWLN, 0>(d, p, ta, tb, args, st);
+      throw TfError{TF_ERR_UNSUPPORTED, "gemm: row-LN epilogue needs EPI_BIAS_RESID"};
+    }
+    if (lnv == 0) {
+      if (red == RED_ONE) return launch_gemm_v<MODE, true, RED_ONE, 0>(d, p, ta, tb, args, st);
+      if (red == RED_PUSH) return launch_gemm_v<MODE, true, RED_PUSH, 0>(d, p, ta, tb, args, st);
+      return launch_gemm_v<MODE, true, RED_PULL, 0>(d, p, ta, tb, args, st);
+    }
+    constexpr bool ln_ok = MODE == EPI_F32 || MODE == EPI_QKV || MODE == EPI_BIAS_GELU || MODE == EPI_LOGITS;
+    if constexpr (ln_ok) {
+      if (lnv == 1) {
+        if (red == RED_ONE) return launch_gemm_v<MODE, true, RED_ONE, 1>(d, p, ta, tb, args, st);
+        if (red == RED_PUSH) return launch_gemm_v<MODE, true, RED_PUSH, 1>(d, p, ta, tb, args, st);
+        return launch_gemm_v<MODE, true, RED_PULL, 1>(d, p, ta, tb, args, st);
+      }
+      if (red == RED_ONE) return launch_gemm_v<MODE, true, RED_ONE, 2>(d, p, ta, tb, args, st);
+      if (red == RED_PUSH) return launch_gemm_v<MODE, true, RED_PUSH, 2>(d, p, ta, tb, args, st);
+      return launch_gemm_v<MODE, true, RED_PULL, 2>(d, p, ta, tb, args, st);
+    }
+    throw TfError{TF_ERR_UNSUPPORTED, "gemm: fused operand LayerNorm not built for this epilogue"};
+  }
 }
 
 template <int MODE>
@@ -319,18 +386,13 @@ struct GemmExtra {
   const void* l2pf = nullptr;  // HBM -> L2 prefetch range (next layer's operand)
   unsigned long long l2pf_bytes = 0;
   int ln_coop = 0;  // with desc.ln_x: cooperative cluster LayerNorm (gemm_tc.cuh ln_coop_build)
-  int* lnf_cnt = nullptr;  // fused LN of the finished rows (EPI_BIAS_RESID, swap, split-K)
+  int row_ln = 0;   // EPI_BIAS_RESID: whole rows in one cluster + fused LN (gemm_rowln_epilogue)
   const float* lnf_g = nullptr;
   const float* lnf_b = nullptr;
   void* lnf_h = nullptr;
   int lnf_ldh = 0;
 };
 
-bool gemm_fuses_ln(const tf_gemm_desc& d) {
-  const GemmPlan p = plan_gemm(d);
-  return p.swap && p.splits > 1 && d.epilogue == TF_EPI_BIAS_RESID && d.n_feat <= 1024 && d.n_feat % 8 == 0 &&
-         d.ldo % 8 == 0;
-}
 
 void run_gemm(const tf_gemm_desc& d, cudaStream_t st, const GemmExtra& ex = GemmExtra{}) {
   TF_REQUIRE(d.m_tok > 0 && d.n_feat > 0 && d.k > 0, TF_ERR_SHAPE, "gemm: empty shape");
@@ -370,10 +432,12 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st, const GemmExtra& ex = Gemm
   a.late_trigger = d.pdl == 2 ? 1 : 0;
   a.l2pf = ex.l2pf;
   a.l2pf_bytes = ex.l2pf_bytes;
-  if (ex.lnf_cnt) {
-    TF_REQUIRE(gemm_fuses_ln(d) && ex.lnf_g && ex.lnf_b && ex.lnf_h && ex.lnf_ldh % 8 == 0, TF_ERR_ARG,
-               "gemm: fused epilogue LayerNorm not applicable");
-    a.lnf_cnt = ex.lnf_cnt;
+  if (ex.row_ln) {
+    TF_REQUIRE(p.swap && p.splits == 2 && d.epilogue == TF_EPI_BIAS_RESID && p.tiles_b == 1 && p.bn <= 64 &&
+                   p.tiles_a * 2 <= 16 && ex.lnf_g && ex.lnf_b && ex.lnf_h &&
+                   gemm_ring_bytes(p.bn, p.stages, p.splits, true) >= gemm_rowln_scratch_bytes(p.bn, p.tiles_a),
+               TF_ERR_ARG, "gemm: row-LN epilogue not applicable");
+    a.row_ln = 1;
     a.lnf_g = ex.lnf_g;
     a.lnf_b = ex.lnf_b;
     a.lnf_h = static_cast<__half*>(ex.lnf_h);
@@ -821,16 +885,6 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     }
     return ex;
   };
-  // decode: the LayerNorms after the two residual GEMMs run in those GEMMs'
-  // epilogues (last CTA to finish a row normalises it) instead of as kernels
-  // (measured slower than the LN launch it replaces: opt-in TF_LN_EPI=1)
-  static const bool lnf_on = [] {
-    const char* e = getenv("TF_LN_EPI");
-    return e && e[0] == '1';
-  }();
-  int* ln_cnt = (lnf_on && T == 1 && !fuse_ln && sd.counters && sd.n_counters >= B * NH + M)
-                    ? sd.counters + B * NH
-                    : nullptr;
 
   // small-batch decode: narrow-tile whole-K GEMMs with the LayerNorms fused
   // into the QKV / FFN1 operand (dgemm.cuh). Opt-in (TF_DGEMM=1): the whole-K
@@ -844,7 +898,6 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
   const bool dg = dg_on && T == 1 && !fuse_ln && D % 8 == 0 && H % 8 == 0 && H <= 1024 &&
                   dg_plan(M, 3 * H, H, pq) && dg_plan(M, H, H, po) && dg_plan(M, F, H, p1) && dg_plan(M, H, F, p2) &&
                   pq.splits == 1 && p1.splits == 1;
-  if (dg) ln_cnt = nullptr;
   // decode: attn_norm / ffn_norm computed by the consuming QKV / FFN1 split-K
   // cluster (cooperative LN, gemm_tc.cuh) instead of stand-alone launches.
   // Opt-in (TF_LN_COOP=1): measured slower in the PDL-chained step
@@ -853,7 +906,17 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     return e && e[0] == '1';
   }();
   const bool coop = coop_on && !dg && !fuse_ln && T == 1 && M <= 256 && H <= 1024 && H % 8 == 0 && m.ldk_h % 8 == 0;
-  if (coop) ln_cnt = nullptr;
+  // decode, batch <= 64: the two residual GEMMs (Wo, FFN2) run as ONE cluster
+  // covering whole output rows (tiles x 2 K-halves <= 16 CTAs) and fuse the
+  // following LayerNorm into their epilogue (gemm_rowln_epilogue). Opt-in
+  // (TF_ROWLN=1): 12 CTAs carry the whole weight matrix and three cluster
+  // exchange rounds sit on the critical path (measured 4.9 -> 20 us)
+  static const bool rowln_on = [] {
+    const char* e = getenv("TF_ROWLN");
+    return e && e[0] == '1';
+  }();
+  const bool rowln = rowln_on && !dg && !coop && !fuse_ln && T == 1 && M <= 64 && (H + 127) / 128 <= 8 &&
+                     (H / 64) % 2 == 0 && (F / 64) % 2 == 0 && H % 8 == 0;
 
   for (int l = 0; l < L; ++l) {
     const tf_layer_weights& w = s.m->layers[l];
@@ -945,9 +1008,9 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     o.resid = x;
     o.ldr = m.ldk_h;
     GemmExtra oex = pf_next(l, 1);
-    const bool o_ln = ln_cnt && gemm_fuses_ln(o);
-    if (o_ln) {
-      oex.lnf_cnt = ln_cnt;
+    if (rowln) {
+      o.splits = 2;
+      oex.row_ln = 1;
       oex.lnf_g = w.ln2_gamma;
       oex.lnf_b = w.ln2_beta;
       oex.lnf_h = h;
@@ -970,7 +1033,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     ln.b = w.ln2_beta;
     ln.h = h;
     ln.ldh = m.ldk_h;
-    if (!fuse_ln && !o_ln && !dg && !coop) {
+    if (!fuse_ln && !dg && !coop && !rowln) {
       run_ln(ln, st, pdl);
       ++launches;
     }
@@ -1028,9 +1091,9 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
       }
     }
     GemmExtra f2ex = pf_next(l, 3);
-    const bool f2_ln = ln_cnt && gemm_fuses_ln(f2);
-    if (f2_ln) {  // T == 1: every row is the last position
-      f2ex.lnf_cnt = ln_cnt;
+    if (rowln) {  // T == 1: every row is the last position
+      f2.splits = 2;
+      f2ex.row_ln = 1;
       f2ex.lnf_g = nl.g;
       f2ex.lnf_b = nl.b;
       f2ex.lnf_h = h;
@@ -1041,7 +1104,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     else
       run_gemm(f2, st, f2ex);
     ++launches;
-    if (f2_ln) continue;
+    if (rowln) continue;
     if ((dg || coop) && l + 1 < L) continue;  // the next QKV normalises its own operand
     if (l + 1 < L ? !fuse_ln : !fuse_final) {
       run_ln(nl, st, pdl);

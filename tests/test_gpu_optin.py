@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.parametrize("env", [
     {"TF_DGEMM": "1"},      # whole-K narrow-tile decode GEMM, LN fused into the operand
     {"TF_LN_COOP": "1"},    # cluster-cooperative LN in the QKV / FFN1 split-K GEMMs
-    {"TF_LN_EPI": "1"},     # LN by the last CTA to finish a row in the residual GEMMs
+    {"TF_ROWLN": "1"},      # residual GEMMs as one whole-row cluster with the LayerNorm in the epilogue
     {"TF_L2PF": "0"},       # no next-layer L2 prefetch
 ])
 def test_optin_decode_variant_matches_oracle(cuda_device, env):
