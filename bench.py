@@ -27,8 +27,11 @@ own batch, no collective): "scaling": "weak".
 * ``e2e``    — the same metric through the public API (batched_greedy_decode /
   beam_search_decode) with host prompt lists: H2D of ids/positions/pads and D2H
   of results inside the timed region (wall clock + device sync), max over ranks.
-* ``roofline`` — the dominant kernel: algorithmic bytes per
-  launch / its CUDA-event launch time, against MEASURED_PEAKS.json.
+* ``roofline`` — the decode step, the unit of the north-star target (DESIGN.md
+  §5): SURVEY §8d algorithmic bytes per step / the CUDA-event time of a
+  graph-replayed step, against MEASURED_PEAKS.json; ``traffic`` = ncu DRAM bytes
+  of one step (profiles/r1_ncu_step_<w>.json). ``largest_launch``: the lm_head
+  GEMM + argmax alone (rotating weight copies, HBM-streamed).
 * ``cpu_baseline`` — the oracle port (oracle/tinfer_oracle.py, numpy) on this
   host's cores, bounded sample (prefill + a few decode steps, extrapolated).
   ``--impl reference`` prints that arm alone (rank 0; other ranks exit 0).
@@ -105,6 +108,17 @@ def make_prompts(V, w, rank):
         out.append(ids[k:k + n])
         k += n
     return out
+
+
+def ncu_step_traffic(wname):
+    """DRAM bytes (read + write) of one decode step from the committed ncu
+    per-launch capture (profiles/r1_ncu_step_<w>.json: tools/one_step.py under
+    ncu --cache-control none, summed by tools/step_profile.py), or None."""
+    path = os.path.join(ROOT, "profiles", f"r1_ncu_step_{wname}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        return float(json.load(fh)["dram_bytes"])
 
 
 def ncu_traffic(kernel_tag="prof_lm_head"):
@@ -407,6 +421,7 @@ def run_ours(args):
     t_step = probe_decode_step(torch, run, flush, stream, w)
     step_bw = float(np.mean(step_bytes)) / t_step / 1e9
     kern = probe_dominant_kernel(torch, dm, run.sess, flush, stream, S)
+    n_launch = int(N.lib().tf_session_launches_per_step(run.sess.handle))
 
     if rank == 0:
         line = base_line(args, w, world, value, 1e3 * total / args.steps)
@@ -414,15 +429,21 @@ def run_ours(args):
             "e2e": {"value": gen_per_step * args.steps * world / e2e_t, "unit": "generated tokens/s",
                     "h2d_bytes_per_step": int(st.h2d_bytes), "d2h_bytes_per_step": int(st.d2h_bytes)},
             "gpu_launches": int(run.launches() * args.steps),
-            "roofline": {"bound": "hbm", "achieved": kern["gbs"], "peak": hbm_peak, "unit": "GB/s",
-                         "frac": kern["gbs"] / hbm_peak,
-                         "traffic": ncu_traffic() if args.workload == "c2" else None,
-                         "kernel": kern["name"],
-                         "bytes_per_launch": kern["bytes"], "launch_us": kern["us"],
+            # the roofline unit is the decode step (north star: fraction of the
+            # HBM roofline per decode step): one CUDA-graph replay of the step's
+            # PDL-chained launches, device-timed over the 63 steps of a generate
+            "roofline": {"bound": "hbm", "achieved": step_bw, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": step_bw / hbm_peak,
+                         "traffic": ncu_step_traffic(args.workload),
+                         "kernel": f"decode step (CUDA graph of {n_launch} PDL-chained launches)",
+                         "bytes_per_launch": float(np.mean(step_bytes)), "launch_us": t_step * 1e6,
                          "peak_kind": peak_kind},
             "decode_step": {"us": t_step * 1e6, "algorithmic_bytes": float(np.mean(step_bytes)),
                             "achieved_gbs": step_bw, "frac_of_hbm": step_bw / hbm_peak,
-                            "launches": int(N.lib().tf_session_launches_per_step(run.sess.handle))},
+                            "launches": n_launch},
+            "largest_launch": {"kernel": kern["name"], "bytes_per_launch": kern["bytes"], "launch_us": kern["us"],
+                               "achieved_gbs": kern["gbs"], "frac": kern["gbs"] / hbm_peak,
+                               "traffic": ncu_traffic() if args.workload == "c2" else None},
             "clocks": clk.summary(),
         })
         if not args.no_cpu_baseline and world == 1:
@@ -453,27 +474,33 @@ def probe_decode_step(torch, run, flush, stream, w):
 
 def probe_dominant_kernel(torch, dm, sess, flush, stream, batch):
     """The lm_head GEMM fused with argmax — the largest single launch of a decode
-    step. The launch is captured into a CUDA graph (no host/ctypes time inside
-    the measurement) and each replay is timed with CUDA events on the replay
-    stream, L2 flushed before each replay. Algorithmic bytes = lm_head weights
-    (as stored, K padded to 64) + activations + argmax keys."""
+    step. COPIES launches, each on its own copy of the lm_head weights (together
+    > 2x the 126 MB L2, so every launch streams its weights from HBM), are
+    captured back to back into one CUDA graph; the replay is timed with CUDA
+    events on the replay stream and divided by COPIES. Algorithmic bytes =
+    lm_head weights (as stored, K padded to 64) + activations + argmax keys."""
     from paper_2407_04991_b200 import _native as N
     from paper_2407_04991_b200 import ops
 
     H, V = dm.H, dm.V
+    wbytes = V * dm.ldk_h * 2
+    copies = max(4, int(2 * (126 << 20) // wbytes) + 1)
+    ws = [dm.lm_head_t.clone() for _ in range(copies)]
     keys = torch.zeros(batch, dtype=torch.int64, device=dm.device)
     act = sess.h[:batch]
     gs = torch.cuda.Stream()
     with torch.cuda.stream(gs):
-        ops.gemm(act, dm.lm_head_t, H, N.EPI_LOGITS, keys=keys)
+        for w in ws:
+            ops.gemm(act, w, H, N.EPI_LOGITS, keys=keys)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=gs):
-            ops.gemm(act, dm.lm_head_t, H, N.EPI_LOGITS, keys=keys)
+            for w in ws:
+                ops.gemm(act, w, H, N.EPI_LOGITS, keys=keys)
     torch.cuda.synchronize()
     ts = []
     with torch.cuda.stream(gs):
-        for i in range(12):
+        for i in range(7):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(gs)
@@ -481,9 +508,10 @@ def probe_dominant_kernel(torch, dm, sess, flush, stream, batch):
             e1.record(gs)
             e1.synchronize()
             if i >= 2:
-                ts.append(e0.elapsed_time(e1) / 1e3)
+                ts.append(e0.elapsed_time(e1) / 1e3 / copies)
     t = float(statistics.median(ts))
-    nbytes = V * dm.ldk_h * 2 + batch * H * 2 + batch * 8
+    del ws
+    nbytes = wbytes + batch * H * 2 + batch * 8
     return {"name": "gemm_tc_kernel<EPI_LOGITS,swap> (lm_head + argmax)", "bytes": nbytes,
             "us": t * 1e6, "gbs": nbytes / t / 1e9}
 
