@@ -43,6 +43,16 @@ struct AttnArgs {
   // streams its own window of them HBM -> L2 (null = off)
   const __half* pf_kc;
   const __half* pf_vc;
+  // decode prefetch kernel, whole window in one CTA: fused output projection.
+  // The CTA multiplies its head's (f16) output row by that head's K-slice of
+  // Wo (wo_t [H, ldw] K-major, columns h*D .. h*D+D) and writes the f32 partial
+  // wo_part[(b * NH + h) * H + n]; the heads are summed (in head order) with the
+  // bias and residual by resid_heads_ln_kernel (model.py:478-482).
+  const __half* wo_t;
+  int ldw, H;
+  float* wo_part;
+  const void* l2pf;  // HBM -> L2 prefetch range (the next layer's Wo)
+  unsigned long long l2pf_bytes;
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
@@ -446,6 +456,7 @@ __global__ void __launch_bounds__(128) attn_decode_pf_kernel(const AttnArgs a) {
     const size_t off = kv_off(s0);
     l2_prefetch_bulk((tid == 0 ? a.pf_kc : a.pf_vc) + off, (uint32_t)((s1 - s0) * D * 2));
   }
+  if (tid == 32) l2_prefetch_share(a.l2pf, a.l2pf_bytes);
   pdl_trigger();
   pdl_wait();
   if (threadIdx.x == 0) tr.mark(a.trace, 1);
@@ -559,6 +570,42 @@ __global__ void __launch_bounds__(128) attn_decode_pf_kernel(const AttnArgs a) {
   };
   if (ngr == 1) {
     merge(part_s, nch);
+    if (a.wo_t != nullptr) {
+      // o (as stored, f16-rounded: model.py:476-477) -> smem, then one 128-B Wo
+      // row segment per 8 lanes: lane part p sums its 8 products in order, the
+      // 8 parts combine by an xor butterfly (fixed order), 16 rows per pass
+      __syncthreads();
+      if (tid < D) qs[tid] = __half2float(orow[tid]);
+      __syncthreads();
+      const int part = tid & 7, r0 = tid >> 3;
+      float o8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o8[e] = qs[part * 8 + e];
+      const __half* wbase = a.wo_t + (size_t)h * D + part * 8;
+      float* dst = a.wo_part + ((size_t)b * a.NH + h) * a.H;
+      constexpr int U = 12;  // 128-B row segments in flight per 8 lanes
+      for (int n0 = r0; n0 < a.H; n0 += 16 * U) {
+        uint4 raw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int n = n0 + 16 * u;
+          raw[u] = n < a.H ? __ldg(reinterpret_cast<const uint4*>(wbase + (size_t)n * a.ldw)) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int n = n0 + 16 * u;
+          float wv[8];
+          unpack8(raw[u], wv);
+          float acc = __fmul_rn(o8[0], wv[0]);
+#pragma unroll
+          for (int e = 1; e < 8; ++e) acc = __fadd_rn(acc, __fmul_rn(o8[e], wv[e]));
+          acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+          acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+          acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+          if (part == 0 && n < a.H) dst[n] = acc;
+        }
+      }
+    }
   } else {
     float* part = a.ws + (((size_t)b * a.NH + h) * a.max_chunks) * 66;
     for (int e = tid; e < nc * 66; e += 128) __stcg(part + (size_t)c0 * 66 + e, part_s[e]);

@@ -662,6 +662,11 @@ void run_embed(const EmbedArgs& a, cudaStream_t st, bool pdl) {
 
 void run_ln(const LnArgs& a0, cudaStream_t st, bool pdl) {
   LnArgs a = a0;
+  static const bool early = [] {  // TF_LN_EARLY=1: LN releases its successor before its own wait (A/B)
+    const char* e = getenv("TF_LN_EARLY");
+    return e && e[0] == '1';
+  }();
+  a.early_trigger = early ? 1 : 0;
   a.trace = trace_next("layernorm");
   const dim3 grid((a.n_rows + 7) / 8);
   if (vec_ok(a.H, a.ldx, a.ldh) && a.H <= 2048) {
@@ -700,6 +705,7 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
     // else groups of <= 4 (64 KB of K/V each) merged through the workspace
     const int nch = a.max_chunks;
     const int ngr = (nch + 3) / 4;
+    TF_REQUIRE(a.wo_t == nullptr || ngr == 1, TF_ERR_ARG, "attention: fused Wo needs the window in one CTA");
     AttnArgs t = a;
     t.group = (nch + ngr - 1) / ngr;
     t.trace = trace_next("attn_decode_pf");
@@ -906,6 +912,19 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     return e && e[0] == '1';
   }();
   const bool coop = coop_on && !dg && !fuse_ln && T == 1 && M <= 256 && H <= 1024 && H % 8 == 0 && m.ldk_h % 8 == 0;
+  // decode: the output projection runs inside the attention kernel (per-head
+  // partials of o_h @ Wo_h) and the head sum + bias + residual + ffn_norm in one
+  // row kernel, replacing the Wo GEMM and the LayerNorm launch. Opt-in
+  // (TF_ATTN_WO=1): every attention CTA streams its head's 98 KB Wo slice, which
+  // lengthens the attention more than the two launches it removes
+  static const bool attn_wo_on = [] {
+    const char* e = getenv("TF_ATTN_WO");
+    return e && e[0] == '1';
+  }();
+  const bool attn_wo = attn_wo_on && NH <= 16 && !dg && !fuse_ln && T == 1 && D == 64 && !sd.beam_indir &&
+                       (sd.capacity + 63) / 64 <= 4 && H % 8 == 0 && H <= 2048 && m.ldk_h % 8 == 0 &&
+                       sd.workspace && sd.workspace_bytes >= (size_t)B * NH * H * sizeof(float) && sd.counters &&
+                       sd.n_counters >= B * NH;
   // decode, batch <= 64: the two residual GEMMs (Wo, FFN2) run as ONE cluster
   // covering whole output rows (tiles x 2 K-halves <= 16 CTAs) and fuse the
   // following LayerNorm into their epilogue (gemm_rowln_epilogue). Opt-in
@@ -949,6 +968,10 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     // decode: attention (next) prefetches the whole KV window; release it only
     // once the QKV weights are in (after this GEMM's own dependency wait)
     if (pdl && T == 1 && qkv_late) q.pdl = 2;
+    static const int late_mask = [] {  // TF_LATE_MASK bits: 1 Wo, 2 FFN1, 4 FFN2 release late (A/B)
+      const char* e = getenv("TF_LATE_MASK");
+      return e ? atoi(e) : 0;
+    }();
     if (dg) {
       q.act = x;  // attn_norm (model.py:460-462) runs on the operand inside the GEMM
       run_dgemm(q, pq, w.ln1_gamma, w.ln1_beta, pf_next(l, 0), st);
@@ -995,10 +1018,38 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
         at.pf_vc = static_cast<const __half*>(sd.v_cache) + (l + 1) * layer_cache;
       }
     }
+    if (attn_wo) {
+      at.wo_t = static_cast<const __half*>(w.wo_t);
+      at.ldw = m.ldk_h;
+      at.H = H;
+      at.wo_part = sd.workspace;
+      const GemmExtra wex = pf_next(l, 1);
+      at.l2pf = wex.l2pf;
+      at.l2pf_bytes = wex.l2pf_bytes;
+    }
     run_attention(at, st, pdl);
     ++launches;
+    if (attn_wo) {
+      // head sum + bias + residual (model.py:478-482) and ffn_norm (model.py:484-486)
+      ResLnArgs r{};
+      r.B = B;
+      r.NH = NH;
+      r.H = H;
+      r.part = sd.workspace;
+      r.bias = w.bo;
+      r.x = x;
+      r.ldx = m.ldk_h;
+      r.g = w.ln2_gamma;
+      r.b = w.ln2_beta;
+      r.h = h;
+      r.ldh = m.ldk_h;
+      r.trace = trace_next("resid_heads_ln");
+      launch_mc(resid_heads_ln_kernel, dim3(B), dim3(kResThreads), 0, st, pdl, r);
+      ++launches;
+    }
     // output projection + residual (model.py:478-482)
     tf_gemm_desc o = g;
+    const bool skip_wo = attn_wo;
     o.n_feat = H;
     o.k = H;
     o.act = sd.attn;
@@ -1020,11 +1071,15 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
       oex.lnf_h = h;
       oex.lnf_ldh = m.ldk_h;
     }
-    if (dg)
+    if (pdl && T == 1 && (late_mask & 1)) o.pdl = 2;
+    if (skip_wo) {
+    } else if (dg) {
       run_dgemm(o, po, nullptr, nullptr, oex, st);
-    else
+      ++launches;
+    } else {
       run_gemm(o, st, oex);
-    ++launches;
+      ++launches;
+    }
     // ffn_norm (model.py:484-486)
     LnArgs ln{};
     ln.n_rows = M;
@@ -1037,7 +1092,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     ln.b = w.ln2_beta;
     ln.h = h;
     ln.ldh = m.ldk_h;
-    if (!fuse_ln && !dg && !coop && !rowln) {
+    if (!fuse_ln && !dg && !coop && !rowln && !skip_wo) {
       run_ln(ln, st, pdl);
       ++launches;
     }
@@ -1059,6 +1114,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
       run_dgemm(f1, p1, w.ln2_gamma, w.ln2_beta, pf_next(l, 2), st);
     } else {
       GemmExtra f1ex = pf_next(l, 2);
+      if (pdl && T == 1 && (late_mask & 2)) f1.pdl = 2;
       if (coop) {
         set_ln(f1, w.ln2_gamma, w.ln2_beta, 1, 0);
         f1ex.ln_coop = 1;
@@ -1103,6 +1159,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
       f2ex.lnf_h = h;
       f2ex.lnf_ldh = m.ldk_h;
     }
+    if (pdl && T == 1 && (late_mask & 4)) f2.pdl = 2;
     if (dg)
       run_dgemm(f2, p2, nullptr, nullptr, f2ex, st);
     else

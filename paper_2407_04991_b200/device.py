@@ -189,7 +189,9 @@ class Session:
         d.logits = self.logits.data_ptr() if logits else None
         # split-KV decode attention scratch: per (row, head, 64-slot chunk) {m, z, o[64]}
         chunks = (capacity + 63) // 64
-        self.att_ws = torch.empty(max(1, batch * dm.NH * chunks * 66), dtype=torch.float32, device=dev)
+        # (also the per-head partials of the attention-fused output projection)
+        self.att_ws = torch.empty(max(1, batch * dm.NH * chunks * 66, batch * dm.NH * dm.H), dtype=torch.float32,
+                                  device=dev)
         self.att_cnt = torch.zeros(batch * dm.NH, dtype=torch.int32, device=dev)
         d.workspace, d.workspace_bytes = self.att_ws.data_ptr(), self.att_ws.numel() * 4
         d.counters, d.n_counters = self.att_cnt.data_ptr(), self.att_cnt.numel()
