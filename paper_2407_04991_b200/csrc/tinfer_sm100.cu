@@ -895,7 +895,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
   // small-batch decode: narrow-tile whole-K GEMMs with the LayerNorms fused
   // into the QKV / FFN1 operand (dgemm.cuh). Opt-in (TF_DGEMM=1): the whole-K
   // MMA chain (~35 cycles per tcgen05.mma issue) and the per-CTA LayerNorm of
-  // all rows cost more than the split-K reduction they remove (DESIGN.md §8).
+  // all rows cost more than the split-K reduction they remove (DESIGN.md §8c).
   static const bool dg_on = [] {
     const char* e = getenv("TF_DGEMM");
     return e && e[0] == '1';
@@ -906,7 +906,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
                   pq.splits == 1 && p1.splits == 1;
   // decode: attn_norm / ffn_norm computed by the consuming QKV / FFN1 split-K
   // cluster (cooperative LN, gemm_tc.cuh) instead of stand-alone launches.
-  // Opt-in (TF_LN_COOP=1): measured slower in the PDL-chained step (DESIGN.md §8)
+  // Opt-in (TF_LN_COOP=1): measured slower in the PDL-chained step (DESIGN.md §8c)
   static const bool coop_on = [] {
     const char* e = getenv("TF_LN_COOP");
     return e && e[0] == '1';
@@ -916,7 +916,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
   // partials of o_h @ Wo_h) and the head sum + bias + residual + ffn_norm in one
   // row kernel, replacing the Wo GEMM and the LayerNorm launch. Opt-in
   // (TF_ATTN_WO=1): every attention CTA streams its head's 98 KB Wo slice, which
-  // lengthens the attention more than the two launches it removes (DESIGN §8)
+  // lengthens the attention more than the two launches it removes (DESIGN §8c)
   static const bool attn_wo_on = [] {
     const char* e = getenv("TF_ATTN_WO");
     return e && e[0] == '1';
