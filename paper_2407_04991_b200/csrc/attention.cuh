@@ -402,13 +402,18 @@ __global__ void __launch_bounds__(kSplitThreads) attn_decode_split_kernel(const 
 // last-arriving CTA merges them.
 constexpr int kPfKeysPerChunk = 64, kPfChunkBytes = 2 * 64 * 64 * 2;  // K + V, f16
 __host__ __device__ inline size_t attn_pf_smem_bytes(int G) {
-  return (size_t)G * kPfChunkBytes + (size_t)G * 66 * sizeof(float);
+  return (size_t)G * kPfChunkBytes + (size_t)G * (66 + 64) * sizeof(float);
 }
+// 128 threads (4 CTAs per SM: a batch-32 step is one wave) or 256 (one key
+// per thread for QK^T, every chunk half its own warp; large batches)
 
-__global__ void __launch_bounds__(128) attn_decode_pf_kernel(const AttnArgs a) {
+// WO: the fused output projection epilogue (AttnArgs::wo_t) is compiled in
+template <bool WO, int kPfThreads>
+__global__ void __launch_bounds__(kPfThreads) attn_decode_pf_kernel(const AttnArgs a) {
   extern __shared__ __align__(128) uint8_t pf_smem[];
   __shared__ __align__(16) float qs[64];
   __shared__ float sc_all[4 * 64];
+  __shared__ float ew_all[4 * 64];
   __shared__ int s_last;
   constexpr int D = 64;
   TF_TRACE_INIT(tr);
@@ -416,6 +421,7 @@ __global__ void __launch_bounds__(128) attn_decode_pf_kernel(const AttnArgs a) {
   const int G = a.group;
   __half* kvs = reinterpret_cast<__half*>(pf_smem);                           // [G][K|V][64][64]
   float* part_s = reinterpret_cast<float*>(pf_smem + (size_t)G * kPfChunkBytes);  // [G][66]
+  float* part_h = part_s + (size_t)G * 66;  // [G][64]: second key half of each chunk's PV
   const int g = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // the cache length and left pad were written by earlier steps (complete)
@@ -437,7 +443,7 @@ __global__ void __launch_bounds__(128) attn_decode_pf_kernel(const AttnArgs a) {
     return (size_t)src * row_stride + (size_t)h * head_stride + (size_t)s * D;
   };
   // ---- before the wait: K/V of every slot < hi in this CTA's chunks
-  for (int seg = tid; seg < nc * 64 * 8; seg += 128) {
+  for (int seg = tid; seg < nc * 64 * 8; seg += kPfThreads) {
     const int i = seg >> 9, j = (seg >> 3) & 63, part = seg & 7;
     const int slot = lo + (c0 + i) * 64 + j;
     if (slot != hi) {  // slots past the window are zero-filled (src-size 0)
@@ -486,7 +492,7 @@ __global__ void __launch_bounds__(128) attn_decode_pf_kernel(const AttnArgs a) {
   // distinct bank groups; 8 independent partial dot products, summed in that
   // order (fixed by the key's position in its chunk -> batch-invariant)
   const int n_keys = min(nc * 64, n - c0 * 64);
-  for (int key = tid; key < n_keys; key += 128) {
+  for (int key = tid; key < n_keys; key += kPfThreads) {
     const int i = key >> 6, j = key & 63;
     const __half* kr = kvs + ((size_t)(2 * i) * 64 + j) * 64;
     float ps[8];
@@ -516,42 +522,58 @@ __global__ void __launch_bounds__(128) attn_decode_pf_kernel(const AttnArgs a) {
     tr.mark(a.trace, 4);
     if (a.trace > 0) tr.t[6] = (unsigned long long)(clock64() - clk0);
   }
-  // one warp per chunk: chunk max / exp / sum, then o = sum_j e_j v_j with
-  // each lane owning dims (2 lane, 2 lane + 1), keys in order
-  for (int i = warp; i < nc; i += 4) {
+  // WPC warps per chunk (1 with 128 threads; 2 with 256: key halves 0-31 and
+  // 32-63). Each warp computes the chunk max / exp / sum over all 64 keys (the
+  // same values in every warp of the chunk), writes the weights of its keys, and
+  // o = sum_j e_j v_j over its 64/WPC keys with each lane owning dims (2 lane,
+  // 2 lane + 1), 4 accumulators (keys j % 4) combined pairwise; key halves are
+  // added in order before the merge
+  constexpr int WPC = kPfThreads >= 256 ? 2 : 1, KPW = 64 / WPC;
+  for (int wi = warp; wi < WPC * nc; wi += kPfThreads / 32) {
+    const int i = wi / WPC, hf = wi % WPC;
     const int cnt_keys = min(64, n - (c0 + i) * 64);
-    float* sci = sc_all + i * 64;
+    const float* sci = sc_all + i * 64;
     const float s0 = lane < cnt_keys ? sci[lane] : -INFINITY;
     const float s1 = lane + 32 < cnt_keys ? sci[lane + 32] : -INFINITY;
     const float m = warp_max(fmaxf(s0, s1));
     const float e0 = lane < cnt_keys ? expf(__fsub_rn(s0, m)) : 0.0f;
     const float e1 = lane + 32 < cnt_keys ? expf(__fsub_rn(s1, m)) : 0.0f;
     const float z = warp_sum(__fadd_rn(e0, e1));
-    sci[lane] = e0;
-    sci[lane + 32] = e1;
+    // weights go to their own array: another warp of the chunk may still be
+    // reading the scores
+    float* wts = ew_all + i * 64;
+    if (WPC == 1 || hf == 0) wts[lane] = e0;
+    if (WPC == 1 || hf == 1) wts[lane + 32] = e1;
     __syncwarp();
-    const __half* Vs = kvs + (size_t)(2 * i + 1) * 64 * 64;
-    // 4 independent accumulators (keys j % 4), combined pairwise; e_j = 0
-    // past cnt_keys, so the loop runs the whole chunk
+    const __half* Vs = kvs + (size_t)(2 * i + 1) * 64 * 64 + (size_t)hf * KPW * 64;
+    const float* w0 = wts + hf * KPW;
     float o0[4] = {0.f, 0.f, 0.f, 0.f}, o1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
-    for (int j = 0; j < 64; j += 4) {
+    for (int j = 0; j < KPW; j += 4) {
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const float2 v = __half22float2(*reinterpret_cast<const __half2*>(Vs + (j + r) * 64 + 2 * lane));
-        const float w = sci[j + r];
+        const float w = w0[j + r];
         o0[r] = __fadd_rn(o0[r], __fmul_rn(w, v.x));
         o1[r] = __fadd_rn(o1[r], __fmul_rn(w, v.y));
       }
     }
-    part_s[i * 66 + 2 + 2 * lane] = __fadd_rn(__fadd_rn(o0[0], o0[1]), __fadd_rn(o0[2], o0[3]));
-    part_s[i * 66 + 3 + 2 * lane] = __fadd_rn(__fadd_rn(o1[0], o1[1]), __fadd_rn(o1[2], o1[3]));
-    if (lane == 0) {
+    float* dst = hf ? part_h + i * 64 : part_s + i * 66 + 2;
+    dst[2 * lane] = __fadd_rn(__fadd_rn(o0[0], o0[1]), __fadd_rn(o0[2], o0[3]));
+    dst[2 * lane + 1] = __fadd_rn(__fadd_rn(o1[0], o1[1]), __fadd_rn(o1[2], o1[3]));
+    if (lane == 0 && hf == 0) {
       part_s[i * 66] = m;
       part_s[i * 66 + 1] = z;
     }
   }
   __syncthreads();
+  if constexpr (WPC == 2) {
+    for (int e = tid; e < nc * 64; e += kPfThreads) {
+      const int i = e >> 6, d = e & 63;
+      part_s[i * 66 + 2 + d] = __fadd_rn(part_s[i * 66 + 2 + d], part_h[i * 64 + d]);
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) tr.mark(a.trace, 5);
   if (threadIdx.x == 0) tr.mark(a.trace, 3);
   // merge in chunk order: M = max m_c, Z = sum z_c e^(m_c - M), O = sum o_c e^(m_c - M)
@@ -570,30 +592,31 @@ __global__ void __launch_bounds__(128) attn_decode_pf_kernel(const AttnArgs a) {
   };
   if (ngr == 1) {
     merge(part_s, nch);
-    if (a.wo_t != nullptr) {
+    if constexpr (WO) {
       // o (as stored, f16-rounded: model.py:476-477) -> smem, then one 128-B Wo
       // row segment per 8 lanes: lane part p sums its 8 products in order, the
       // 8 parts combine by an xor butterfly (fixed order), 16 rows per pass
       __syncthreads();
       if (tid < D) qs[tid] = __half2float(orow[tid]);
       __syncthreads();
+      constexpr int RPP = kPfThreads / 8;  // Wo rows per pass
       const int part = tid & 7, r0 = tid >> 3;
       float o8[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) o8[e] = qs[part * 8 + e];
       const __half* wbase = a.wo_t + (size_t)h * D + part * 8;
       float* dst = a.wo_part + ((size_t)b * a.NH + h) * a.H;
-      constexpr int U = 12;  // 128-B row segments in flight per 8 lanes
-      for (int n0 = r0; n0 < a.H; n0 += 16 * U) {
+      constexpr int U = 6;  // 128-B row segments in flight per 8 lanes
+      for (int n0 = r0; n0 < a.H; n0 += RPP * U) {
         uint4 raw[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int n = n0 + 16 * u;
+          const int n = n0 + RPP * u;
           raw[u] = n < a.H ? __ldg(reinterpret_cast<const uint4*>(wbase + (size_t)n * a.ldw)) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int n = n0 + 16 * u;
+          const int n = n0 + RPP * u;
           float wv[8];
           unpack8(raw[u], wv);
           float acc = __fmul_rn(o8[0], wv[0]);
@@ -608,7 +631,7 @@ __global__ void __launch_bounds__(128) attn_decode_pf_kernel(const AttnArgs a) {
     }
   } else {
     float* part = a.ws + (((size_t)b * a.NH + h) * a.max_chunks) * 66;
-    for (int e = tid; e < nc * 66; e += 128) __stcg(part + (size_t)c0 * 66 + e, part_s[e]);
+    for (int e = tid; e < nc * 66; e += kPfThreads) __stcg(part + (size_t)c0 * 66 + e, part_s[e]);
     __threadfence();
     __syncthreads();
     if (tid == 0) {

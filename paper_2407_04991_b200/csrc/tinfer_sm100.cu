@@ -693,6 +693,18 @@ void run_ln(const LnArgs& a0, cudaStream_t st, bool pdl) {
   }
 }
 
+template <bool WO, int THREADS>
+void launch_pf(dim3 grid, size_t smem, cudaStream_t st, bool pdl, const AttnArgs& t) {
+  static bool attr = false;
+  if (!attr) {
+    TF_CHECK_CUDA(cudaFuncSetAttribute(attn_decode_pf_kernel<WO, THREADS>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_pf_smem_bytes(4)));
+    set_max_carveout(attn_decode_pf_kernel<WO, THREADS>);
+    attr = true;
+  }
+  launch(attn_decode_pf_kernel<WO, THREADS>, grid, dim3(THREADS), smem, st, pdl, t);
+}
+
 void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
   TF_REQUIRE(a.D >= 1 && a.D <= 128, TF_ERR_UNSUPPORTED, "head_dim must be in [1, 128]");
   static const int pf_mode = [] {  // TF_ATTN_PF=0 selects the split kernel (A/B diagnostics)
@@ -710,14 +722,19 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
     t.group = (nch + ngr - 1) / ngr;
     t.trace = trace_next("attn_decode_pf");
     const size_t smem = attn_pf_smem_bytes(t.group);
-    static bool attr = false;
-    if (!attr) {
-      TF_CHECK_CUDA(cudaFuncSetAttribute(attn_decode_pf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)attn_pf_smem_bytes(4)));
-      set_max_carveout(attn_decode_pf_kernel);
-      attr = true;
+    // 256 threads only when the grid is several waves anyway (large batch)
+    const bool wide = (size_t)ngr * a.NH * a.B > (size_t)4 * num_sms();
+    if (a.wo_t) {
+      if (wide)
+        launch_pf<true, 256>(dim3(ngr, a.NH, a.B), smem, st, pdl, t);
+      else
+        launch_pf<true, 128>(dim3(ngr, a.NH, a.B), smem, st, pdl, t);
+    } else {
+      if (wide)
+        launch_pf<false, 256>(dim3(ngr, a.NH, a.B), smem, st, pdl, t);
+      else
+        launch_pf<false, 128>(dim3(ngr, a.NH, a.B), smem, st, pdl, t);
     }
-    launch(attn_decode_pf_kernel, dim3(ngr, a.NH, a.B), dim3(128), smem, st, pdl, t);
   } else if (a.T == 1 && a.D == 64 && a.ws && a.cnt && a.max_chunks >= (a.cap + kSplitKeys - 1) / kSplitKeys) {
     AttnArgs t = a;
     t.trace = trace_next("attn_decode_split");
@@ -937,6 +954,14 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
   const bool rowln = rowln_on && !dg && !coop && !fuse_ln && T == 1 && M <= 64 && (H + 127) / 128 <= 8 &&
                      (H / 64) % 2 == 0 && (F / 64) % 2 == 0 && H % 8 == 0;
 
+  // diagnostics: TF_SPLITS="q,o,f1,f2" forces the decode split counts (0 = auto)
+  static const std::vector<int> force_splits = [] {
+    std::vector<int> v(4, 0);
+    if (const char* e = getenv("TF_SPLITS")) sscanf(e, "%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3]);
+    return v;
+  }();
+  const bool fs = T == 1;
+
   for (int l = 0; l < L; ++l) {
     const tf_layer_weights& w = s.m->layers[l];
     // fused QKV projection, K/V straight into the cache (model.py:464-474)
@@ -960,6 +985,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     q.cap = sd.capacity;
     q.seq_len = T;
     q.qbase_dev = sd.len_dev;
+    if (fs && force_splits[0]) q.splits = force_splits[0];
     if (coop) set_ln(q, w.ln1_gamma, w.ln1_beta, 1, 0);
     static const bool qkv_late = [] {  // TF_QKV_LATE=0 disables (A/B diagnostics)
       const char* e = getenv("TF_QKV_LATE");
@@ -1062,6 +1088,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     o.ldo = m.ldk_h;
     o.resid = x;
     o.ldr = m.ldk_h;
+    if (fs && force_splits[1]) o.splits = force_splits[1];
     GemmExtra oex = pf_next(l, 1);
     if (rowln) {
       o.splits = 2;
@@ -1109,6 +1136,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     f1.bias = w.b1;
     f1.out = sd.ffn;
     f1.ldo = m.ldk_f;
+    if (fs && force_splits[2]) f1.splits = force_splits[2];
     if (dg) {
       f1.act = x;  // ffn_norm (model.py:484-486) inside the GEMM
       run_dgemm(f1, p1, w.ln2_gamma, w.ln2_beta, pf_next(l, 2), st);
@@ -1136,6 +1164,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     f2.ldo = m.ldk_h;
     f2.resid = x;
     f2.ldr = m.ldk_h;
+    if (fs && force_splits[3]) f2.splits = force_splits[3];
     // next layer's attn_norm, or final_norm (model.py:460-462, 497-498)
     LnArgs nl = ln;
     if (l + 1 < L) {
