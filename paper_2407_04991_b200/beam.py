@@ -86,6 +86,10 @@ class BeamRun:
         nbytes = s.load_inputs(self.ids, self.pos, self.pads)
         s.indir.copy_((torch.arange(B, device=s.indir.device, dtype=torch.int32) % K)[:, None]
                       .expand(B, s.capacity))
+        # prompt slots hold identical K/V in every beam row of a request: all
+        # beams read them from beam 0's row (children inherit the entry), so the
+        # shared prefix streams from DRAM once per request instead of once per beam
+        s.indir[:, :self.L] = 0
         s.scores.fill_(float("-inf"))
         s.scores[::K] = 0.0
         s.finished.zero_()

@@ -438,8 +438,16 @@ __global__ void __launch_bounds__(kPfThreads) attn_decode_pf_kernel(const AttnAr
   const size_t row_stride = (size_t)a.NH * a.cap * D, head_stride = (size_t)a.cap * D;
   const int* ind = a.indir ? a.indir + (size_t)b * a.cap : nullptr;
   const int beam0 = a.indir ? (b / a.beam) * a.beam : b;
+  // beam: this CTA's slice of the indirection row staged in smem once (one
+  // coalesced load instead of a dependent global load per copied segment)
+  __shared__ int s_ind[4 * 64];
+  const int slot0 = lo + c0 * 64;
+  if (ind != nullptr) {
+    for (int i = tid; i < nc * 64; i += kPfThreads) s_ind[i] = slot0 + i < hi ? ind[slot0 + i] : 0;
+    __syncthreads();
+  }
   auto kv_off = [&](int s) -> size_t {
-    const int src = ind ? beam0 + ind[s] : b;
+    const int src = ind ? beam0 + (s - slot0 < nc * 64 && s >= slot0 && s < hi ? s_ind[s - slot0] : ind[s]) : b;
     return (size_t)src * row_stride + (size_t)h * head_stride + (size_t)s * D;
   };
   // ---- before the wait: K/V of every slot < hi in this CTA's chunks

@@ -723,7 +723,11 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
     t.trace = trace_next("attn_decode_pf");
     const size_t smem = attn_pf_smem_bytes(t.group);
     // 256 threads only when the grid is several waves anyway (large batch)
-    const bool wide = (size_t)ngr * a.NH * a.B > (size_t)4 * num_sms();
+    static const int wide_env = [] {  // TF_ATTN_WIDE=0/1 forces the thread count (A/B)
+      const char* e = getenv("TF_ATTN_WIDE");
+      return e ? atoi(e) : -1;
+    }();
+    const bool wide = wide_env >= 0 ? wide_env != 0 : (size_t)ngr * a.NH * a.B > (size_t)4 * num_sms();
     if (a.wo_t) {
       if (wide)
         launch_pf<true, 256>(dim3(ngr, a.NH, a.B), smem, st, pdl, t);

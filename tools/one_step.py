@@ -18,6 +18,20 @@ def main():
     model = bench.build_model(w)
     run = bench.Runner(model, bench.make_prompts(model.config.vocab_size, w, 0), w)
     run.stage()
+    if run.beam:  # beam: prefill + select, warm steps, then one (T=1 forward + select) step
+        import ctypes as C
+        br, s = run.beam, run.sess
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        s.forward(br.L, N.FWD_LOGITS_LAST)
+        N.check(N.lib().tf_beam_select(s.handle, C.byref(br.desc), st), "tf_beam_select")
+        N.check(N.lib().tf_beam_decode(s.handle, C.byref(br.desc), 4, 0, st), "tf_beam_decode")
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("step")
+        N.check(N.lib().tf_beam_decode(s.handle, C.byref(br.desc), 1, 0, st), "tf_beam_decode")
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
+        print("ok")
+        return
     run.sess.forward(run.ids.shape[1], N.FWD_ARGMAX)
     run.sess.decode(4, use_graph=False)
     torch.cuda.synchronize()
