@@ -234,8 +234,9 @@ struct GemmPlan {
   int bn, tiles_a, tiles_b, k_blocks, splits, stages;
 };
 
-// Deterministic split count: a function of (features, K) only, never of the
-// batch, so decode results are batch-invariant. Splits form one cluster per
+// Deterministic split count: a function of (features, K, row tiles), so
+// decode results are batch-invariant for batches <= 64 (one row tile); above
+// that the row-tile count can change the split (and summation) order. Splits form one cluster per
 // tile: up to 8 (portable) when there are many tiles, up to 16 (non-portable,
 // one cluster per GPC) when a few tiles must cover the machine.
 // The largest split count whose grid stays within 128 CTAs: every cluster is
@@ -258,7 +259,16 @@ GemmPlan plan_gemm(const tf_gemm_desc& d, bool ln_coop = false) {
   p.k_blocks = (d.k + 63) / 64;
   p.swap = d.force_swap >= 0 ? d.force_swap != 0 : d.m_tok <= 256;
   if (p.swap) {
-    const int mt = d.m_tok < 256 ? d.m_tok : 256;
+    // decode batch tile: <= 64 rows for the split-K GEMMs (batch 128: two row
+    // tiles with half the split count each -> smaller partial tiles to reduce;
+    // C3 step 798 -> 714 us); the argmax lm_head keeps whole-batch tiles.
+    // TF_BN_MAX overrides (A/B)
+    static const int bn_max = [] {
+      const char* e = getenv("TF_BN_MAX");
+      return e ? atoi(e) : 64;
+    }();
+    const int cap_bn = d.epilogue == TF_EPI_LOGITS ? 256 : bn_max;
+    const int mt = d.m_tok < cap_bn ? d.m_tok : cap_bn;
     p.bn = ((mt + 15) / 16) * 16;
     if (p.bn < 16) p.bn = 16;
     p.tiles_a = (d.n_feat + 127) / 128;
