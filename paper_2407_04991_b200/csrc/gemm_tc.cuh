@@ -349,6 +349,52 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
   __syncthreads();
   const int cpr = bn * ESZ / 16;  // 16-byte chunks per row
   const int epc = 16 / ESZ;       // elements per chunk
+  if constexpr (MODE == EPI_BIAS_RESID) {
+    // residual chunks are loaded 8 at a time before use (one exposed global
+    // latency per 8 chunks instead of per chunk)
+    constexpr int BATCH = 8;
+    for (int base = threadIdx.x; base < kTileA * cpr; base += 128 * BATCH) {
+      uint4 rv[BATCH];
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) {
+        const int idx = base + u * 128;
+        const int r = idx / cpr, ch = idx - r * cpr;
+        const int t = tile_a * kTileA + r, f0 = tile_b * bn + ch * 8;
+        const bool fast = idx < kTileA * cpr && t < p.m_tok && f0 + 8 <= p.n_feat && (p.ldr % 8) == 0;
+        rv[u] = fast ? *reinterpret_cast<const uint4*>(p.resid + (size_t)t * p.ldr + f0) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) {
+        const int idx = base + u * 128;
+        if (idx >= kTileA * cpr) break;
+        const int r = idx / cpr, ch = idx - r * cpr;
+        const int t = tile_a * kTileA + r, f0 = tile_b * bn + ch * 8;
+        if (t >= p.m_tok || f0 >= p.n_feat) continue;
+        const uint4 val = *reinterpret_cast<const uint4*>(stage + (size_t)r * pitch + ch * 16);
+        const bool full = f0 + 8 <= p.n_feat;
+        float a8[8], r8[8];
+        unpack8(val, a8);
+        if (full && (p.ldr % 8) == 0) {
+          unpack8(rv[u], r8);
+        } else {
+          const __half* rp = p.resid + (size_t)t * p.ldr + f0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) r8[e] = f0 + e < p.n_feat ? __half2float(rp[e]) : 0.0f;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a8[e] = __fadd_rn(r8[e], a8[e]);
+        const uint4 res = pack8(a8);
+        __half* o = p.out + (size_t)t * p.ldo + f0;
+        if (full && (p.ldo % 8) == 0) {
+          *reinterpret_cast<uint4*>(o) = res;
+        } else {
+          const __half* hv = reinterpret_cast<const __half*>(&res);
+          for (int e = 0; e < 8 && f0 + e < p.n_feat; ++e) o[e] = hv[e];
+        }
+      }
+    }
+    return;
+  }
   for (int idx = threadIdx.x; idx < kTileA * cpr; idx += 128) {
     const int r = idx / cpr, ch = idx - r * cpr;
     const int t = tile_a * kTileA + r;
