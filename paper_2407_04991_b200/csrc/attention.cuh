@@ -59,6 +59,9 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool v
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
                : "memory");
 }
+// release/acquire ordering for the last-arriver merges (cheaper than the
+// sequentially consistent fence __threadfence() emits)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(kSplitThreads) attn_decode_split_kernel(const 
     }
   }
   if (nch == 1) return;
-  __threadfence();
+  fence_acq_rel_gpu();
   __syncthreads();
   if (tid == 0) {
     tr.mark(a.trace, 3);
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(kSplitThreads) attn_decode_split_kernel(const 
     }
     return;
   }
-  __threadfence();
+  fence_acq_rel_gpu();
   // merge in chunk order: M = max m_c, Z = sum z_c e^(m_c - M), O = sum o_c e^(m_c - M)
   if (tid < D) {
     float M = -INFINITY;
@@ -401,6 +404,7 @@ __global__ void __launch_bounds__(kSplitThreads) attn_decode_split_kernel(const 
 // the merge is local; otherwise partials go to the workspace and the
 // last-arriving CTA merges them.
 constexpr int kPfKeysPerChunk = 64, kPfChunkBytes = 2 * 64 * 64 * 2;  // K + V, f16
+constexpr int kPfMaxG = 8;  // chunks per CTA at most
 __host__ __device__ inline size_t attn_pf_smem_bytes(int G) {
   return (size_t)G * kPfChunkBytes + (size_t)G * (66 + 64) * sizeof(float);
 }
@@ -412,8 +416,8 @@ template <bool WO, int kPfThreads>
 __global__ void __launch_bounds__(kPfThreads) attn_decode_pf_kernel(const AttnArgs a) {
   extern __shared__ __align__(128) uint8_t pf_smem[];
   __shared__ __align__(16) float qs[64];
-  __shared__ float sc_all[4 * 64];
-  __shared__ float ew_all[4 * 64];
+  __shared__ float sc_all[kPfMaxG * 64];
+  __shared__ float ew_all[kPfMaxG * 64];
   __shared__ int s_last;
   constexpr int D = 64;
   TF_TRACE_INIT(tr);
@@ -440,7 +444,7 @@ __global__ void __launch_bounds__(kPfThreads) attn_decode_pf_kernel(const AttnAr
   const int beam0 = a.indir ? (b / a.beam) * a.beam : b;
   // beam: this CTA's slice of the indirection row staged in smem once (one
   // coalesced load instead of a dependent global load per copied segment)
-  __shared__ int s_ind[4 * 64];
+  __shared__ int s_ind[kPfMaxG * 64];
   const int slot0 = lo + c0 * 64;
   if (ind != nullptr) {
     for (int i = tid; i < nc * 64; i += kPfThreads) s_ind[i] = slot0 + i < hi ? ind[slot0 + i] : 0;
@@ -640,7 +644,7 @@ __global__ void __launch_bounds__(kPfThreads) attn_decode_pf_kernel(const AttnAr
   } else {
     float* part = a.ws + (((size_t)b * a.NH + h) * a.max_chunks) * 66;
     for (int e = tid; e < nc * 66; e += kPfThreads) __stcg(part + (size_t)c0 * 66 + e, part_s[e]);
-    __threadfence();
+    fence_acq_rel_gpu();
     __syncthreads();
     if (tid == 0) {
       const int prev = atomicAdd(a.cnt + (size_t)b * a.NH + h, 1);
@@ -648,7 +652,7 @@ __global__ void __launch_bounds__(kPfThreads) attn_decode_pf_kernel(const AttnAr
     }
     __syncthreads();
     if (s_last) {
-      __threadfence();
+      fence_acq_rel_gpu();
       if (tid < D) {
         float M = -INFINITY;
         for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(part + (size_t)cc * 66));

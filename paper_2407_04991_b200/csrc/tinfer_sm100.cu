@@ -719,7 +719,7 @@ void launch_pf(dim3 grid, size_t smem, cudaStream_t st, bool pdl, const AttnArgs
   static bool attr = false;
   if (!attr) {
     TF_CHECK_CUDA(cudaFuncSetAttribute(attn_decode_pf_kernel<WO, THREADS>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_pf_smem_bytes(4)));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_pf_smem_bytes(kPfMaxG)));
     set_max_carveout(attn_decode_pf_kernel<WO, THREADS>);
     attr = true;
   }
@@ -736,8 +736,12 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
       pf_mode) {
     // chunks per CTA: the whole window when it is <= 4 chunks (local merge),
     // else groups of <= 4 (64 KB of K/V each) merged through the workspace
+    static const int gmax = [] {  // TF_ATTN_G: max 64-slot chunks per CTA (A/B), <= kPfMaxG
+      const char* e = getenv("TF_ATTN_G");
+      return e ? std::max(1, std::min(kPfMaxG, atoi(e))) : 4;
+    }();
     const int nch = a.max_chunks;
-    const int ngr = (nch + 3) / 4;
+    const int ngr = (nch + gmax - 1) / gmax;
     TF_REQUIRE(a.wo_t == nullptr || ngr == 1, TF_ERR_ARG, "attention: fused Wo needs the window in one CTA");
     AttnArgs t = a;
     t.group = (nch + ngr - 1) / ngr;
