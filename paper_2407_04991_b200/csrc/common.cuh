@@ -15,11 +15,20 @@ namespace tf {
 
 constexpr float kF16Max = 65504.0f;
 
-// f32 -> f16, saturating, RNE (reference round_to). Comparisons are false for
-// NaN, so NaN passes through unchanged like np.clip.
+// f32 -> f16, saturating, RNE (reference round_to), in one F2FP.SATFINITE
+// instruction: cvt.rn.satfinite clamps to +-65504 and
+// rounds to nearest even, NaN -> NaN; bit-identical to the clamp-then-RNE form
+// over all 2^32 f32 inputs (tools/satfinite_check.cu).
 __device__ __forceinline__ __half f16_sat(float x) {
-  x = (x > kF16Max) ? kF16Max : ((x < -kF16Max) ? -kF16Max : x);
-  return __float2half_rn(x);
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(0.0f), "f"(x));
+  return __ushort_as_half((unsigned short)(r & 0xffffu));
+}
+// two values -> packed f16x2 (lo = a, hi = b), same rounding as f16_sat
+__device__ __forceinline__ uint32_t f16x2_sat(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
 }
 __device__ __forceinline__ float q16(float x) { return __half2float(f16_sat(x)); }
 
@@ -308,11 +317,7 @@ __device__ __forceinline__ void unpack8(const uint4& r, float* f) {
   }
 }
 __device__ __forceinline__ uint4 pack8(const float* f) {
-  uint4 r;
-  __half* h = reinterpret_cast<__half*>(&r);
-#pragma unroll
-  for (int e = 0; e < 8; ++e) h[e] = f16_sat(f[e]);
-  return r;
+  return make_uint4(f16x2_sat(f[0], f[1]), f16x2_sat(f[2], f[3]), f16x2_sat(f[4], f[5]), f16x2_sat(f[6], f[7]));
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

@@ -319,6 +319,12 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
   const int pitch = bn * ESZ + 16;
   const int row = threadIdx.x;
   const int tok = tile_a * kTileA + row;
+  // the tile's bias columns, loaded once (not one dependent load per element)
+  __shared__ float s_bias[256];
+  if constexpr (MODE != EPI_F32 && MODE != EPI_LOGITS) {
+    for (int c = threadIdx.x; c < bn; c += 128) s_bias[c] = p.bias[min(tile_b * bn + c, p.n_feat - 1)];
+    __syncthreads();
+  }
   float v[16];
   for (int c = 0; c < bn; c += 16) {
     tmem_ld16(trow + (uint32_t)c, v);
@@ -331,13 +337,12 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
       float y[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const int f = min(tile_b * bn + c + j, p.n_feat - 1);
         if constexpr (MODE == EPI_BIAS || MODE == EPI_QKV) {
-          y[j] = __fadd_rn(v[j], p.bias[f]);
+          y[j] = __fadd_rn(v[j], s_bias[c + j]);
         } else if constexpr (MODE == EPI_BIAS_GELU) {
-          y[j] = gelu_ref(__fadd_rn(v[j], p.bias[f]));
+          y[j] = gelu_ref(__fadd_rn(v[j], s_bias[c + j]));
         } else if constexpr (MODE == EPI_BIAS_RESID) {
-          y[j] = __fadd_rn(v[j], p.bias[f]);  // rounded to f16 here, residual added below
+          y[j] = __fadd_rn(v[j], s_bias[c + j]);  // rounded to f16 here, residual added below
         } else {  // EPI_LOGITS
           y[j] = v[j];
         }
