@@ -417,7 +417,9 @@ def run_ours(args):
     # ---------------- rooflines
     H, F, V, L = c.hidden_size, c.ffn_size, c.vocab_size, c.num_layers
     S = w["batch"] * w["beam"]
-    step_bytes = [decode_step_bytes(L, H, F, V, S, S * (w["src"] + i)) for i in range(1, w["new"])]
+    # live context: the prompt once per request (beams share it: SURVEY 8d shared
+    # prefix, read from beam 0's rows) + the generated slots per row
+    step_bytes = [decode_step_bytes(L, H, F, V, S, w["batch"] * w["src"] + S * i) for i in range(1, w["new"])]
     t_step = probe_decode_step(torch, run, flush, stream, w)
     step_bw = float(np.mean(step_bytes)) / t_step / 1e9
     kern = probe_dominant_kernel(torch, dm, run.sess, flush, stream, S)
@@ -456,8 +458,24 @@ def run_ours(args):
 def probe_decode_step(torch, run, flush, stream, w):
     """Median per-decode-step time (CUDA events around the graph-replayed steps)."""
     from paper_2407_04991_b200 import _native as N
-    if run.beam:
-        return float("nan")
+    if run.beam:  # prefill + first select untimed, then the graph-replayed beam steps
+        import ctypes as C
+        br, s = run.beam, run.sess
+        ts = []
+        for _ in range(3):
+            run.stage()
+            st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+            s.forward(br.L, N.FWD_LOGITS_LAST)
+            N.check(N.lib().tf_beam_select(s.handle, C.byref(br.desc), st), "tf_beam_select")
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            N.check(N.lib().tf_beam_decode(s.handle, C.byref(br.desc), w["new"] - 1, 1, st), "tf_beam_decode")
+            e1.record(stream)
+            e1.synchronize()
+            s.len += w["new"] - 1
+            ts.append(e0.elapsed_time(e1) / 1e3 / (w["new"] - 1))
+        return float(statistics.median(ts))
     ts = []
     for _ in range(5):
         run.stage()
