@@ -310,20 +310,33 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& p, int ra, int qb, con
 // after the per-element math, then written out cooperatively: each thread moves
 // 16-byte chunks of one row (8 f16 / 4 f32), consecutive threads consecutive
 // chunks, with the residual read and the Q/K/V routing done per chunk.
-template <int MODE>
+// NAMED: run by the 4 epilogue warps of the persistent prefill kernel (named
+// barrier 1 instead of __syncthreads); `row` = this thread's TMEM lane / tile
+// row (a bijection over 0..127); `tmem_free` (mbarrier, or 0) is arrived once
+// every TMEM read of the tile is done, so the MMA warp can refill the buffer
+// while the stores drain.
+template <int MODE, bool NAMED = false>
 __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, int tile_b, uint32_t trow,
-                                                 uint8_t* stage) {
+                                                 uint8_t* stage, int row_ = -1, uint32_t tmem_free = 0) {
+  auto esync = [] {
+    if constexpr (NAMED)
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    else
+      __syncthreads();
+  };
   constexpr bool F32OUT = MODE == EPI_F32;
   constexpr int ESZ = F32OUT ? 4 : 2;
   const int bn = p.bn;
   const int pitch = bn * ESZ + 16;
-  const int row = threadIdx.x;
+  const int row = row_ >= 0 ? row_ : (int)threadIdx.x;
   const int tok = tile_a * kTileA + row;
   // the tile's bias columns, loaded once (not one dependent load per element)
   __shared__ float s_bias[256];
   if constexpr (MODE != EPI_F32 && MODE != EPI_LOGITS) {
-    for (int c = threadIdx.x; c < bn; c += 128) s_bias[c] = p.bias[min(tile_b * bn + c, p.n_feat - 1)];
-    __syncthreads();
+    for (int c = row; c < bn; c += 128) s_bias[c] = p.bias[min(tile_b * bn + c, p.n_feat - 1)];
+    esync();
+  } else if constexpr (NAMED) {
+    esync();  // persistent loop: the previous tile's stores have drained the staging buffer
   }
   float v[16];
   for (int c = 0; c < bn; c += 16) {
@@ -351,14 +364,16 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
       *reinterpret_cast<uint4*>(dst + 16) = pack8(y + 8);
     }
   }
-  __syncthreads();
+  if (tmem_free) tc_fence_before();
+  esync();
+  if (tmem_free && row == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tmem_free) : "memory");
   const int cpr = bn * ESZ / 16;  // 16-byte chunks per row
   const int epc = 16 / ESZ;       // elements per chunk
   if constexpr (MODE == EPI_BIAS_RESID) {
     // residual chunks are loaded 8 at a time before use (one exposed global
     // latency per 8 chunks instead of per chunk)
     constexpr int BATCH = 8;
-    for (int base = threadIdx.x; base < kTileA * cpr; base += 128 * BATCH) {
+    for (int base = row; base < kTileA * cpr; base += 128 * BATCH) {
       uint4 rv[BATCH];
 #pragma unroll
       for (int u = 0; u < BATCH; ++u) {
@@ -400,7 +415,7 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
     }
     return;
   }
-  for (int idx = threadIdx.x; idx < kTileA * cpr; idx += 128) {
+  for (int idx = row; idx < kTileA * cpr; idx += 128) {
     const int r = idx / cpr, ch = idx - r * cpr;
     const int t = tile_a * kTileA + r;
     const int f0 = tile_b * bn + ch * epc;
@@ -1079,6 +1094,122 @@ __global__ void __launch_bounds__(128, 1)
     }
     if (threadIdx.x == 0) tr.mark(p.trace, 6);
     cluster_wait_any();  // partial tiles stay alive until every CTA has read them
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tr.mark(p.trace, 7);
+    tr.flush(p.trace);
+  }
+  if (warp == 2) tmem_dealloc(tmem, ncols);
+}
+
+// ---------------------------------------------------------------- persistent prefill GEMM
+// Non-swap (token-major) GEMM for prefill-sized M: one CTA per SM loops over
+// output tiles; warp 0 streams A/B k-blocks through a `stages`-deep TMA ring
+// across tile boundaries, warp 1 issues tcgen05.mma into one of TWO TMEM
+// accumulators, warps 2-5 run the staged epilogue of the previous tile from the
+// other accumulator (released to the MMA warp as soon as its TMEM reads are
+// done). Tiles are visited token-tile-fastest so the CTAs running at the same
+// time share the weight tile (L2 reuse).
+constexpr int kPfThreadsGemm = 192;
+__host__ __device__ inline size_t gemm_pf_smem_bytes(int bn, int stages, bool f32out) {
+  return 1024 + (size_t)stages * gemm_stage_bytes(bn) + (size_t)kTileA * (bn * (f32out ? 4 : 2) + 16) +
+         (size_t)(2 * stages + 4) * 8 + 16;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kPfThreadsGemm, 1)
+    gemm_pf_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const GemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  constexpr bool F32OUT = MODE == EPI_F32;
+  const int bn = p.bn, stages = p.stages;
+  const int stage_bytes = gemm_stage_bytes(bn);
+  uint8_t* out_stage = smem + (size_t)stages * stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(out_stage + (size_t)kTileA * (bn * (F32OUT ? 4 : 2) + 16));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 4);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + stages);
+  const uint32_t accf0 = smem_u32(bars + 2 * stages), acce0 = smem_u32(bars + 2 * stages + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_a = (p.m_tok + kTileA - 1) / kTileA, tiles_b = (p.n_feat + bn - 1) / bn;
+  const int n_tiles = tiles_a * tiles_b, nkb = p.k_blocks;
+  const uint32_t ncols = 2 * bn <= 32 ? 32u : (2 * bn <= 64 ? 64u : (2 * bn <= 128 ? 128u : (2 * bn <= 256 ? 256u : 512u)));
+  TF_TRACE_INIT(tr);
+  if (threadIdx.x == 0) tr.mark(p.trace, 0);
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), ncols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) tr.mark(p.trace, 1);
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer, continuous over tiles
+      int it = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int ta = t % tiles_a, tb = t / tiles_a;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % stages;
+          const uint32_t ph = (uint32_t)(it / stages) & 1u;
+          mbar_wait(empty0 + 8 * s, ph ^ 1u);
+          const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
+          mbar_expect_tx(full0 + 8 * s, (uint32_t)stage_bytes);
+          tma_load_2d(sa, &tmA, kb * kBK, ta * kTileA, full0 + 8 * s);
+          tma_load_2d(sa + kABytes, &tmB, kb * kBK, tb * bn, full0 + 8 * s);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer, two TMEM accumulators
+      const uint32_t idesc = idesc_f16_m128((uint32_t)bn);
+      int it = 0, tc = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tc) {
+        const int b = tc & 1, use = tc >> 1;
+        mbar_wait(acce0 + 8 * b, ((uint32_t)use & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(b * bn);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % stages;
+          const uint32_t ph = (uint32_t)(it / stages) & 1u;
+          mbar_wait(full0 + 8 * s, ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
+          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + kABytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) tc_mma_f16(acc, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          tc_commit(empty0 + 8 * s);
+        }
+        tc_commit(accf0 + 8 * b);
+      }
+    }
+  } else {  // ---- epilogue warps 2..5 (TMEM lane quadrant = warp % 4)
+    const int q = warp & 3, row = q * 32 + lane;
+    int tc = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tc) {
+      const int ta = t % tiles_a, tb = t / tiles_a;
+      const int b = tc & 1, use = tc >> 1;
+      mbar_wait(accf0 + 8 * b, (uint32_t)use & 1u);
+      tc_fence_after();
+      const uint32_t trow = tmem + (uint32_t)(b * bn) + ((uint32_t)(q * 32) << 16);
+      epi_tile_nonswap<MODE, true>(p, ta, tb, trow, out_stage, row, acce0 + 8 * b);
+    }
   }
   tc_fence_before();
   __syncthreads();

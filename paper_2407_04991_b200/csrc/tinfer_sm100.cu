@@ -366,6 +366,30 @@ void launch_gemm_t(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& 
                               : (p.splits == 1 ? RED_ONE : (gemm_push_reduce(p.bn, p.splits, SWAP) ? RED_PUSH : RED_PULL));
   const int lnv = (SWAP && d.ln_x) ? (args.ln_coop ? 2 : 1) : 0;
   if constexpr (!SWAP) {
+    // opt-in (TF_PF_PERSIST=1): measured slower than two one-tile CTAs per SM,
+    // whose two epilogues run side by side (the ~6 us staged epilogue bounds both)
+    static const bool persist = [] {
+      const char* e = getenv("TF_PF_PERSIST");
+      return e && e[0] == '1';
+    }();
+    if (red == RED_ONE && persist && (MODE != EPI_LOGITS || args.keys == nullptr)) {
+      // persistent tile loop, two TMEM accumulators, ring as deep as smem allows
+      static bool done = false;
+      if (!done) {
+        TF_CHECK_CUDA(cudaFuncSetAttribute(gemm_pf_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kMaxSmem));
+        done = true;
+      }
+      GemmArgs a2 = args;
+      const size_t fixed = gemm_pf_smem_bytes(p.bn, 0, MODE == EPI_F32);
+      int stages = (int)((kMaxSmem - fixed) / gemm_stage_bytes(p.bn));
+      stages = std::max(2, std::min(stages, 8));
+      a2.stages = stages;
+      const int n_tiles = p.tiles_a * p.tiles_b;
+      const dim3 grid(std::min(n_tiles, num_sms()));
+      return launch_cluster(gemm_pf_kernel<MODE>, grid, dim3(kPfThreadsGemm),
+                            gemm_pf_smem_bytes(p.bn, stages, MODE == EPI_F32), st, d.pdl != 0, 1, ta, tb, a2);
+    }
     if (red == RED_ONE) return launch_gemm_v<MODE, false, RED_ONE, 0>(d, p, ta, tb, args, st);
     return launch_gemm_v<MODE, false, RED_PULL, 0>(d, p, ta, tb, args, st);
   } else {
