@@ -315,7 +315,10 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& p, int ra, int qb, con
 // row (a bijection over 0..127); `tmem_free` (mbarrier, or 0) is arrived once
 // every TMEM read of the tile is done, so the MMA warp can refill the buffer
 // while the stores drain.
-template <int MODE, bool NAMED = false>
+// NT = 256: eight warps; warps w and w + 4 share TMEM lane quadrant w % 4 and
+// split the tile's columns in halves (the phase-1 TMEM reads and math are
+// latency-bound with one warp per scheduler).
+template <int MODE, bool NAMED = false, int NT = 128>
 __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, int tile_b, uint32_t trow,
                                                  uint8_t* stage, int row_ = -1, uint32_t tmem_free = 0) {
   auto esync = [] {
@@ -328,18 +331,21 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
   constexpr int ESZ = F32OUT ? 4 : 2;
   const int bn = p.bn;
   const int pitch = bn * ESZ + 16;
-  const int row = row_ >= 0 ? row_ : (int)threadIdx.x;
+  const int et = row_ >= 0 ? row_ : (int)threadIdx.x;  // linear epilogue thread id, 0 .. NT-1
+  const int row = NT == 256 ? (int)(((threadIdx.x >> 5) & 3) * 32 + (threadIdx.x & 31)) : et;
+  const int c_begin = NT == 256 ? (int)(threadIdx.x >> 7) * (p.bn / 2) : 0;
+  const int c_end = NT == 256 ? c_begin + p.bn / 2 : p.bn;
   const int tok = tile_a * kTileA + row;
   // the tile's bias columns, loaded once (not one dependent load per element)
   __shared__ float s_bias[256];
   if constexpr (MODE != EPI_F32 && MODE != EPI_LOGITS) {
-    for (int c = row; c < bn; c += 128) s_bias[c] = p.bias[min(tile_b * bn + c, p.n_feat - 1)];
+    for (int c = et; c < bn; c += NT) s_bias[c] = p.bias[min(tile_b * bn + c, p.n_feat - 1)];
     esync();
   } else if constexpr (NAMED) {
     esync();  // persistent loop: the previous tile's stores have drained the staging buffer
   }
   float v[16];
-  for (int c = 0; c < bn; c += 16) {
+  for (int c = c_begin; c < c_end; c += 16) {
     tmem_ld16(trow + (uint32_t)c, v);
     uint8_t* dst = stage + (size_t)row * pitch + (size_t)c * ESZ;
     if constexpr (F32OUT) {
@@ -373,11 +379,11 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
     // residual chunks are loaded 8 at a time before use (one exposed global
     // latency per 8 chunks instead of per chunk)
     constexpr int BATCH = 8;
-    for (int base = row; base < kTileA * cpr; base += 128 * BATCH) {
+    for (int base = et; base < kTileA * cpr; base += NT * BATCH) {
       uint4 rv[BATCH];
 #pragma unroll
       for (int u = 0; u < BATCH; ++u) {
-        const int idx = base + u * 128;
+        const int idx = base + u * NT;
         const int r = idx / cpr, ch = idx - r * cpr;
         const int t = tile_a * kTileA + r, f0 = tile_b * bn + ch * 8;
         const bool fast = idx < kTileA * cpr && t < p.m_tok && f0 + 8 <= p.n_feat && (p.ldr % 8) == 0;
@@ -385,7 +391,7 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
       }
 #pragma unroll
       for (int u = 0; u < BATCH; ++u) {
-        const int idx = base + u * 128;
+        const int idx = base + u * NT;
         if (idx >= kTileA * cpr) break;
         const int r = idx / cpr, ch = idx - r * cpr;
         const int t = tile_a * kTileA + r, f0 = tile_b * bn + ch * 8;
@@ -415,7 +421,7 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
     }
     return;
   }
-  for (int idx = row; idx < kTileA * cpr; idx += 128) {
+  for (int idx = et; idx < kTileA * cpr; idx += NT) {
     const int r = idx / cpr, ch = idx - r * cpr;
     const int t = tile_a * kTileA + r;
     const int f0 = tile_b * bn + ch * epc;
@@ -802,8 +808,14 @@ enum GemmRed : int {
 };
 // LayerNorm of the B operand built in-kernel: 0 none, 1 full-row staging
 // (ln_build_b), 2 cluster-cooperative (ln_coop_build)
+// threads per CTA: the prefill (non-swap, full-K) tiles run their staged
+// epilogue with eight warps
+__host__ __device__ constexpr int gemm_threads(int mode, bool swap, int red) {
+  return (!swap && red == RED_ONE && mode != EPI_LOGITS) ? 256 : 128;
+}
+
 template <int MODE, bool SWAP, int RED, int LNV>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs p) {
   extern __shared__ uint8_t smem_raw[];
@@ -957,7 +969,8 @@ __global__ void __launch_bounds__(128, 1)
     if constexpr (MODE == EPI_BIAS_RESID && SWAP) gemm_rowln_epilogue(p, trow, smem);
   } else if constexpr (RED == RED_ONE && !SWAP) {
     if (MODE != EPI_LOGITS || p.keys == nullptr) {
-      epi_tile_nonswap<MODE>(p, tile_a, tile_b, tmem + (uint32_t)(warp * 32 << 16), smem);
+      epi_tile_nonswap<MODE, false, gemm_threads(MODE, SWAP, RED)>(p, tile_a, tile_b,
+                                                                   tmem + (uint32_t)((warp & 3) * 32 << 16), smem);
     } else {
       for (int c = 0; c < bn; c += 16) {
         tmem_ld16(trow + (uint32_t)c, v);
