@@ -369,12 +369,14 @@ class KVCache:
 # validation helpers (reference model.py:507-514)
 # ---------------------------------------------------------------------------
 def _check_ids(config: ModelConfig, ids) -> list[int]:
-    out = []
-    for t in ids:
-        t = int(t)
+    # int() per id as the reference does (model.py:507-514); one min/max range
+    # check, and the first offending id reported by the scalar loop
+    out = list(map(int, ids))
+    if not out or (min(out) >= 0 and max(out) < config.vocab_size):
+        return out
+    for t in out:
         if not 0 <= t < config.vocab_size:
             raise VocabError(f"token id {t} out of range [0, {config.vocab_size})")
-        out.append(t)
     return out
 
 
@@ -596,9 +598,9 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
     COUNTERS.launches += n_dec
     global LAST_STATS
     LAST_STATS = stats
+    # append up to and including each row's first eos (model.py:656-661)
+    hit = toks == c.eos_token
+    cut = np.where(hit.any(axis=1), hit.argmax(axis=1) + 1, toks.shape[1])
     for i in range(B):
-        for tok in toks[i]:
-            seqs[i].append(int(tok))
-            if int(tok) == c.eos_token:
-                break
+        seqs[i].extend(toks[i, :cut[i]].tolist())
     return seqs
