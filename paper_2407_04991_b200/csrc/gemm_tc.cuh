@@ -809,13 +809,14 @@ enum GemmRed : int {
 // LayerNorm of the B operand built in-kernel: 0 none, 1 full-row staging
 // (ln_build_b), 2 cluster-cooperative (ln_coop_build)
 // threads per CTA: the prefill (non-swap, full-K) tiles run their staged
-// epilogue with eight warps
-__host__ __device__ constexpr int gemm_threads(int mode, bool swap, int red) {
-  return (!swap && red == RED_ONE && mode != EPI_LOGITS) ? 256 : 128;
+// epilogue with eight warps; so does the decode push reduction (one pass over
+// the CTA's units instead of two at batch 32 with 6 or fewer splits)
+__host__ __device__ constexpr int gemm_threads(int mode, bool swap, int red, int lnv = 0) {
+  return ((!swap && red == RED_ONE && mode != EPI_LOGITS) || (swap && red == RED_PUSH && lnv == 0)) ? 256 : 128;
 }
 
 template <int MODE, bool SWAP, int RED, int LNV>
-__global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED), 1)
+__global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs p) {
   extern __shared__ uint8_t smem_raw[];
@@ -991,11 +992,19 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED), 1)
     // reduces them from local smem in split order 0..S-1 (deterministic; the
     // same sums as the pull form). No cluster barrier on the data path; the
     // CTA only waits for its outgoing copies to finish reading before exit.
+    constexpr int NT = gemm_threads(MODE, SWAP, RED, LNV);
     float* part = reinterpret_cast<float*>(smem);
-    for (int c = 0; c < bn; c += 16) {
-      tmem_ld16(trow + (uint32_t)c, v);
+    {
+      // warps w and w + 4 share TMEM lane quadrant w % 4 and park column halves
+      const int prow = (warp & 3) * 32 + lane;
+      const int pc0 = NT == 256 ? (warp >> 2) * (bn / 2) : 0, pc1 = NT == 256 ? pc0 + bn / 2 : bn;
+      const uint32_t prow_t = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+      for (int c = pc0; c < pc1; c += 16) {
+        tmem_ld16(prow_t + (uint32_t)c, v);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) part[(c + j) * kTileA + row] = v[j];
+        for (int j = 0; j < 16; ++j)
+          if (c + j < pc1) part[(c + j) * kTileA + prow] = v[j];
+      }
     }
     fence_proxy_async_smem();  // generic smem writes -> visible to the bulk-copy engine
     const uint32_t rank = cluster_ctarank();
@@ -1024,12 +1033,12 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED), 1)
     EpiPre4 pre, pre2;
     int u = u_lo + (int)threadIdx.x;
     if (u < u_hi) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
-    if (u + 128 < u_hi) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u + 128, pre2);
+    if (u + NT < u_hi) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u + NT, pre2);
     mbar_wait(recv_bar, 0);
     if (threadIdx.x == 0) tr.mark(p.trace, 4);
     const float4* own = reinterpret_cast<const float4*>(part);
     const float4* rin = reinterpret_cast<const float4*>(recv);
-    for (int it = 0; u < u_hi; u += 128, ++it) {
+    for (int it = 0; u < u_hi; u += NT, ++it) {
       const bool first = it == 0;
       if (it == 1) pre = pre2;
       if (it >= 2) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);

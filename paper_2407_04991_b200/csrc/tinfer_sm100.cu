@@ -351,10 +351,10 @@ void launch_gemm_v(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& 
                : (LNV == 1 ? gemm_ln_bytes(p.bn, p.k_blocks / p.splits, p.k_blocks) : 0);
   const size_t smem = gemm_smem_bytes(p.bn, p.stages, p.splits, SWAP, ln_bytes);
   if (RED == RED_ROWLN)
-    launch_cluster3(gemm_tc_kernel<MODE, SWAP, RED, LNV>, grid, dim3(gemm_threads(MODE, SWAP, RED)), smem, st,
+    launch_cluster3(gemm_tc_kernel<MODE, SWAP, RED, LNV>, grid, dim3(gemm_threads(MODE, SWAP, RED, LNV)), smem, st,
                     d.pdl != 0, grid, ta, tb, args);
   else
-    launch_cluster(gemm_tc_kernel<MODE, SWAP, RED, LNV>, grid, dim3(gemm_threads(MODE, SWAP, RED)), smem, st,
+    launch_cluster(gemm_tc_kernel<MODE, SWAP, RED, LNV>, grid, dim3(gemm_threads(MODE, SWAP, RED, LNV)), smem, st,
                    d.pdl != 0, p.splits, ta, tb,
                    args);
 }
