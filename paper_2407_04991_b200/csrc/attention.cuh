@@ -412,8 +412,10 @@ __host__ __device__ inline size_t attn_pf_smem_bytes(int G) {
 // per thread for QK^T, every chunk half its own warp; large batches)
 
 // WO: the fused output projection epilogue (AttnArgs::wo_t) is compiled in
-template <bool WO, int kPfThreads>
-__global__ void __launch_bounds__(kPfThreads) attn_decode_pf_kernel(const AttnArgs a) {
+// MINB: resident CTAs per SM the register budget must allow (3 lets a
+// batch-32 step's 384 CTAs of 256 threads run in one wave)
+template <bool WO, int kPfThreads, int MINB = 1>
+__global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const AttnArgs a) {
   extern __shared__ __align__(128) uint8_t pf_smem[];
   __shared__ __align__(16) float qs[64];
   __shared__ float sc_all[kPfMaxG * 64];

@@ -740,16 +740,16 @@ void run_ln(const LnArgs& a0, cudaStream_t st, bool pdl) {
   }
 }
 
-template <bool WO, int THREADS>
+template <bool WO, int THREADS, int MINB = 1>
 void launch_pf(dim3 grid, size_t smem, cudaStream_t st, bool pdl, const AttnArgs& t) {
   static bool attr = false;
   if (!attr) {
-    TF_CHECK_CUDA(cudaFuncSetAttribute(attn_decode_pf_kernel<WO, THREADS>,
+    TF_CHECK_CUDA(cudaFuncSetAttribute(attn_decode_pf_kernel<WO, THREADS, MINB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_pf_smem_bytes(kPfMaxG)));
-    set_max_carveout(attn_decode_pf_kernel<WO, THREADS>);
+    set_max_carveout(attn_decode_pf_kernel<WO, THREADS, MINB>);
     attr = true;
   }
-  launch(attn_decode_pf_kernel<WO, THREADS>, grid, dim3(THREADS), smem, st, pdl, t);
+  launch(attn_decode_pf_kernel<WO, THREADS, MINB>, grid, dim3(THREADS), smem, st, pdl, t);
 }
 
 void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
@@ -773,22 +773,32 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
     t.group = (nch + ngr - 1) / ngr;
     t.trace = trace_next("attn_decode_pf");
     const size_t smem = attn_pf_smem_bytes(t.group);
-    // 256 threads only when the grid is several waves anyway (large batch)
-    static const int wide_env = [] {  // TF_ATTN_WIDE=0/1 forces the thread count (A/B)
+    // 128 threads by default; TF_ATTN_WIDE=1 selects 256 threads (registers
+    // capped for 3 CTAs per SM while the grid fits one such wave, uncapped for
+    // multi-wave grids): faster in the eager trace, within noise / slightly
+    // slower in graph-replayed bench runs on the same box (C2 85.3k vs 86.5k,
+    // C3 178.1k vs 181.8k)
+    static const int wide_env = [] {
       const char* e = getenv("TF_ATTN_WIDE");
-      return e ? atoi(e) : -1;
+      return e ? atoi(e) : 0;
     }();
-    const bool wide = wide_env >= 0 ? wide_env != 0 : (size_t)ngr * a.NH * a.B > (size_t)4 * num_sms();
+    const size_t ctas = (size_t)ngr * a.NH * a.B;
+    const bool one_wave = ctas <= (size_t)3 * num_sms();
+    const dim3 grid(ngr, a.NH, a.B);
     if (a.wo_t) {
-      if (wide)
-        launch_pf<true, 256>(dim3(ngr, a.NH, a.B), smem, st, pdl, t);
+      if (wide_env == 0)
+        launch_pf<true, 128>(grid, smem, st, pdl, t);
+      else if (one_wave)
+        launch_pf<true, 256, 3>(grid, smem, st, pdl, t);
       else
-        launch_pf<true, 128>(dim3(ngr, a.NH, a.B), smem, st, pdl, t);
+        launch_pf<true, 256>(grid, smem, st, pdl, t);
     } else {
-      if (wide)
-        launch_pf<false, 256>(dim3(ngr, a.NH, a.B), smem, st, pdl, t);
+      if (wide_env == 0)
+        launch_pf<false, 128>(grid, smem, st, pdl, t);
+      else if (one_wave)
+        launch_pf<false, 256, 3>(grid, smem, st, pdl, t);
       else
-        launch_pf<false, 128>(dim3(ngr, a.NH, a.B), smem, st, pdl, t);
+        launch_pf<false, 256>(grid, smem, st, pdl, t);
     }
   } else if (a.T == 1 && a.D == 64 && a.ws && a.cnt && a.max_chunks >= (a.cap + kSplitKeys - 1) / kSplitKeys) {
     AttnArgs t = a;
