@@ -463,7 +463,11 @@ __global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const 
     if (slot != hi) {  // slots past the window are zero-filled (src-size 0)
       const bool ok = slot < hi;
       const size_t off = ok ? kv_off(slot) + part * 8 : 0;
-      __half* kd = kvs + ((size_t)(2 * i) * 64 + j) * 64 + part * 8;
+      // K rows are stored with their 16-byte segments rotated by the row index
+      // (segment g of row j at position (g + j) & 7): the QK^T loop then reads
+      // logical segment g of 8 consecutive rows from 8 distinct bank groups
+      // while indexing q with the compile-time g
+      __half* kd = kvs + ((size_t)(2 * i) * 64 + j) * 64 + ((part + j) & 7) * 8;
       __half* vd = kvs + ((size_t)(2 * i + 1) * 64 + j) * 64 + part * 8;
       cp_async16(smem_u32(kd), a.kc + off, ok);
       cp_async16(smem_u32(vd), a.vc + off, ok);
@@ -493,7 +497,7 @@ __global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const 
       const int part = tid & 7;
       const size_t off = kv_off(hi) + part * 8;
       const __half* src = (tid < 8 ? a.kc : a.vc) + off;
-      __half* dst = kvs + ((size_t)(2 * i + (tid < 8 ? 0 : 1)) * 64 + j) * 64 + part * 8;
+      __half* dst = kvs + ((size_t)(2 * i + (tid < 8 ? 0 : 1)) * 64 + j) * 64 + (tid < 8 ? ((part + j) & 7) : part) * 8;
       *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
     }
   }
@@ -506,26 +510,32 @@ __global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const 
   // distinct bank groups; 8 independent partial dot products, summed in that
   // order (fixed by the key's position in its chunk -> batch-invariant)
   const int n_keys = min(nc * 64, n - c0 * 64);
+  // q in registers (logical segment g = dims 8g .. 8g+7); per key 8 partial dot
+  // products (one per segment, fixed order within), summed as a fixed tree
+  float qr[64];
+#pragma unroll
+  for (int e = 0; e < 64; e += 4) {
+    const float4 q4 = *reinterpret_cast<const float4*>(qs + e);
+    qr[e] = q4.x;
+    qr[e + 1] = q4.y;
+    qr[e + 2] = q4.z;
+    qr[e + 3] = q4.w;
+  }
   for (int key = tid; key < n_keys; key += kPfThreads) {
     const int i = key >> 6, j = key & 63;
     const __half* kr = kvs + ((size_t)(2 * i) * 64 + j) * 64;
+    uint4 raw[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) raw[g] = *reinterpret_cast<const uint4*>(kr + ((g + j) & 7) * 8);
     float ps[8];
 #pragma unroll
-    for (int s8 = 0; s8 < 8; ++s8) {
-      const int seg = (s8 + j) & 7;
+    for (int g = 0; g < 8; ++g) {
       float kf[8];
-      unpack8(*reinterpret_cast<const uint4*>(kr + seg * 8), kf);
-      const float4 qa = *reinterpret_cast<const float4*>(qs + seg * 8);
-      const float4 qb = *reinterpret_cast<const float4*>(qs + seg * 8 + 4);
-      float acc = __fmul_rn(qa.x, kf[0]);
-      acc = __fadd_rn(acc, __fmul_rn(qa.y, kf[1]));
-      acc = __fadd_rn(acc, __fmul_rn(qa.z, kf[2]));
-      acc = __fadd_rn(acc, __fmul_rn(qa.w, kf[3]));
-      acc = __fadd_rn(acc, __fmul_rn(qb.x, kf[4]));
-      acc = __fadd_rn(acc, __fmul_rn(qb.y, kf[5]));
-      acc = __fadd_rn(acc, __fmul_rn(qb.z, kf[6]));
-      acc = __fadd_rn(acc, __fmul_rn(qb.w, kf[7]));
-      ps[s8] = acc;
+      unpack8(raw[g], kf);
+      float acc = __fmul_rn(qr[8 * g], kf[0]);
+#pragma unroll
+      for (int e = 1; e < 8; ++e) acc = __fadd_rn(acc, __fmul_rn(qr[8 * g + e], kf[e]));
+      ps[g] = acc;
     }
     const float d = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
                               __fadd_rn(__fadd_rn(ps[4], ps[5]), __fadd_rn(ps[6], ps[7])));
