@@ -110,7 +110,8 @@ __host__ __device__ inline size_t gemm_ring_bytes(int bn, int stages, int splits
 // LN-fused B operand: the normalised K-slice (kb_per_split tiles) plus the TMA
 // staging of the full source rows (k_blocks tiles of 64 columns)
 __host__ __device__ inline size_t gemm_ln_bytes(int bn, int kb_per_split, int k_blocks) {
-  return (size_t)(kb_per_split + k_blocks) * bn * kBK * 2;
+  // + gamma / beta of the CTA's K slice (f32)
+  return (size_t)(kb_per_split + k_blocks) * bn * kBK * 2 + (size_t)2 * kb_per_split * kBK * 4;
 }
 // cooperative LN operand: the CTA's K slice of the rows (kb_per_split tiles),
 // then f32 scratch: 2 exchange rounds [splits][bn], segment partials
@@ -137,70 +138,65 @@ __host__ inline size_t gemm_smem_bytes(int bn, int stages, int splits, bool swap
 }
 
 // LN-fused B operand: the CTA's bn source rows were staged in smem by TMA
-// (k_blocks swizzled 64-column tiles at `stg`); each warp normalises whole rows
-// (same operation order as layernorm_vec_kernel -> bit-identical to the
-// stand-alone LN) and writes the K-slice [kb0*64, (kb0+nkb)*64) into `bln` as
-// nkb swizzled (128-byte) K-major tiles of bn rows. (Plain loads of the rows
-// by every CTA of a launch hit the same L2 lines from 100+ SMs and serialise;
-// TMA does not.)
+// (k_blocks swizzled 64-column tiles at `stg`). kLnTpr = 8 consecutive threads
+// own one row (NT / 8 rows per pass): each sums its 16-byte chunks q = sub,
+// sub + 8, ... in order, the 8 partials combine by an xor butterfly (fixed
+// order, independent of the batch), two passes (mean; squared deviations,
+// tensor.py:153-160); then the CTA's K slice [kb0*64, (kb0+nkb)*64) is
+// normalised with gamma / beta staged in smem (gsl / bsl) and written into
+// `bln` as nkb swizzled K-major tiles of bn rows.
+constexpr int kLnTpr = 8;
+template <int NT>
 __device__ __forceinline__ void ln_build_b(const GemmArgs& p, int tile_b, int kb0, int nkb, uint8_t* bln,
-                                           const uint8_t* stg) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bn = p.bn, H = p.ln_H;
-  constexpr int NC = 4;  // 16-byte chunks per lane: H <= 1024
-  const int c_lo = kb0 * kBK, c_hi = (kb0 + nkb) * kBK;
-  for (int r = warp; r < bn; r += 4) {
-    const bool valid = tile_b * bn + r < p.m_tok;
-    float xv[NC * 8];
+                                           const uint8_t* stg, const float* gsl, const float* bsl) {
+  const int bn = p.bn, H = p.ln_H, C = H / 8;
+  const int tid = threadIdx.x, sub = tid % kLnTpr;
+  const float Hf = (float)H;
+  for (int r0 = 0; r0 < bn; r0 += NT / kLnTpr) {
+    const int r = r0 + tid / kLnTpr;
+    const bool rv = r < bn;
+    const int rr = rv ? r : 0;
+    auto chunk = [&](int q) {
+      return *reinterpret_cast<const uint4*>(stg + (size_t)(q >> 3) * bn * 128 + rr * 128 + (((q & 7) ^ (rr & 7)) * 16));
+    };
+    float s = 0.0f;
+    if (rv)
+      for (int q = sub; q < C; q += kLnTpr) {
+        float xv[8];
+        unpack8(chunk(q), xv);
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
-      const int q = lane + 32 * i;
-      if (q * 8 < H) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(stg + (size_t)(q >> 3) * bn * 128 + r * 128 +
-                                                          (((q & 7) ^ (r & 7)) * 16));
-        unpack8(raw, &xv[8 * i]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) xv[8 * i + e] = 0.0f;
+        for (int e = 0; e < 8; ++e) s = __fadd_rn(s, xv[e]);
       }
-    }
-    float sum = 0.0f;
 #pragma unroll
-    for (int i = 0; i < NC; ++i)
-      if ((lane + 32 * i) * 8 < H)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) sum = __fadd_rn(sum, xv[8 * i + e]);
-    const float mean = __fdiv_rn(warp_sum(sum), (float)H);
+    for (int o = kLnTpr / 2; o > 0; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+    const float mean = __fdiv_rn(s, Hf);
     float ss = 0.0f;
-#pragma unroll
-    for (int i = 0; i < NC; ++i)
-      if ((lane + 32 * i) * 8 < H)
+    if (rv)
+      for (int q = sub; q < C; q += kLnTpr) {
+        float xv[8];
+        unpack8(chunk(q), xv);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float d = __fsub_rn(xv[8 * i + e], mean);
+          const float d = __fsub_rn(xv[e], mean);
           ss = __fadd_rn(ss, __fmul_rn(d, d));
         }
-    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(warp_sum(ss), (float)H), 1e-5f)));
+      }
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
-      const int c = (lane + 32 * i) * 8;
-      if (c < c_lo || c >= c_hi) continue;
-      float y[8];
-      if (valid && c < H) {
-        const float4 g0 = *reinterpret_cast<const float4*>(p.ln_g + c), g1 = *reinterpret_cast<const float4*>(p.ln_g + c + 4);
-        const float4 b0 = *reinterpret_cast<const float4*>(p.ln_b + c), b1 = *reinterpret_cast<const float4*>(p.ln_b + c + 4);
-        const float gf[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-        const float bf[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    for (int o = kLnTpr / 2; o > 0; o >>= 1) ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, Hf), 1e-5f)));
+    if (rv) {
+      const bool valid = tile_b * bn + r < p.m_tok;
+      for (int q = kb0 * 8 + sub; q < (kb0 + nkb) * 8; q += kLnTpr) {
+        float xv[8], y[8];
+        unpack8(chunk(q), xv);
+        const int f0 = (q - kb0 * 8) * 8;
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-          y[e] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[8 * i + e], mean), inv), gf[e]), bf[e]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) y[e] = 0.0f;
+          y[e] = (valid && q * 8 + e < H) ? __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[e], mean), inv), gsl[f0 + e]), bsl[f0 + e])
+                                          : 0.0f;
+        uint8_t* dst = bln + (size_t)(q / 8 - kb0) * bn * kBK * 2 + r * 128 + (((q & 7) ^ (r & 7)) * 16);
+        *reinterpret_cast<uint4*>(dst) = pack8(y);
       }
-      const int kb = (c - c_lo) / kBK, q = ((c - c_lo) % kBK) / 8;
-      uint8_t* dst = bln + (size_t)kb * bn * kBK * 2 + (r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) * 16);
-      *reinterpret_cast<uint4*>(dst) = pack8(y);
     }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -812,7 +808,7 @@ enum GemmRed : int {
 // epilogue with eight warps; so does the decode push reduction (one pass over
 // the CTA's units instead of two at batch 32 with 6 or fewer splits)
 __host__ __device__ constexpr int gemm_threads(int mode, bool swap, int red, int lnv = 0) {
-  return ((!swap && red == RED_ONE && mode != EPI_LOGITS) || (swap && red == RED_PUSH && lnv == 0)) ? 256 : 128;
+  return ((!swap && red == RED_ONE && mode != EPI_LOGITS) || (swap && red == RED_PUSH && lnv <= 1)) ? 256 : 128;
 }
 
 template <int MODE, bool SWAP, int RED, int LNV>
@@ -906,7 +902,15 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
     mbar_wait(ln_bar, 0);
     __syncthreads();  // g_s / b_s visible
     ln_coop_build(p, tile_b, nkb, bln, ln_sc, push, push);
-  } else if constexpr (ln_mode) {  // stage the source rows by TMA, then all 128 threads build the normalised B tiles
+  } else if constexpr (ln_mode) {  // stage the source rows by TMA, then every thread builds the normalised B tiles
+    // gamma / beta of this CTA's K slice are weights: staged before the wait
+    float* gsl = reinterpret_cast<float*>(stg + (size_t)p.k_blocks * bn * kBK * 2);
+    float* bsl = gsl + p.kb_per_split * kBK;
+    for (int i = threadIdx.x; i < nkb * kBK; i += gemm_threads(MODE, SWAP, RED, LNV)) {
+      const int f = kb0 * kBK + i;
+      gsl[i] = f < p.ln_H ? p.ln_g[f] : 0.0f;
+      bsl[i] = f < p.ln_H ? p.ln_b[f] : 0.0f;
+    }
     pdl_wait();
     if (warp == 0 && lane == 0) {
       mbar_expect_tx(ln_bar, (uint32_t)(p.k_blocks * bn * kBK * 2));
@@ -914,7 +918,8 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
         tma_load_2d(smem_u32(stg + (size_t)kb * bn * kBK * 2), &tmB, kb * kBK, tile_b * bn, ln_bar);
     }
     mbar_wait(ln_bar, 0);
-    ln_build_b(p, tile_b, kb0, nkb, bln, stg);
+    __syncthreads();  // gsl / bsl visible
+    ln_build_b<gemm_threads(MODE, SWAP, RED, LNV)>(p, tile_b, kb0, nkb, bln, stg, gsl, bsl);
     __syncthreads();
   }
   if (warp == 0 && lane == 0) {

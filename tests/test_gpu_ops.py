@@ -163,8 +163,10 @@ def test_embed_gather_sum_bit_exact_and_remap(cuda_device):
 
 @pytest.mark.parametrize("m,n,k", [(32, 2304, 768), (5, 200, 128), (32, 1000, 768)])
 def test_gemm_fused_layernorm_operand(cuda_device, m, n, k):
-    """Swap-AB GEMM whose activation operand is LN(x) built in-kernel equals
-    LN kernel + GEMM (bitwise: same LN operation order)."""
+    """Swap-AB GEMM whose activation operand is LN(x) built in-kernel matches
+    LN kernel + GEMM. The in-kernel LN sums each row with 8 threads (fixed
+    order) instead of the LN kernel's 32 lanes, so an f16-rounded LN value can
+    differ by one ulp: compared within 5e-3 absolute."""
     x = rand16(m, k, seed=20).to(cuda_device)
     g = (1 + 0.05 * torch.randn(k)).half().float().to(cuda_device)
     b = (0.05 * torch.randn(k)).half().float().to(cuda_device)
@@ -186,4 +188,4 @@ def test_gemm_fused_layernorm_operand(cuda_device, m, n, k):
     import ctypes as C
     N.check(N.lib().tf_gemm(C.byref(d), C.c_void_p(torch.cuda.current_stream().cuda_stream)), "tf_gemm")
     torch.cuda.synchronize()
-    assert torch.equal(got, ref)
+    assert (got - ref).abs().max().item() <= 5e-3
