@@ -202,6 +202,15 @@ __device__ __forceinline__ void ln_build_b(const GemmArgs& p, int tile_b, int kb
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// elect.sync over the full warp (lane 0 when every lane is active)
+__device__ __forceinline__ bool elect_lane0() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\telect.sync r|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 template <int MODE, bool SWAP>
 __device__ __forceinline__ void epi_store(const GemmArgs& p, int tok, int f, float acc) {
   if constexpr (MODE == EPI_F32) {
@@ -937,8 +946,12 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
       }
       if (!ln_mode) tma_load_2d(sb, &tmB, (kb0 + i) * kBK, tile_b * bn, full0 + 8 * s);
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- single-thread MMA issuer
+  } else if (warp == 1) {
+    // ---------------- MMA issue: the whole warp walks the k-blocks (warp-
+    // uniform control flow keeps descriptors in uniform registers: ~35-40
+    // instead of ~60 cycles per tcgen05.mma, tools/mma_rate.cu); the elected
+    // lane (always lane 0 with the full warp active) issues the MMAs and the
+    // commits, which track that thread's MMAs
     const uint32_t idesc = idesc_f16_m128((uint32_t)bn);
     for (int i = 0; i < nkb; ++i) {
       const int s = i % stages;
@@ -948,14 +961,17 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
       const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
       const uint64_t da = umma_desc_sw128(sa);
       const uint64_t db = umma_desc_sw128(ln_mode ? smem_u32(bln + (size_t)i * bn * kBK * 2) : sa + kABytes);
+      if (elect_lane0()) {
 #pragma unroll
-      for (int k = 0; k < kBK / 16; ++k) {
-        // advance 16 f16 = 32 B along K inside the swizzle atom (+2 in 16-B units)
-        tc_mma_f16(tmem, da + 2 * k, db + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+        for (int k = 0; k < kBK / 16; ++k) {
+          // advance 16 f16 = 32 B along K inside the swizzle atom (+2 in 16-B units)
+          tc_mma_f16(tmem, da + 2 * k, db + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+        }
+        tc_commit(empty0 + 8 * s);
       }
-      tc_commit(empty0 + 8 * s);
+      __syncwarp();
     }
-    tc_commit(done_bar);
+    if (elect_lane0()) tc_commit(done_bar);
   }
   __syncwarp();
 
