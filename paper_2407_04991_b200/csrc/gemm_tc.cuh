@@ -83,6 +83,10 @@ struct GemmArgs {
   // the new residual rows over DSMEM (gemm_rowln_epilogue); writes out (x) and
   // lnf_h = q16(LN(x)) with lnf_g / lnf_b
   int row_ln;
+  // RED_PUSHLN: lnf_cnt[token] counts the features of a row stored so far; the
+  // CTA that completes a row normalises it (gemm_ln_tail), writes lnf_h and
+  // resets the counter
+  int* lnf_cnt;
   const float* lnf_g;
   const float* lnf_b;
   __half* lnf_h;
@@ -802,6 +806,63 @@ __device__ __noinline__ void gemm_rowln_epilogue(const GemmArgs& p, uint32_t tro
   }
 }
 
+// LayerNorm of the rows this CTA completes (RED_PUSHLN). [u_lo, u_hi): the
+// CTA's reduction units (unit u = token column u / 32, features 4 * (u % 32)
+// .. +3 of the tile). Release: every thread's x stores, a CTA barrier, then one
+// acq_rel fence; each touched token gets one atomicAdd (its own thread) of the
+// features this CTA stored; the add that completes n_feat makes this CTA the
+// row's normaliser (acquire fence, L2 reads of the row). Arithmetic: the
+// stand-alone LN kernel's (ln_row_apply), so h is bit-identical to it.
+template <int NT>
+__device__ __forceinline__ void gemm_ln_tail(const GemmArgs& p, int tile_a, int tile_b, int u_lo, int u_hi) {
+  __shared__ int s_rows[64];
+  __shared__ int s_nrows;
+  if (threadIdx.x == 0) s_nrows = 0;
+  __syncthreads();  // every thread's x stores happen-before the fences below
+  const int c_lo = u_lo / 32, c_hi = u_hi > u_lo ? (u_hi - 1) / 32 : c_lo - 1;
+  for (int c = c_lo + (int)threadIdx.x; c <= c_hi; c += NT) {
+    const int tok = tile_b * p.bn + c;
+    if (tok >= p.m_tok) continue;
+    int n = 0;
+    for (int u = max(u_lo, c * 32); u < min(u_hi, c * 32 + 32); ++u)
+      n += max(0, min(4, p.n_feat - (tile_a * kTileA + (u % 32) * 4)));
+    if (n == 0) continue;
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // release (cumulative over the barrier)
+    const int prev = atomicAdd(p.lnf_cnt + tok, n);
+    if (prev + n == p.n_feat) s_rows[atomicAdd(&s_nrows, 1)] = tok;
+  }
+  __syncthreads();
+  const int nl = s_nrows;
+  if (nl == 0) return;
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NC = 4;  // H <= 1024; chunks past H are skipped (same sums as NC = ceil(H/256))
+  float4 gv[NC * 2], bv[NC * 2];
+  ln_load_gb<NC>(p.n_feat, p.lnf_g, p.lnf_b, lane, gv, bv);
+  for (int i = warp; i < nl; i += NT / 32) {
+    const int tok = s_rows[i];
+    const __half* xr = p.out + (size_t)tok * p.ldo;
+    uint4 raw[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int c = (lane + 32 * j) * 8;
+      if (c < p.n_feat) raw[j] = __ldcg(reinterpret_cast<const uint4*>(xr + c));
+    }
+    float xv[NC * 8];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      if ((lane + 32 * j) * 8 < p.n_feat) {
+        unpack8(raw[j], &xv[8 * j]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xv[8 * j + e] = 0.0f;
+      }
+    }
+    ln_row_apply<NC>(xv, p.n_feat, gv, bv, p.lnf_h + (size_t)tok * p.lnf_ldh, lane);
+    if (lane == 0) p.lnf_cnt[tok] = 0;
+  }
+}
+
 // Reduction / epilogue path of a launch (template parameter, so every
 // instantiation carries only the code it executes: decode kernels are
 // i-cache-bound when they carry all paths)
@@ -810,6 +871,7 @@ enum GemmRed : int {
   RED_PUSH = 1,   // split-K cluster, push form (swap, bn <= 128)
   RED_PULL = 2,   // split-K cluster, pull form
   RED_ROWLN = 3,  // whole-row cluster + fused LayerNorm (EPI_BIAS_RESID, swap)
+  RED_PUSHLN = 4,  // push split-K + LayerNorm of completed rows by their last CTA (EPI_BIAS_RESID)
 };
 // LayerNorm of the B operand built in-kernel: 0 none, 1 full-row staging
 // (ln_build_b), 2 cluster-cooperative (ln_coop_build)
@@ -817,7 +879,9 @@ enum GemmRed : int {
 // epilogue with eight warps; so does the decode push reduction (one pass over
 // the CTA's units instead of two at batch 32 with 6 or fewer splits)
 __host__ __device__ constexpr int gemm_threads(int mode, bool swap, int red, int lnv = 0) {
-  return ((!swap && red == RED_ONE && mode != EPI_LOGITS) || (swap && red == RED_PUSH && lnv <= 1)) ? 256 : 128;
+  return ((!swap && red == RED_ONE && mode != EPI_LOGITS) || (swap && (red == RED_PUSH || red == RED_PUSHLN) && lnv <= 1))
+             ? 256
+             : 128;
 }
 
 template <int MODE, bool SWAP, int RED, int LNV>
@@ -837,7 +901,7 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
                                  : 0);
   float* ln_sc = reinterpret_cast<float*>(bln + (size_t)p.kb_per_split * bn * kBK * 2);  // coop scratch
   uint8_t* stg = bln + (size_t)p.kb_per_split * bn * kBK * 2;  // LN source rows (ln_mode)
-  constexpr bool push = RED == RED_PUSH;
+  constexpr bool push = RED == RED_PUSH || RED == RED_PUSHLN;
   uint64_t* bars = reinterpret_cast<uint64_t*>(recv + gemm_recv_bytes(bn, p.splits, SWAP));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 3);
   __shared__ unsigned long long red[64];
@@ -1004,7 +1068,7 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
       tmem_ld16(trow + (uint32_t)c, v);
       epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, reinterpret_cast<unsigned long long*>(smem));
     }
-  } else if constexpr (RED == RED_PUSH) {
+  } else if constexpr (RED == RED_PUSH || RED == RED_PUSHLN) {
     // Split-K across the CTAs of one cluster, push form. Each CTA parks its f32
     // partial tile ([column][128 rows], in the drained ring), then one thread
     // bulk-copies the slice owned by every peer r (units [r*per, r*per+per),
@@ -1080,6 +1144,7 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
       tr.mark(p.trace, 6);
       bulk_wait_read_all();  // outgoing slices read before this smem is released
     }
+    if constexpr (RED == RED_PUSHLN && MODE == EPI_BIAS_RESID) gemm_ln_tail<NT>(p, tile_a, tile_b, u_lo, u_hi);
   } else {
     static_assert(RED == RED_PULL, "reduction path");
     // Split-K across the CTAs of one thread-block cluster (grid.z == cluster.z

@@ -369,7 +369,8 @@ template <int MODE, bool SWAP>
 void launch_gemm_t(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& ta,
                    const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
   const int red = args.row_ln ? RED_ROWLN
-                              : (p.splits == 1 ? RED_ONE : (gemm_push_reduce(p.bn, p.splits, SWAP) ? RED_PUSH : RED_PULL));
+                  : args.lnf_cnt ? RED_PUSHLN
+                  : (p.splits == 1 ? RED_ONE : (gemm_push_reduce(p.bn, p.splits, SWAP) ? RED_PUSH : RED_PULL));
   const int lnv = (SWAP && d.ln_x) ? (args.ln_coop ? 2 : 1) : 0;
   if constexpr (!SWAP) {
     // opt-in (TF_PF_PERSIST=1): measured slower than two one-tile CTAs per SM,
@@ -402,6 +403,10 @@ void launch_gemm_t(const tf_gemm_desc& d, const GemmPlan& p, const CUtensorMap& 
     if (red == RED_ROWLN) {
       if constexpr (MODE == EPI_BIAS_RESID) return launch_gemm_v<MODE, true, RED_ROWLN, 0>(d, p, ta, tb, args, st);
       throw TfError{TF_ERR_UNSUPPORTED, "gemm: row-LN epilogue needs EPI_BIAS_RESID"};
+    }
+    if (red == RED_PUSHLN) {
+      if constexpr (MODE == EPI_BIAS_RESID) return launch_gemm_v<MODE, true, RED_PUSHLN, 0>(d, p, ta, tb, args, st);
+      throw TfError{TF_ERR_UNSUPPORTED, "gemm: last-arriver LN epilogue needs EPI_BIAS_RESID"};
     }
     if (lnv == 0) {
       if (red == RED_ONE) return launch_gemm_v<MODE, true, RED_ONE, 0>(d, p, ta, tb, args, st);
@@ -438,6 +443,7 @@ struct GemmExtra {
   unsigned long long l2pf_bytes = 0;
   int ln_coop = 0;  // with desc.ln_x: cooperative cluster LayerNorm (gemm_tc.cuh ln_coop_build)
   int row_ln = 0;   // EPI_BIAS_RESID: whole rows in one cluster + fused LN (gemm_rowln_epilogue)
+  int* lnf_cnt = nullptr;  // EPI_BIAS_RESID push split-K: LN of completed rows by their last CTA
   const float* lnf_g = nullptr;
   const float* lnf_b = nullptr;
   void* lnf_h = nullptr;
@@ -483,6 +489,17 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st, const GemmExtra& ex = Gemm
   a.late_trigger = d.pdl == 2 ? 1 : 0;
   a.l2pf = ex.l2pf;
   a.l2pf_bytes = ex.l2pf_bytes;
+  if (ex.lnf_cnt) {
+    TF_REQUIRE(p.swap && gemm_push_reduce(p.bn, p.splits, true) && d.epilogue == TF_EPI_BIAS_RESID &&
+                   d.n_feat <= 1024 && d.n_feat % 8 == 0 && d.ldo % 8 == 0 && ex.lnf_g && ex.lnf_b && ex.lnf_h &&
+                   ex.lnf_ldh % 8 == 0 && p.bn / 32 + 2 <= 64,
+               TF_ERR_ARG, "gemm: last-arriver LN epilogue not applicable");
+    a.lnf_cnt = ex.lnf_cnt;
+    a.lnf_g = ex.lnf_g;
+    a.lnf_b = ex.lnf_b;
+    a.lnf_h = static_cast<__half*>(ex.lnf_h);
+    a.lnf_ldh = ex.lnf_ldh;
+  }
   if (ex.row_ln) {
     TF_REQUIRE(p.swap && p.splits == 2 && d.epilogue == TF_EPI_BIAS_RESID && p.tiles_b == 1 && p.bn <= 64 &&
                    p.tiles_a * 2 <= 16 && ex.lnf_g && ex.lnf_b && ex.lnf_h &&
@@ -1011,6 +1028,19 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
                        (sd.capacity + 63) / 64 <= 4 && H % 8 == 0 && H <= 2048 && m.ldk_h % 8 == 0 &&
                        sd.workspace && sd.workspace_bytes >= (size_t)B * NH * H * sizeof(float) && sd.counters &&
                        sd.n_counters >= B * NH;
+  // decode: the LayerNorm after each residual GEMM (Wo -> ffn_norm, FFN2 ->
+  // next attn_norm / final_norm) runs in that GEMM's epilogue: the CTA whose
+  // stores complete a row normalises it (RED_PUSHLN), no LN launch. Opt-in
+  // (TF_LN_TAIL=1): fence + counter + dependent row reload add ~4 us to each
+  // residual GEMM vs the 2.4 us LN launch they replace
+  static const bool lntail_on = [] {
+    const char* e = getenv("TF_LN_TAIL");
+    return e && e[0] == '1';
+  }();
+  int* ln_cnt = (lntail_on && T == 1 && !fuse_ln && !dg && !coop && H <= 1024 && H % 8 == 0 && m.ldk_h % 8 == 0 &&
+                 sd.counters && sd.n_counters >= B * NH + M)
+                    ? sd.counters + B * NH
+                    : nullptr;
   // decode, batch <= 64: the two residual GEMMs (Wo, FFN2) run as ONE cluster
   // covering whole output rows (tiles x 2 K-halves <= 16 CTAs) and fuse the
   // following LayerNorm into their epilogue (gemm_rowln_epilogue). Opt-in
@@ -1022,6 +1052,11 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
   }();
   const bool rowln = rowln_on && !dg && !coop && !fuse_ln && T == 1 && M <= 64 && (H + 127) / 128 <= 8 &&
                      (H / 64) % 2 == 0 && (F / 64) % 2 == 0 && H % 8 == 0;
+  if (rowln) ln_cnt = nullptr;
+  auto push_plan = [&](const tf_gemm_desc& d) {
+    const GemmPlan gp = plan_gemm(d);
+    return gp.swap && gemm_push_reduce(gp.bn, gp.splits, true) && gp.bn / 32 + 2 <= 64;
+  };
 
   // diagnostics: TF_SPLITS="q,o,f1,f2" forces the decode split counts (0 = auto)
   static const std::vector<int> force_splits = [] {
@@ -1168,6 +1203,14 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
       oex.lnf_ldh = m.ldk_h;
     }
     if (pdl && T == 1 && (late_mask & 1)) o.pdl = 2;
+    const bool o_tail = ln_cnt && !skip_wo && push_plan(o);
+    if (o_tail) {
+      oex.lnf_cnt = ln_cnt;
+      oex.lnf_g = w.ln2_gamma;
+      oex.lnf_b = w.ln2_beta;
+      oex.lnf_h = h;
+      oex.lnf_ldh = m.ldk_h;
+    }
     if (skip_wo) {
     } else if (dg) {
       run_dgemm(o, po, nullptr, nullptr, oex, st);
@@ -1188,7 +1231,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     ln.b = w.ln2_beta;
     ln.h = h;
     ln.ldh = m.ldk_h;
-    if (!fuse_ln && !dg && !coop && !rowln && !skip_wo) {
+    if (!fuse_ln && !dg && !coop && !rowln && !skip_wo && !o_tail) {
       run_ln(ln, st, pdl);
       ++launches;
     }
@@ -1258,12 +1301,20 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
       f2ex.lnf_ldh = m.ldk_h;
     }
     if (pdl && T == 1 && (late_mask & 4)) f2.pdl = 2;
+    const bool f2_tail = ln_cnt && push_plan(f2);
+    if (f2_tail) {  // T == 1: every row is the last position
+      f2ex.lnf_cnt = ln_cnt;
+      f2ex.lnf_g = nl.g;
+      f2ex.lnf_b = nl.b;
+      f2ex.lnf_h = h;
+      f2ex.lnf_ldh = m.ldk_h;
+    }
     if (dg)
       run_dgemm(f2, p2, nullptr, nullptr, f2ex, st);
     else
       run_gemm(f2, st, f2ex);
     ++launches;
-    if (rowln) continue;
+    if (rowln || f2_tail) continue;
     if ((dg || coop) && l + 1 < L) continue;  // the next QKV normalises its own operand
     if (l + 1 < L ? !fuse_ln : !fuse_final) {
       run_ln(nl, st, pdl);

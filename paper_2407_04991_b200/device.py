@@ -192,7 +192,8 @@ class Session:
         # (also the per-head partials of the attention-fused output projection)
         self.att_ws = torch.empty(max(1, batch * dm.NH * chunks * 66, batch * dm.NH * dm.H), dtype=torch.float32,
                                   device=dev)
-        self.att_cnt = torch.zeros(batch * dm.NH, dtype=torch.int32, device=dev)
+        # (+ one row-completion counter per token for the last-arriver LayerNorm)
+        self.att_cnt = torch.zeros(batch * dm.NH + batch * max(1, max_tokens), dtype=torch.int32, device=dev)
         d.workspace, d.workspace_bytes = self.att_ws.data_ptr(), self.att_ws.numel() * 4
         d.counters, d.n_counters = self.att_cnt.data_ptr(), self.att_cnt.numel()
         d.keys = self.keys.data_ptr()

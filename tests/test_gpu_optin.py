@@ -19,6 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     {"TF_LN_COOP": "1"},    # cluster-cooperative LN in the QKV / FFN1 split-K GEMMs
     {"TF_ROWLN": "1"},      # residual GEMMs as one whole-row cluster with the LayerNorm in the epilogue
     {"TF_L2PF": "0"},       # no next-layer L2 prefetch
+    {"TF_LN_TAIL": "1"},    # LayerNorm of a row by the CTA that completes it in the residual GEMM
     {"TF_PF_PERSIST": "1"},  # persistent prefill GEMM with two TMEM accumulators
     {"TF_ATTN_WO": "1"},    # output projection inside the attention + head-sum/residual/LN row kernel
 ])
