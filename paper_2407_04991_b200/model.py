@@ -495,6 +495,10 @@ def greedy_decode(model: Model, prompt, max_new_tokens: int, use_cache: bool = T
 def _left_pad(c: ModelConfig, prompts):
     lens = [len(p) for p in prompts]
     B, L = len(prompts), max(lens)
+    if min(lens) == L:  # equal lengths: no padding, one array conversion
+        ids = np.asarray(prompts, dtype=np.int32).reshape(B, L)
+        pos = np.broadcast_to(np.arange(L, dtype=np.int32), (B, L)).copy()
+        return ids, pos, np.zeros(B, np.int32), lens
     pads = np.asarray([L - n for n in lens], np.int32)
     ids = np.full((B, L), c.pad_token, np.int32)
     pos = np.zeros((B, L), np.int32)
