@@ -78,3 +78,35 @@ def test_pruned_model_and_device_remap(cuda_device, pair):
     full = P.forward_full(m, prompts_old[0]).array[-1]
     pr = P.forward_full(pm, prompts_new[0]).array[-1]
     assert np.array_equal(full[list(kept)], pr)
+
+
+def test_ragged_batch_tiles_match_oracle(cuda_device, pair):
+    """Batch 100: two 64-row decode tiles, the second partial (rows past the
+    batch masked in every epilogue), with ragged prompts."""
+    m, w, oc = pair
+    s = O.Stream(O.derive_seed(4, "tiles"))
+    lens = (s.randint(100, 40) + 8).tolist()
+    ids = (s.randint(sum(lens), oc.vocab_size - 3) + 3).tolist()
+    prompts, k = [], 0
+    for n in lens:
+        prompts.append(ids[k:k + n])
+        k += n
+    got = P.batched_greedy_decode(m, prompts, 5)
+    rec = []
+    ref = O.batched_greedy_decode(w, oc, prompts, 5, step_logits=rec)
+    check_margin_gated(got, ref, rec, prompts)
+
+
+def test_generation_up_to_max_position(cuda_device, pair):
+    """prompt + max_new_tokens == max_position: the last generated token sits in
+    the last position / cache slot."""
+    m, w, oc = pair
+    P_max = oc.max_position
+    s = O.Stream(O.derive_seed(5, "maxpos"))
+    prompts = [(s.randint(P_max - 4, oc.vocab_size - 3) + 3).tolist(), [7, 8, 9]]
+    got = P.batched_greedy_decode(m, prompts, 4)
+    rec = []
+    ref = O.batched_greedy_decode(w, oc, prompts, 4, step_logits=rec)
+    check_margin_gated(got, ref, rec, prompts)
+    with pytest.raises(P.PositionError):
+        P.batched_greedy_decode(m, prompts, 5)
