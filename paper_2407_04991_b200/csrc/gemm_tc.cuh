@@ -430,6 +430,32 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
     }
     return;
   }
+  if constexpr (MODE == EPI_QKV) {
+    // the thread's chunk column is fixed (NT is a multiple of the chunks per
+    // row), so the q/k/v routing of its 8 features is computed once
+    if (NT % cpr == 0 && (p.D % 8) == 0 && (p.ldq % 8) == 0) {
+      const int ch = et % cpr, f0 = tile_b * bn + ch * 8;
+      if (f0 + 8 > p.n_feat) return;
+      const int which = f0 / p.H, rr = f0 - which * p.H;
+      const int head = rr / p.D, d = rr - head * p.D;
+      const int qb = *p.qbase_dev;
+      __half* const cache = which == 1 ? p.kc : p.vc;
+      for (int r = et / cpr; r < kTileA; r += NT / cpr) {
+        const int t = tile_a * kTileA + r;
+        if (t >= p.m_tok) break;
+        const uint4 val = *reinterpret_cast<const uint4*>(stage + (size_t)r * pitch + ch * 16);
+        __half* dst;
+        if (which == 0) {
+          dst = p.q_out + (size_t)t * p.ldq + rr;
+        } else {
+          const int b = t / p.T, tt = t - b * p.T;
+          dst = cache + (((size_t)b * p.NH + head) * p.cap + qb + tt) * p.D + d;
+        }
+        *reinterpret_cast<uint4*>(dst) = val;
+      }
+      return;
+    }
+  }
   for (int idx = et; idx < kTileA * cpr; idx += NT) {
     const int r = idx / cpr, ch = idx - r * cpr;
     const int t = tile_a * kTileA + r;
