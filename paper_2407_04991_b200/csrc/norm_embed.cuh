@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256) layernorm_vec_kernel(const LnArgs a) {
   pdl_wait();
   if (threadIdx.x == 0) tr.mark(a.trace, 1);
   if (!a.early_trigger) pdl_trigger();
-  const int row = blockIdx.x * 8 + warp;
+  const int row = blockIdx.x * (blockDim.x >> 5) + warp;
   if (row < a.n_rows) {
     const __half* xr = a.x + ((size_t)row * a.src_stride + a.src_off) * a.ldx;
     uint4 raw[NC];

@@ -737,15 +737,21 @@ void run_ln(const LnArgs& a0, cudaStream_t st, bool pdl) {
   a.early_trigger = early ? 1 : 0;
   a.trace = trace_next("layernorm");
   const dim3 grid((a.n_rows + 7) / 8);
+  static const int ln_rpc = [] {  // TF_LN_RPC: rows (warps) per CTA of the vector LN kernel (A/B)
+    const char* e = getenv("TF_LN_RPC");
+    const int v = e ? atoi(e) : 8;
+    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 8;
+  }();
+  const dim3 vgrid((a.n_rows + ln_rpc - 1) / ln_rpc), vblock(32 * ln_rpc);
   if (vec_ok(a.H, a.ldx, a.ldh) && a.H <= 2048) {
     const int nc = (a.H / 8 + 31) / 32;
     switch (nc) {
-      case 1: launch_mc(layernorm_vec_kernel<1>, grid, dim3(256), 0, st, pdl, a); return;
-      case 2: launch_mc(layernorm_vec_kernel<2>, grid, dim3(256), 0, st, pdl, a); return;
-      case 3: launch_mc(layernorm_vec_kernel<3>, grid, dim3(256), 0, st, pdl, a); return;
-      case 4: launch_mc(layernorm_vec_kernel<4>, grid, dim3(256), 0, st, pdl, a); return;
-      case 6: launch_mc(layernorm_vec_kernel<6>, grid, dim3(256), 0, st, pdl, a); return;
-      case 8: launch_mc(layernorm_vec_kernel<8>, grid, dim3(256), 0, st, pdl, a); return;
+      case 1: launch_mc(layernorm_vec_kernel<1>, vgrid, vblock, 0, st, pdl, a); return;
+      case 2: launch_mc(layernorm_vec_kernel<2>, vgrid, vblock, 0, st, pdl, a); return;
+      case 3: launch_mc(layernorm_vec_kernel<3>, vgrid, vblock, 0, st, pdl, a); return;
+      case 4: launch_mc(layernorm_vec_kernel<4>, vgrid, vblock, 0, st, pdl, a); return;
+      case 6: launch_mc(layernorm_vec_kernel<6>, vgrid, vblock, 0, st, pdl, a); return;
+      case 8: launch_mc(layernorm_vec_kernel<8>, vgrid, vblock, 0, st, pdl, a); return;
       default: break;
     }
   }
