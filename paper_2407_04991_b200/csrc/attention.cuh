@@ -685,6 +685,231 @@ __global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const 
   }
 }
 
+// ------------------------------------------------------------------ decode, beam groups
+// head_dim 64, beam search (indir != null). One CTA (256 threads) per (head,
+// request) scores all R = beam rows of the request over the whole window. The
+// beams of a request share their prompt: a 64-slot chunk whose slots resolve
+// to the same source row for every beam (checked on the indirection table, so
+// shared generated ancestry counts too) is staged in shared memory ONCE and
+// every K row read from it serves R dot products; other chunks are staged per
+// beam. Chunks are staged in 16 KB planes (K rotated | V, as in
+// attn_decode_pf_kernel) from a pool of `planes`; windows needing more planes
+// run in several batches. Per (beam, chunk) the arithmetic -- scores, chunk
+// softmax, PV with one warp, and the merge in chunk order -- is that of
+// attn_decode_pf_kernel<.., 128>, so the output is bitwise the same as the
+// per-row kernel's (the oracle comparison and batch invariance carry over).
+constexpr int kBmThreads = 256, kBmMaxCh = 8;  // window <= 512 slots
+__host__ __device__ inline size_t attn_beam_aux_bytes(int R) {
+  // s_ind [R][512] int | sc [R][8][64] f32 | part [R][8][66] f32 | q [R][64] f32
+  return (size_t)R * (kBmMaxCh * 64 * 4 + kBmMaxCh * 64 * 4 + kBmMaxCh * 66 * 4 + 64 * 4);
+}
+__host__ __device__ inline size_t attn_beam_smem_bytes(int R, int planes) {
+  return (size_t)planes * kPfChunkBytes + attn_beam_aux_bytes(R);
+}
+
+__global__ void __launch_bounds__(kBmThreads, 1) attn_decode_beam_kernel(const AttnArgs a, int planes) {
+  extern __shared__ __align__(128) uint8_t bm_smem[];
+  __shared__ int s_sh[kBmMaxCh], s_pl[kBmMaxCh], s_bend[kBmMaxCh + 1], s_nb;
+  constexpr int D = 64;
+  TF_TRACE_INIT(tr);
+  if (threadIdx.x == 0) tr.mark(a.trace, 0);
+  const int R = a.beam;
+  __half* kvs = reinterpret_cast<__half*>(bm_smem);
+  int* s_ind = reinterpret_cast<int*>(bm_smem + (size_t)planes * kPfChunkBytes);  // [R][512]
+  float* sc = reinterpret_cast<float*>(s_ind + (size_t)R * kBmMaxCh * 64);      // [R][8][64]
+  float* part = sc + (size_t)R * kBmMaxCh * 64;                                  // [R][8][66]
+  float* qs = part + (size_t)R * kBmMaxCh * 66;                                  // [R][64]
+  const int h = blockIdx.y, rq = blockIdx.z, beam0 = rq * R;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qbase = *a.qbase_dev;
+  const int lo = a.start[beam0], hi = qbase;  // the beams of a request share the left pad
+  const int n = hi - lo + 1;
+  const int nch = n > 0 ? (n + 63) / 64 : 0;
+  const size_t row_stride = (size_t)a.NH * a.cap * D, head_stride = (size_t)a.cap * D;
+  // ---- before the wait: indirection rows (slots < hi), sharing per chunk, plan
+  for (int i = tid; i < R * nch * 64; i += kBmThreads) {
+    const int r = i / (nch * 64), k = i % (nch * 64), s = lo + k;
+    s_ind[r * kBmMaxCh * 64 + k] = s < hi ? a.indir[(size_t)(beam0 + r) * a.cap + s] : 0;
+  }
+  __syncthreads();
+  if (warp < nch) {
+    bool same = true;
+    for (int k = warp * 64 + lane; k < warp * 64 + 64; k += 32) {
+      const int s = lo + k;
+      if (s == hi) same = false;  // the newest slot: each beam's own row
+      for (int r = 1; r < R && s < hi; ++r) same = same && s_ind[r * kBmMaxCh * 64 + k] == s_ind[k];
+    }
+    same = __all_sync(0xffffffffu, same);
+    if (lane == 0) s_sh[warp] = same;
+  }
+  __syncthreads();
+  if (tid == 0) {  // batches of consecutive chunks whose planes fit the pool
+    int nb = 0, used = 0;
+    s_bend[0] = 0;
+    for (int c = 0; c < nch; ++c) {
+      const int need = s_sh[c] ? 1 : R;
+      if (used + need > planes) {
+        s_bend[++nb] = c;
+        used = 0;
+      }
+      s_pl[c] = used;
+      used += need;
+    }
+    s_bend[++nb] = nch;
+    s_nb = nb;
+  }
+  __syncthreads();
+  const int nbatch = nch > 0 ? s_nb : 0;
+  // copies of chunks [c0, c1): plane p of chunk c holds beam p's rows (or all
+  // beams' when shared); slot hi only after the wait (after_wait)
+  auto stage = [&](int c0, int c1, bool after_wait) {
+    for (int c = c0; c < c1; ++c) {
+      const int np = s_sh[c] ? 1 : R;
+      for (int seg = tid; seg < np * 64 * 8; seg += kBmThreads) {
+        const int p = seg >> 9, j = (seg >> 3) & 63, prt = seg & 7;
+        const int k = c * 64 + j, slot = lo + k;
+        if (slot == hi && !after_wait) continue;
+        const bool ok = slot <= hi;
+        const int src = slot == hi ? beam0 + a.indir[(size_t)(beam0 + p) * a.cap + hi]
+                                   : beam0 + s_ind[p * kBmMaxCh * 64 + k];
+        const size_t off = ok ? (size_t)src * row_stride + (size_t)h * head_stride + (size_t)slot * D + prt * 8 : 0;
+        __half* pb = kvs + (size_t)(s_pl[c] + p) * (2 * 64 * 64);
+        cp_async16(smem_u32(pb + (size_t)j * 64 + ((prt + j) & 7) * 8), a.kc + off, ok);
+        cp_async16(smem_u32(pb + (size_t)(64 + j) * 64 + prt * 8), a.vc + off, ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (threadIdx.x == 0) tr.mark(a.trace, 6);
+  if (nbatch > 0) stage(0, s_bend[1], false);
+  if (tid == 32) l2_prefetch_share(a.l2pf, a.l2pf_bytes);
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) tr.mark(a.trace, 1);
+  if (n <= 0) {
+    for (int i = tid; i < R * D; i += kBmThreads)
+      a.out[(size_t)(beam0 + i / D) * a.ldo + (size_t)h * D + i % D] = __float2half_rn(0.0f);
+    return;
+  }
+  if (threadIdx.x == 0) tr.mark(a.trace, 3);
+  for (int i = tid; i < R * D; i += kBmThreads)
+    qs[i] = __half2float(a.q[(size_t)(beam0 + i / D) * a.ldq + (size_t)h * D + i % D]);
+  // the newest slot of batch 0 (if there): after the wait
+  {
+    const int cl = (hi - lo) / 64;
+    if (cl < s_bend[1]) {
+      const int j = (hi - lo) % 64;
+      for (int i = tid; i < R * 16; i += kBmThreads) {
+        const int p = i >> 4, kv = (i >> 3) & 1, prt = i & 7;
+        const int src = beam0 + a.indir[(size_t)(beam0 + p) * a.cap + hi];
+        const size_t off = (size_t)src * row_stride + (size_t)h * head_stride + (size_t)hi * D + prt * 8;
+        __half* pb = kvs + (size_t)(s_pl[cl] + p) * (2 * 64 * 64);
+        __half* dst = pb + (size_t)(kv * 64 + j) * 64 + (kv ? prt : ((prt + j) & 7)) * 8;
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>((kv ? a.vc : a.kc) + off);
+      }
+    }
+  }
+  __syncthreads();  // qs complete
+  // QK^T: thread -> fixed beam r = tid % R (q in registers), keys strided
+  const int RT = (kBmThreads / R) * R;  // threads with a beam
+  const int my_r = tid % R;
+  float qr[64];
+#pragma unroll
+  for (int e = 0; e < 64; e += 4) {
+    const float4 q4 = *reinterpret_cast<const float4*>(qs + (tid < RT ? my_r : 0) * 64 + e);
+    qr[e] = q4.x;
+    qr[e + 1] = q4.y;
+    qr[e + 2] = q4.z;
+    qr[e + 3] = q4.w;
+  }
+  for (int bt = 0; bt < nbatch; ++bt) {
+    const int c0 = s_bend[bt], c1 = s_bend[bt + 1];
+    if (bt > 0) stage(c0, c1, true);
+    cp_async_commit_wait_all();
+    __syncthreads();
+    if (threadIdx.x == 0 && bt == 0) tr.mark(a.trace, 2);
+    const int nk = min((c1 - c0) * 64, n - c0 * 64);
+    if (tid < RT) {
+      for (int key = tid / R; key < nk; key += kBmThreads / R) {
+        const int c = c0 + (key >> 6), j = key & 63;
+        const __half* kr = kvs + (size_t)(s_pl[c] + (s_sh[c] ? 0 : my_r)) * (2 * 64 * 64) + (size_t)j * 64;
+        uint4 raw[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) raw[g] = *reinterpret_cast<const uint4*>(kr + ((g + j) & 7) * 8);
+        float ps[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          float kf[8];
+          unpack8(raw[g], kf);
+          float acc = __fmul_rn(qr[8 * g], kf[0]);
+#pragma unroll
+          for (int e = 1; e < 8; ++e) acc = __fadd_rn(acc, __fmul_rn(qr[8 * g + e], kf[e]));
+          ps[g] = acc;
+        }
+        const float d = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
+                                  __fadd_rn(__fadd_rn(ps[4], ps[5]), __fadd_rn(ps[6], ps[7])));
+        sc[((size_t)my_r * kBmMaxCh + c) * 64 + j] = __fmul_rn(d, a.scale);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && bt == 0) tr.mark(a.trace, 4);
+    // one warp per (beam, chunk): chunk softmax + PV (attn_decode_pf_kernel, WPC 1)
+    for (int u = warp; u < R * (c1 - c0); u += kBmThreads / 32) {
+      const int r = u % R, c = c0 + u / R;
+      const int cnt_keys = min(64, n - c * 64);
+      float* sci = sc + ((size_t)r * kBmMaxCh + c) * 64;
+      const float s0 = lane < cnt_keys ? sci[lane] : -INFINITY;
+      const float s1 = lane + 32 < cnt_keys ? sci[lane + 32] : -INFINITY;
+      const float m = warp_max(fmaxf(s0, s1));
+      const float e0 = lane < cnt_keys ? expf(__fsub_rn(s0, m)) : 0.0f;
+      const float e1 = lane + 32 < cnt_keys ? expf(__fsub_rn(s1, m)) : 0.0f;
+      const float z = warp_sum(__fadd_rn(e0, e1));
+      sci[lane] = e0;  // this warp alone reads / writes this row
+      sci[lane + 32] = e1;
+      __syncwarp();
+      const __half* Vs = kvs + (size_t)(s_pl[c] + (s_sh[c] ? 0 : r)) * (2 * 64 * 64) + 64 * 64;
+      float o0[4] = {0.f, 0.f, 0.f, 0.f}, o1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int j = 0; j < 64; j += 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 v = __half22float2(*reinterpret_cast<const __half2*>(Vs + (j + q) * 64 + 2 * lane));
+          const float w = sci[j + q];
+          o0[q] = __fadd_rn(o0[q], __fmul_rn(w, v.x));
+          o1[q] = __fadd_rn(o1[q], __fmul_rn(w, v.y));
+        }
+      }
+      float* dst = part + ((size_t)r * kBmMaxCh + c) * 66;
+      dst[2 + 2 * lane] = __fadd_rn(__fadd_rn(o0[0], o0[1]), __fadd_rn(o0[2], o0[3]));
+      dst[3 + 2 * lane] = __fadd_rn(__fadd_rn(o1[0], o1[1]), __fadd_rn(o1[2], o1[3]));
+      if (lane == 0) {
+        dst[0] = m;
+        dst[1] = z;
+      }
+    }
+    __syncthreads();  // planes free for the next batch
+  }
+  if (threadIdx.x == 0) tr.mark(a.trace, 5);
+  // merge in chunk order per (beam, dim)
+  for (int i = tid; i < R * D; i += kBmThreads) {
+    const int r = i / D, d = i % D;
+    const float* P = part + (size_t)r * kBmMaxCh * 66;
+    float M = -INFINITY;
+    for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, P[(size_t)cc * 66]);
+    float Z = 0.0f, O = 0.0f;
+    for (int cc = 0; cc < nch; ++cc) {
+      const float f = expf(__fsub_rn(P[(size_t)cc * 66], M));
+      Z = __fadd_rn(Z, __fmul_rn(P[(size_t)cc * 66 + 1], f));
+      O = __fadd_rn(O, __fmul_rn(P[(size_t)cc * 66 + 2 + d], f));
+    }
+    a.out[(size_t)(beam0 + r) * a.ldo + (size_t)h * D + d] = f16_sat(__fdiv_rn(O, Z));
+  }
+  if (threadIdx.x == 0) {
+    tr.mark(a.trace, 7);
+    tr.flush(a.trace);
+  }
+}
+
 // ------------------------------------------------------------------ prefill, tensor cores
 // head_dim 64. One CTA = 64 query rows of one (head, sequence), 4 warps x 16 rows.
 // Key/value tiles of 64 slots (aligned to the row's first valid slot `start`, so

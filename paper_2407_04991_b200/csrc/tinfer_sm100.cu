@@ -785,8 +785,28 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
     const char* e = getenv("TF_ATTN_PF");
     return e ? atoi(e) : 1;
   }();
-  if (a.T == 1 && a.D == 64 && a.ws && a.cnt && a.max_chunks >= (a.cap + kSplitKeys - 1) / kSplitKeys &&
-      pf_mode) {
+  static const int beam_mode = [] {  // TF_ATTN_BEAM=0: beams scored by per-row CTAs (A/B)
+    const char* e = getenv("TF_ATTN_BEAM");
+    return e ? atoi(e) : 1;
+  }();
+  if (a.T == 1 && a.D == 64 && a.indir && a.beam >= 2 && a.B % a.beam == 0 && a.cap <= kBmMaxCh * 64 &&
+      a.wo_t == nullptr && beam_mode) {
+    // one CTA per (head, request): prompt chunks staged once for all beams
+    const int planes = (int)std::min<size_t>(12, (kMaxSmem - 2048 - attn_beam_aux_bytes(a.beam)) / kPfChunkBytes);
+    TF_REQUIRE(planes >= a.beam, TF_ERR_UNSUPPORTED, "beam attention: plane pool smaller than the beam");
+    const size_t smem = attn_beam_smem_bytes(a.beam, planes);
+    static bool attr = false;
+    if (!attr) {
+      TF_CHECK_CUDA(cudaFuncSetAttribute(attn_decode_beam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kMaxSmem - 2048)));  // + the kernel's static smem
+      set_max_carveout(attn_decode_beam_kernel);
+      attr = true;
+    }
+    AttnArgs t = a;
+    t.trace = trace_next("attn_decode_beam");
+    launch(attn_decode_beam_kernel, dim3(1, a.NH, a.B / a.beam), dim3(kBmThreads), smem, st, pdl, t, planes);
+  } else if (a.T == 1 && a.D == 64 && a.ws && a.cnt && a.max_chunks >= (a.cap + kSplitKeys - 1) / kSplitKeys &&
+             pf_mode) {
     // chunks per CTA: the whole window when it is <= 4 chunks (local merge),
     // else groups of <= 4 (64 KB of K/V each) merged through the workspace
     static const int gmax = [] {  // TF_ATTN_G: max 64-slot chunks per CTA (A/B), <= kPfMaxG

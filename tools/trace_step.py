@@ -14,6 +14,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("TF_TRACE", "1")
 
+import warnings  # noqa: E402
+
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
@@ -32,22 +34,34 @@ def main():
     run = bench.Runner(model, prompts, w)
     lib = N.lib()
     run.stage()
-    run.sess.forward(run.ids.shape[1], N.FWD_ARGMAX)
-    run.sess.decode(8, use_graph=False)
+    if run.beam:  # beam: prefill + select + warm steps; each traced step = T=1 forward + select
+        br, s = run.beam, run.sess
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        s.forward(br.L, N.FWD_LOGITS_LAST)
+        N.check(lib.tf_beam_select(s.handle, C.byref(br.desc), st), "tf_beam_select")
+        N.check(lib.tf_beam_decode(s.handle, C.byref(br.desc), 8, 0, st), "tf_beam_decode")
+
+        def one():
+            N.check(lib.tf_beam_decode(s.handle, C.byref(br.desc), 1, 0, st), "tf_beam_decode")
+    else:
+        run.sess.forward(run.ids.shape[1], N.FWD_ARGMAX)
+        run.sess.decode(8, use_graph=False)
+
+        def one():
+            run.sess.decode(1, use_graph=False)
     torch.cuda.synchronize()
     reps = int(os.environ.get("TRACE_REPS", "10"))
     agg = {}
     step_us = []
     for rep in range(reps):
         lib.tf_debug_trace(1, None, 0, None)
-        run.sess.decode(1, use_graph=False)
+        one()
         torch.cuda.synchronize()
         raw = np.zeros((256, 2048, 8), dtype=np.uint64)
         names = (C.c_char_p * 256)()
         n = lib.tf_debug_trace(0, raw.ctypes.data, 256, names)
         r = raw[:n].astype(np.float64)
         r[r == 0] = np.nan
-        import warnings
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             mx = np.nanmax(r[:, :, 7], axis=1)
@@ -61,8 +75,25 @@ def main():
         print(f"  {k:<18} mean incr {np.nanmean(v):6.2f} us  x{len(v) // reps:3d}/step = {np.nansum(v) / reps:7.1f} us")
     r = raw[:n].astype(np.float64)
     r[r == 0] = np.nan
+    if os.environ.get("PER_CTA"):  # per-CTA phase durations of the attention launches
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            for i in range(n):
+                if not names[i].decode().startswith("attn_decode"):
+                    continue
+                c = r[i]
+                c = c[~np.isnan(c[:, 0])]
+                ph = lambda x, y: np.nanmedian(c[:, y] - c[:, x]) / 1e3  # noqa: E731
+                life = (c[:, 7] - c[:, 0]) / 1e3
+                print(f"attn #{i}: ctas traced {len(c)} span {(np.nanmax(c[:, 7]) - np.nanmin(c[:, 0])) / 1e3:.1f} us; "
+                      f"median life {np.nanmedian(life):.2f} (p90 {np.nanpercentile(life, 90):.2f}); "
+                      f"0-1 {ph(0, 1):.2f} 1-2 {ph(1, 2):.2f} 2-4 {ph(2, 4):.2f} 4-5 {ph(4, 5):.2f} 5-7 {ph(5, 7):.2f}; "
+                      f"QK cycles median {np.nanmedian(c[:, 6]):.0f}; 0-6 {ph(0, 6):.2f} 1-3 {ph(1, 3):.2f} 3-2 {ph(3, 2):.2f}")
+                st = np.sort(c[:, 0])
+                print(f"   entry times rel: p10 {(st[len(st) // 10] - st[0]) / 1e3:.1f} p50 {(st[len(st) // 2] - st[0]) / 1e3:.1f} "
+                      f"p90 {(st[9 * len(st) // 10] - st[0]) / 1e3:.1f} us")
+                break
     t = np.full((n, NP), np.nan)
-    import warnings
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         t[:, :8] = np.nanmax(r, axis=1)
