@@ -910,6 +910,234 @@ __global__ void __launch_bounds__(kBmThreads, 1) attn_decode_beam_kernel(const A
   }
 }
 
+// Ring-pipelined form of attn_decode_beam_kernel: chunks are processed one at a
+// time in window order, their planes taken from a ring of `planes` (one
+// cp.async group per chunk), so the copies of later chunks land while earlier
+// ones are scored, and the smaller pool lets MINB CTAs share an SM (one CTA's
+// copies overlap another's arithmetic). Same arithmetic, same result.
+__host__ __device__ inline size_t attn_beam_ring_aux_bytes(int R) {
+  // s_ind [R][512] u8 | sc [R][64] f32 | part [R][8][66] f32 | q [R][64] f32
+  return (size_t)R * (kBmMaxCh * 64 + 64 * 4 + kBmMaxCh * 66 * 4 + 64 * 4);
+}
+__device__ __forceinline__ void cp_async_wait_upto(int n) {  // allow <= n pending groups
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kBmThreads, MINB) attn_decode_beam_ring_kernel(const AttnArgs a, int planes) {
+  extern __shared__ __align__(128) uint8_t bm_smem[];
+  __shared__ int s_sh[kBmMaxCh];
+  constexpr int D = 64;
+  TF_TRACE_INIT(tr);
+  if (threadIdx.x == 0) tr.mark(a.trace, 0);
+  const int R = a.beam;
+  __half* kvs = reinterpret_cast<__half*>(bm_smem);
+  float* part = reinterpret_cast<float*>(bm_smem + (size_t)planes * kPfChunkBytes);  // [R][8][66]
+  float* qs = part + (size_t)R * kBmMaxCh * 66;                                        // [R][64]
+  float* sc = qs + (size_t)R * 64;                                                     // [R][64]
+  uint8_t* s_ind = reinterpret_cast<uint8_t*>(sc + (size_t)R * 64);                   // [R][512]
+  const int h = blockIdx.y, rq = blockIdx.z, beam0 = rq * R;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qbase = *a.qbase_dev;
+  const int lo = a.start[beam0], hi = qbase;  // the beams of a request share the left pad
+  const int n = hi - lo + 1;
+  const int nch = n > 0 ? (n + 63) / 64 : 0;
+  const size_t row_stride = (size_t)a.NH * a.cap * D, head_stride = (size_t)a.cap * D;
+  // ---- before the wait: indirection rows (slots < hi), sharing per chunk
+  for (int i = tid; i < R * nch * 64; i += kBmThreads) {
+    const int r = i / (nch * 64), k = i - r * (nch * 64), s = lo + k;
+    s_ind[r * kBmMaxCh * 64 + k] = (uint8_t)(s < hi ? a.indir[(size_t)(beam0 + r) * a.cap + s] : 0);
+  }
+  __syncthreads();
+  if (warp < nch) {
+    bool same = true;
+    for (int k = warp * 64 + lane; k < warp * 64 + 64; k += 32) {
+      const int s = lo + k;
+      if (s == hi) same = false;  // the newest slot: each beam's own row
+      for (int r = 1; r < R && s < hi; ++r) same = same && s_ind[r * kBmMaxCh * 64 + k] == s_ind[k];
+    }
+    same = __all_sync(0xffffffffu, same);
+    if (lane == 0) s_sh[warp] = same;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) tr.mark(a.trace, 6);
+  // ring state (uniform across the CTA): chunk c's planes start at pl_of(c)
+  int next = 0, used = 0, head = 0;
+  int pl[kBmMaxCh];
+#pragma unroll
+  for (int c = 0; c < kBmMaxCh; ++c) pl[c] = 0;
+  const int cl = n > 0 ? (hi - lo) / 64 : -1;  // chunk holding the newest slot
+  bool newest_pending = false;                 // its chunk was staged before the wait
+  auto issue = [&](bool after_wait) {
+    while (next < nch) {
+      const int np = s_sh[next] ? 1 : R;
+      if (used + np > planes) break;
+      const int c = next;
+#pragma unroll
+      for (int cc = 0; cc < kBmMaxCh; ++cc)
+        if (cc == c) pl[cc] = head;
+      for (int seg = tid; seg < np * 64 * 8; seg += kBmThreads) {
+        const int p = seg >> 9, j = (seg >> 3) & 63, prt = seg & 7;
+        const int k = c * 64 + j, slot = lo + k;
+        if (slot == hi && !after_wait) continue;
+        const bool ok = slot <= hi;
+        const int src = slot == hi ? beam0 + a.indir[(size_t)(beam0 + p) * a.cap + hi]
+                                   : beam0 + s_ind[p * kBmMaxCh * 64 + k];
+        const size_t off = ok ? (size_t)src * row_stride + (size_t)h * head_stride + (size_t)slot * D + prt * 8 : 0;
+        int q = head + p;
+        if (q >= planes) q -= planes;
+        __half* pb = kvs + (size_t)q * (2 * 64 * 64);
+        cp_async16(smem_u32(pb + (size_t)j * 64 + ((prt + j) & 7) * 8), a.kc + off, ok);
+        cp_async16(smem_u32(pb + (size_t)(64 + j) * 64 + prt * 8), a.vc + off, ok);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (c == cl && !after_wait) newest_pending = true;
+      head += np;
+      if (head >= planes) head -= planes;
+      used += np;
+      ++next;
+    }
+  };
+  issue(false);
+  if (tid == 32) l2_prefetch_share(a.l2pf, a.l2pf_bytes);
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) tr.mark(a.trace, 1);
+  if (n <= 0) {
+    for (int i = tid; i < R * D; i += kBmThreads)
+      a.out[(size_t)(beam0 + i / D) * a.ldo + (size_t)h * D + i % D] = __float2half_rn(0.0f);
+    return;
+  }
+  for (int i = tid; i < R * D; i += kBmThreads)
+    qs[i] = __half2float(a.q[(size_t)(beam0 + i / D) * a.ldq + (size_t)h * D + i % D]);
+  if (newest_pending) {  // the newest slot of a chunk staged before the wait
+    const int j = (hi - lo) % 64;
+    int plc = 0;
+#pragma unroll
+    for (int cc = 0; cc < kBmMaxCh; ++cc)
+      if (cc == cl) plc = pl[cc];
+    for (int i = tid; i < R * 16; i += kBmThreads) {
+      const int p = i >> 4, kv = (i >> 3) & 1, prt = i & 7;
+      const int src = beam0 + a.indir[(size_t)(beam0 + p) * a.cap + hi];
+      const size_t off = (size_t)src * row_stride + (size_t)h * head_stride + (size_t)hi * D + prt * 8;
+      int q = plc + p;
+      if (q >= planes) q -= planes;
+      __half* dst = kvs + (size_t)q * (2 * 64 * 64) + (size_t)(kv * 64 + j) * 64 + (kv ? prt : ((prt + j) & 7)) * 8;
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>((kv ? a.vc : a.kc) + off);
+    }
+  }
+  __syncthreads();  // qs complete
+  const int RT = (kBmThreads / R) * R;  // threads with a beam (QK^T: fixed beam, q in registers)
+  const int my_r = tid % R;
+  float qr[64];
+#pragma unroll
+  for (int e = 0; e < 64; e += 4) {
+    const float4 q4 = *reinterpret_cast<const float4*>(qs + (tid < RT ? my_r : 0) * 64 + e);
+    qr[e] = q4.x;
+    qr[e + 1] = q4.y;
+    qr[e + 2] = q4.z;
+    qr[e + 3] = q4.w;
+  }
+  for (int c = 0; c < nch; ++c) {
+    issue(true);  // refill the ring (no-op when full or done)
+    cp_async_wait_upto(next - c - 1);
+    __syncthreads();
+    int plc = 0;
+#pragma unroll
+    for (int cc = 0; cc < kBmMaxCh; ++cc)
+      if (cc == c) plc = pl[cc];
+    const bool shc = s_sh[c];
+    const int nk = min(64, n - c * 64);
+    if (tid < RT) {
+      for (int j = tid / R; j < nk; j += kBmThreads / R) {
+        int q = plc + (shc ? 0 : my_r);
+        if (q >= planes) q -= planes;
+        const __half* kr = kvs + (size_t)q * (2 * 64 * 64) + (size_t)j * 64;
+        uint4 raw[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) raw[g] = *reinterpret_cast<const uint4*>(kr + ((g + j) & 7) * 8);
+        float ps[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          float kf[8];
+          unpack8(raw[g], kf);
+          float acc = __fmul_rn(qr[8 * g], kf[0]);
+#pragma unroll
+          for (int e = 1; e < 8; ++e) acc = __fadd_rn(acc, __fmul_rn(qr[8 * g + e], kf[e]));
+          ps[g] = acc;
+        }
+        const float d = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
+                                  __fadd_rn(__fadd_rn(ps[4], ps[5]), __fadd_rn(ps[6], ps[7])));
+        sc[my_r * 64 + j] = __fmul_rn(d, a.scale);
+      }
+    }
+    __syncthreads();
+    // one warp per beam: chunk softmax + PV (attn_decode_pf_kernel, WPC 1)
+    for (int r = warp; r < R; r += kBmThreads / 32) {
+      float* sci = sc + r * 64;
+      const float s0 = lane < nk ? sci[lane] : -INFINITY;
+      const float s1 = lane + 32 < nk ? sci[lane + 32] : -INFINITY;
+      const float m = warp_max(fmaxf(s0, s1));
+      const float e0 = lane < nk ? expf(__fsub_rn(s0, m)) : 0.0f;
+      const float e1 = lane + 32 < nk ? expf(__fsub_rn(s1, m)) : 0.0f;
+      const float z = warp_sum(__fadd_rn(e0, e1));
+      sci[lane] = e0;  // this warp alone reads / writes this row
+      sci[lane + 32] = e1;
+      __syncwarp();
+      int q = plc + (shc ? 0 : r);
+      if (q >= planes) q -= planes;
+      const __half* Vs = kvs + (size_t)q * (2 * 64 * 64) + 64 * 64;
+      float o0[4] = {0.f, 0.f, 0.f, 0.f}, o1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int j = 0; j < 64; j += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2 v = __half22float2(*reinterpret_cast<const __half2*>(Vs + (j + u) * 64 + 2 * lane));
+          const float w = sci[j + u];
+          o0[u] = __fadd_rn(o0[u], __fmul_rn(w, v.x));
+          o1[u] = __fadd_rn(o1[u], __fmul_rn(w, v.y));
+        }
+      }
+      float* dst = part + ((size_t)r * kBmMaxCh + c) * 66;
+      dst[2 + 2 * lane] = __fadd_rn(__fadd_rn(o0[0], o0[1]), __fadd_rn(o0[2], o0[3]));
+      dst[3 + 2 * lane] = __fadd_rn(__fadd_rn(o1[0], o1[1]), __fadd_rn(o1[2], o1[3]));
+      if (lane == 0) {
+        dst[0] = m;
+        dst[1] = z;
+      }
+    }
+    __syncthreads();  // chunk c's planes and the score rows are free
+    used -= shc ? 1 : R;
+  }
+  if (threadIdx.x == 0) tr.mark(a.trace, 5);
+  for (int i = tid; i < R * D; i += kBmThreads) {
+    const int r = i / D, d = i % D;
+    const float* P = part + (size_t)r * kBmMaxCh * 66;
+    float M = -INFINITY;
+    for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, P[(size_t)cc * 66]);
+    float Z = 0.0f, O = 0.0f;
+    for (int cc = 0; cc < nch; ++cc) {
+      const float f = expf(__fsub_rn(P[(size_t)cc * 66], M));
+      Z = __fadd_rn(Z, __fmul_rn(P[(size_t)cc * 66 + 1], f));
+      O = __fadd_rn(O, __fmul_rn(P[(size_t)cc * 66 + 2 + d], f));
+    }
+    a.out[(size_t)(beam0 + r) * a.ldo + (size_t)h * D + d] = f16_sat(__fdiv_rn(O, Z));
+  }
+  if (threadIdx.x == 0) {
+    tr.mark(a.trace, 7);
+    tr.flush(a.trace);
+  }
+}
+
 // ------------------------------------------------------------------ prefill, tensor cores
 // head_dim 64. One CTA = 64 query rows of one (head, sequence), 4 warps x 16 rows.
 // Key/value tiles of 64 slots (aligned to the row's first valid slot `start`, so

@@ -779,19 +779,49 @@ void launch_pf(dim3 grid, size_t smem, cudaStream_t st, bool pdl, const AttnArgs
   launch(attn_decode_pf_kernel<WO, THREADS, MINB>, grid, dim3(THREADS), smem, st, pdl, t);
 }
 
+template <int MINB>
+void launch_beam_ring(dim3 grid, size_t smem, cudaStream_t st, bool pdl, const AttnArgs& t, int planes) {
+  static bool attr = false;
+  if (!attr) {
+    TF_CHECK_CUDA(cudaFuncSetAttribute(attn_decode_beam_ring_kernel<MINB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kMaxSmem - 2048)));
+    set_max_carveout(attn_decode_beam_ring_kernel<MINB>);
+    attr = true;
+  }
+  launch(attn_decode_beam_ring_kernel<MINB>, grid, dim3(kBmThreads), smem, st, pdl, t, planes);
+}
+
 void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
   TF_REQUIRE(a.D >= 1 && a.D <= 128, TF_ERR_UNSUPPORTED, "head_dim must be in [1, 128]");
   static const int pf_mode = [] {  // TF_ATTN_PF=0 selects the split kernel (A/B diagnostics)
     const char* e = getenv("TF_ATTN_PF");
     return e ? atoi(e) : 1;
   }();
-  static const int beam_mode = [] {  // TF_ATTN_BEAM=0: beams scored by per-row CTAs (A/B)
+  static const int beam_mode = [] {  // TF_ATTN_BEAM: 0 per-row CTAs, 1 batched staging, 2 ring (A/B)
     const char* e = getenv("TF_ATTN_BEAM");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
   if (a.T == 1 && a.D == 64 && a.indir && a.beam >= 2 && a.B % a.beam == 0 && a.cap <= kBmMaxCh * 64 &&
       a.wo_t == nullptr && beam_mode) {
-    // one CTA per (head, request): prompt chunks staged once for all beams
+    // one CTA per (head, request): prompt chunks staged once for all beams.
+    // Mode 2 (default): ring-pipelined, two CTAs per SM when a 6-plane ring fits
+    if (beam_mode == 2) {
+      const int R = a.beam;
+      const size_t half = 115712 - 512;  // per-CTA share of the SM with two resident
+      const int p2 = (int)((half - attn_beam_ring_aux_bytes(R)) / kPfChunkBytes);
+      AttnArgs t = a;
+      t.trace = trace_next("attn_decode_beam");
+      const dim3 grid(1, a.NH, a.B / a.beam);
+      if (p2 >= R) {
+        const int planes = std::min(p2, 6);
+        launch_beam_ring<2>(grid, attn_beam_ring_aux_bytes(R) + (size_t)planes * kPfChunkBytes, st, pdl, t, planes);
+      } else {
+        const int planes = (int)std::min<size_t>(12, (kMaxSmem - 2048 - attn_beam_ring_aux_bytes(R)) / kPfChunkBytes);
+        TF_REQUIRE(planes >= R, TF_ERR_UNSUPPORTED, "beam attention: plane pool smaller than the beam");
+        launch_beam_ring<1>(grid, attn_beam_ring_aux_bytes(R) + (size_t)planes * kPfChunkBytes, st, pdl, t, planes);
+      }
+      return;
+    }
     const int planes = (int)std::min<size_t>(12, (kMaxSmem - 2048 - attn_beam_aux_bytes(a.beam)) / kPfChunkBytes);
     TF_REQUIRE(planes >= a.beam, TF_ERR_UNSUPPORTED, "beam attention: plane pool smaller than the beam");
     const size_t smem = attn_beam_smem_bytes(a.beam, planes);
