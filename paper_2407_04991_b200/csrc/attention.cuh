@@ -916,8 +916,8 @@ __global__ void __launch_bounds__(kBmThreads, 1) attn_decode_beam_kernel(const A
 // ones are scored, and the smaller pool lets MINB CTAs share an SM (one CTA's
 // copies overlap another's arithmetic). Same arithmetic, same result.
 __host__ __device__ inline size_t attn_beam_ring_aux_bytes(int R) {
-  // s_ind [R][512] u8 | sc [R][64] f32 | part [R][8][66] f32 | q [R][64] f32
-  return (size_t)R * (kBmMaxCh * 64 + 64 * 4 + kBmMaxCh * 66 * 4 + 64 * 4);
+  // s_ind [R][512] u8 | sc [R][128] f32 | part [R][8][66] f32 | q [R][64] f32
+  return (size_t)R * (kBmMaxCh * 64 + 128 * 4 + kBmMaxCh * 66 * 4 + 64 * 4);
 }
 __device__ __forceinline__ void cp_async_wait_upto(int n) {  // allow <= n pending groups
   switch (n) {
@@ -943,8 +943,8 @@ __global__ void __launch_bounds__(kBmThreads, MINB) attn_decode_beam_ring_kernel
   __half* kvs = reinterpret_cast<__half*>(bm_smem);
   float* part = reinterpret_cast<float*>(bm_smem + (size_t)planes * kPfChunkBytes);  // [R][8][66]
   float* qs = part + (size_t)R * kBmMaxCh * 66;                                        // [R][64]
-  float* sc = qs + (size_t)R * 64;                                                     // [R][64]
-  uint8_t* s_ind = reinterpret_cast<uint8_t*>(sc + (size_t)R * 64);                   // [R][512]
+  float* sc = qs + (size_t)R * 64;                                                     // [R][128]
+  uint8_t* s_ind = reinterpret_cast<uint8_t*>(sc + (size_t)R * 128);                  // [R][512]
   const int h = blockIdx.y, rq = blockIdx.z, beam0 = rq * R;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int qbase = *a.qbase_dev;
@@ -1047,19 +1047,25 @@ __global__ void __launch_bounds__(kBmThreads, MINB) attn_decode_beam_ring_kernel
     qr[e + 2] = q4.z;
     qr[e + 3] = q4.w;
   }
-  for (int c = 0; c < nch; ++c) {
-    issue(true);  // refill the ring (no-op when full or done)
-    cp_async_wait_upto(next - c - 1);
-    __syncthreads();
-    int plc = 0;
+  auto plane_of = [&](int cc) {
+    int v = 0;
 #pragma unroll
-    for (int cc = 0; cc < kBmMaxCh; ++cc)
-      if (cc == c) plc = pl[cc];
-    const bool shc = s_sh[c];
-    const int nk = min(64, n - c * 64);
+    for (int i = 0; i < kBmMaxCh; ++i)
+      if (i == cc) v = pl[i];
+    return v;
+  };
+  // one or two chunks per round: the second when it is already in the ring
+  // (fills the PV warps, halves the barriers per chunk)
+  for (int c = 0; c < nch;) {
+    issue(true);  // refill the ring (no-op when full or done)
+    const int k = c + 1 < next ? 2 : 1;
+    cp_async_wait_upto(next - c - k);
+    __syncthreads();
+    const int nk = min(k * 64, n - c * 64);
     if (tid < RT) {
-      for (int j = tid / R; j < nk; j += kBmThreads / R) {
-        int q = plc + (shc ? 0 : my_r);
+      for (int key = tid / R; key < nk; key += kBmThreads / R) {
+        const int cc = c + (key >> 6), j = key & 63;
+        int q = plane_of(cc) + (s_sh[cc] ? 0 : my_r);
         if (q >= planes) q -= planes;
         const __half* kr = kvs + (size_t)q * (2 * 64 * 64) + (size_t)j * 64;
         uint4 raw[8];
@@ -1077,37 +1083,39 @@ __global__ void __launch_bounds__(kBmThreads, MINB) attn_decode_beam_ring_kernel
         }
         const float d = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
                                   __fadd_rn(__fadd_rn(ps[4], ps[5]), __fadd_rn(ps[6], ps[7])));
-        sc[my_r * 64 + j] = __fmul_rn(d, a.scale);
+        sc[my_r * 128 + key] = __fmul_rn(d, a.scale);
       }
     }
     __syncthreads();
-    // one warp per beam: chunk softmax + PV (attn_decode_pf_kernel, WPC 1)
-    for (int r = warp; r < R; r += kBmThreads / 32) {
-      float* sci = sc + r * 64;
-      const float s0 = lane < nk ? sci[lane] : -INFINITY;
-      const float s1 = lane + 32 < nk ? sci[lane + 32] : -INFINITY;
+    // one warp per (beam, chunk): chunk softmax + PV (attn_decode_pf_kernel, WPC 1)
+    for (int u = warp; u < R * k; u += kBmThreads / 32) {
+      const int r = u % R, ci = u / R, cc = c + ci;
+      const int cnt = min(64, n - cc * 64);
+      float* sci = sc + r * 128 + ci * 64;
+      const float s0 = lane < cnt ? sci[lane] : -INFINITY;
+      const float s1 = lane + 32 < cnt ? sci[lane + 32] : -INFINITY;
       const float m = warp_max(fmaxf(s0, s1));
-      const float e0 = lane < nk ? expf(__fsub_rn(s0, m)) : 0.0f;
-      const float e1 = lane + 32 < nk ? expf(__fsub_rn(s1, m)) : 0.0f;
+      const float e0 = lane < cnt ? expf(__fsub_rn(s0, m)) : 0.0f;
+      const float e1 = lane + 32 < cnt ? expf(__fsub_rn(s1, m)) : 0.0f;
       const float z = warp_sum(__fadd_rn(e0, e1));
       sci[lane] = e0;  // this warp alone reads / writes this row
       sci[lane + 32] = e1;
       __syncwarp();
-      int q = plc + (shc ? 0 : r);
+      int q = plane_of(cc) + (s_sh[cc] ? 0 : r);
       if (q >= planes) q -= planes;
       const __half* Vs = kvs + (size_t)q * (2 * 64 * 64) + 64 * 64;
       float o0[4] = {0.f, 0.f, 0.f, 0.f}, o1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
       for (int j = 0; j < 64; j += 4) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float2 v = __half22float2(*reinterpret_cast<const __half2*>(Vs + (j + u) * 64 + 2 * lane));
-          const float w = sci[j + u];
-          o0[u] = __fadd_rn(o0[u], __fmul_rn(w, v.x));
-          o1[u] = __fadd_rn(o1[u], __fmul_rn(w, v.y));
+        for (int uu = 0; uu < 4; ++uu) {
+          const float2 v = __half22float2(*reinterpret_cast<const __half2*>(Vs + (j + uu) * 64 + 2 * lane));
+          const float w = sci[j + uu];
+          o0[uu] = __fadd_rn(o0[uu], __fmul_rn(w, v.x));
+          o1[uu] = __fadd_rn(o1[uu], __fmul_rn(w, v.y));
         }
       }
-      float* dst = part + ((size_t)r * kBmMaxCh + c) * 66;
+      float* dst = part + ((size_t)r * kBmMaxCh + cc) * 66;
       dst[2 + 2 * lane] = __fadd_rn(__fadd_rn(o0[0], o0[1]), __fadd_rn(o0[2], o0[3]));
       dst[3 + 2 * lane] = __fadd_rn(__fadd_rn(o1[0], o1[1]), __fadd_rn(o1[2], o1[3]));
       if (lane == 0) {
@@ -1115,8 +1123,9 @@ __global__ void __launch_bounds__(kBmThreads, MINB) attn_decode_beam_ring_kernel
         dst[1] = z;
       }
     }
-    __syncthreads();  // chunk c's planes and the score rows are free
-    used -= shc ? 1 : R;
+    __syncthreads();  // the round's planes and score rows are free
+    used -= (s_sh[c] ? 1 : R) + (k == 2 ? (s_sh[c + 1] ? 1 : R) : 0);
+    c += k;
   }
   if (threadIdx.x == 0) tr.mark(a.trace, 5);
   for (int i = tid; i < R * D; i += kBmThreads) {
