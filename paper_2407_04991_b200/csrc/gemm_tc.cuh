@@ -313,6 +313,65 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& p, int ra, int qb, con
   }
 }
 
+// Full-K swap tile (RED_ONE, thread = output feature f, TMEM columns = tokens):
+// the per-feature terms (bias, Q/K/V routing, cache slot) are loaded once per
+// thread instead of once per element -- per-element loads cannot be hoisted
+// past the stores (possible aliasing), so epi_store's form serialises a global
+// load round trip per element (C4 QKV epilogue 17 us -> ~1 us). Same math.
+template <int MODE>
+__device__ __forceinline__ void epi_swap_one(const GemmArgs& p, int f, int tok0, int bn, uint32_t trow) {
+  const bool fok = f < p.n_feat;
+  const float bf = fok ? p.bias[f] : 0.0f;
+  __half* dst = nullptr;
+  size_t stride = 0, tstride = 0;
+  int T = 1;
+  if constexpr (MODE == EPI_QKV) {
+    const int which = fok ? f / p.H : 0, r = f - which * p.H;
+    if (which == 0) {
+      dst = p.q_out + r;
+      stride = p.ldq;
+    } else {
+      const int head = r / p.D, d = r - head * p.D;
+      dst = (which == 1 ? p.kc : p.vc) + ((size_t)head * p.cap + *p.qbase_dev) * p.D + d;
+      stride = (size_t)p.NH * p.cap * p.D;
+      tstride = p.D;
+      T = p.T;
+    }
+  } else {
+    dst = p.out + f;
+    stride = p.ldo;
+  }
+  for (int c = 0; c < bn; c += 16) {
+    float v[16];
+    tmem_ld16(trow + (uint32_t)c, v);
+    float x[16];
+    if constexpr (MODE == EPI_BIAS_RESID) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int tok = tok0 + c + j;
+        x[j] = fok && tok < p.m_tok ? __half2float(p.resid[(size_t)tok * p.ldr + f]) : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int tok = tok0 + c + j;
+      if (fok && tok < p.m_tok) {
+        const float a = __fadd_rn(v[j], bf);
+        __half o;
+        if constexpr (MODE == EPI_BIAS_GELU) {
+          o = f16_sat(gelu_ref(a));
+        } else if constexpr (MODE == EPI_BIAS_RESID) {
+          o = f16_sat(__fadd_rn(x[j], q16(a)));
+        } else {
+          o = f16_sat(a);
+        }
+        const int b = T == 1 ? tok : tok / T;
+        dst[(size_t)b * stride + (size_t)(tok - b * T) * tstride] = o;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- non-swap (prefill) epilogue
 // Thread = output row, so direct stores would hit 32 rows per warp instruction.
 // Instead the tile is staged through the drained ring (row pitch padded by 16 B)
@@ -1090,9 +1149,13 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
       }
     }
   } else if constexpr (RED == RED_ONE) {
-    for (int c = 0; c < bn; c += 16) {
-      tmem_ld16(trow + (uint32_t)c, v);
-      epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, reinterpret_cast<unsigned long long*>(smem));
+    if constexpr (MODE == EPI_QKV || MODE == EPI_BIAS || MODE == EPI_BIAS_GELU || MODE == EPI_BIAS_RESID) {
+      epi_swap_one<MODE>(p, ra, tile_b * bn, bn, trow);
+    } else {
+      for (int c = 0; c < bn; c += 16) {
+        tmem_ld16(trow + (uint32_t)c, v);
+        epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, reinterpret_cast<unsigned long long*>(smem));
+      }
     }
   } else if constexpr (RED == RED_PUSH || RED == RED_PUSHLN) {
     // Split-K across the CTAs of one cluster, push form. Each CTA parks its f32
