@@ -319,7 +319,9 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& p, int ra, int qb, con
 // past the stores (possible aliasing), so epi_store's form serialises a global
 // load round trip per element (C4 QKV epilogue 17 us -> ~1 us). Same math.
 template <int MODE>
-__device__ __forceinline__ void epi_swap_one(const GemmArgs& p, int f, int tok0, int bn, uint32_t trow) {
+// 16-column chunks c0, c0 + cstep, ... (two warps per TMEM lane quadrant split them)
+__device__ __forceinline__ void epi_swap_one(const GemmArgs& p, int f, int tok0, int bn, uint32_t trow, int c0,
+                                             int cstep) {
   const bool fok = f < p.n_feat;
   const float bf = fok ? p.bias[f] : 0.0f;
   __half* dst = nullptr;
@@ -341,7 +343,7 @@ __device__ __forceinline__ void epi_swap_one(const GemmArgs& p, int f, int tok0,
     dst = p.out + f;
     stride = p.ldo;
   }
-  for (int c = 0; c < bn; c += 16) {
+  for (int c = c0; c < bn; c += cstep) {
     float v[16];
     tmem_ld16(trow + (uint32_t)c, v);
     float x[16];
@@ -964,7 +966,9 @@ enum GemmRed : int {
 // epilogue with eight warps; so does the decode push reduction (one pass over
 // the CTA's units instead of two at batch 32 with 6 or fewer splits)
 __host__ __device__ constexpr int gemm_threads(int mode, bool swap, int red, int lnv = 0) {
-  return ((!swap && red == RED_ONE && mode != EPI_LOGITS) || (swap && (red == RED_PUSH || red == RED_PUSHLN) && lnv <= 1))
+  return ((!swap && red == RED_ONE && mode != EPI_LOGITS) || (swap && (red == RED_PUSH || red == RED_PUSHLN) && lnv <= 1) ||
+          (swap && red == RED_ONE && lnv == 0 &&
+           (mode == EPI_QKV || mode == EPI_BIAS || mode == EPI_BIAS_GELU || mode == EPI_BIAS_RESID)))
              ? 256
              : 128;
 }
@@ -1150,7 +1154,10 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
     }
   } else if constexpr (RED == RED_ONE) {
     if constexpr (MODE == EPI_QKV || MODE == EPI_BIAS || MODE == EPI_BIAS_GELU || MODE == EPI_BIAS_RESID) {
-      epi_swap_one<MODE>(p, ra, tile_b * bn, bn, trow);
+      constexpr int NT = gemm_threads(MODE, SWAP, RED, LNV);
+      const uint32_t tq = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+      epi_swap_one<MODE>(p, tile_a * kTileA + (warp & 3) * 32 + lane, tile_b * bn, bn, tq, NT == 256 ? (warp >> 2) * 16 : 0,
+                         NT == 256 ? 32 : 16);
     } else {
       for (int c = 0; c < bn; c += 16) {
         tmem_ld16(trow + (uint32_t)c, v);
