@@ -55,11 +55,21 @@ __device__ __forceinline__ void topk_insert(Cand (&t)[kMaxBeam], int K, Cand c) 
   t[j] = c;
 }
 
-// blockDim = 256; dynamic smem = K * cap ints (indirection staging)
-__global__ void __launch_bounds__(256) beam_select_kernel(const BeamArgs a) {
+__device__ __forceinline__ Cand cand_shfl_best(Cand c) {  // warp arg-best (total order: any tree)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const Cand x{__shfl_xor_sync(0xffffffffu, c.v, o), __shfl_xor_sync(0xffffffffu, c.i, o)};
+    if (cand_better(x, c)) c = x;
+  }
+  return c;
+}
+
+// blockDim = kSelThreads; dynamic smem = K * cap ints (indirection staging)
+constexpr int kSelThreads = 1024, kSelWarps = kSelThreads / 32;
+__global__ void __launch_bounds__(kSelThreads) beam_select_kernel(const BeamArgs a) {
   pdl_wait();
-  __shared__ float s_max[kMaxBeam], s_lz[kMaxBeam], s_red[8];
-  __shared__ Cand s_cand[256];
+  __shared__ float s_max[kMaxBeam], s_lz[kMaxBeam], s_red[kSelWarps];
+  __shared__ Cand s_cand[kSelWarps];
   __shared__ int s_parent[kMaxBeam], s_tok[kMaxBeam];
   __shared__ float s_best[kMaxBeam];
   __shared__ unsigned char s_pfin[kMaxBeam];
@@ -73,21 +83,21 @@ __global__ void __launch_bounds__(256) beam_select_kernel(const BeamArgs a) {
   for (int k = 0; k < K; ++k) {
     const __half* row = a.logits + (size_t)(r * K + k) * a.ldl;
     float m = -INFINITY;
-    for (int v = tid; v < V; v += 256) m = fmaxf(m, __half2float(row[v]));
+    for (int v = tid; v < V; v += kSelThreads) m = fmaxf(m, __half2float(row[v]));
     m = warp_max(m);
     if (lane == 0) s_red[warp] = m;
     __syncthreads();
     m = s_red[0];
-    for (int w = 1; w < 8; ++w) m = fmaxf(m, s_red[w]);
+    for (int w = 1; w < kSelWarps; ++w) m = fmaxf(m, s_red[w]);
     __syncthreads();
     float z = 0.0f;
-    for (int v = tid; v < V; v += 256) z += expf(__fsub_rn(__half2float(row[v]), m));
+    for (int v = tid; v < V; v += kSelThreads) z += expf(__fsub_rn(__half2float(row[v]), m));
     z = warp_sum(z);
     if (lane == 0) s_red[warp] = z;
     __syncthreads();
     if (tid == 0) {
       float t = 0.0f;
-      for (int w = 0; w < 8; ++w) t += s_red[w];
+      for (int w = 0; w < kSelWarps; ++w) t += s_red[w];
       s_max[k] = m;
       s_lz[k] = logf(t);
     }
@@ -107,21 +117,24 @@ __global__ void __launch_bounds__(256) beam_select_kernel(const BeamArgs a) {
     if (sc == -INFINITY) continue;
     const float m = s_max[k], lz = s_lz[k];
     const __half* row = a.logits + (size_t)b * a.ldl;
-    for (int v = tid; v < V; v += 256) {
+    for (int v = tid; v < V; v += kSelThreads) {
       const float lp = __fsub_rn(__fsub_rn(__half2float(row[v]), m), lz);
       topk_insert(top, K, Cand{__fadd_rn(sc, lp), k * V + v});
     }
   }
   // ---- block merge: K rounds of arg-best over the per-thread list heads
+  // (warp shuffles, then the warp winners; candidates are unique by index)
   int head = 0;
   for (int round = 0; round < K; ++round) {
     const Cand mine = head < K ? top[head] : Cand{-INFINITY, 0x7fffffff};
-    s_cand[tid] = mine;
+    const Cand wb = cand_shfl_best(mine);
+    if (lane == 0) s_cand[warp] = wb;
     __syncthreads();
-    for (int stride = 128; stride > 0; stride >>= 1) {
-      if (tid < stride && cand_better(s_cand[tid + stride], s_cand[tid])) s_cand[tid] = s_cand[tid + stride];
-      __syncthreads();
+    if (warp == 0) {
+      const Cand c = cand_shfl_best(lane < kSelWarps ? s_cand[lane] : Cand{-INFINITY, 0x7fffffff});
+      if (lane == 0) s_cand[0] = c;
     }
+    __syncthreads();
     const Cand best = s_cand[0];
     if (head < K && mine.i == best.i && mine.v == best.v) ++head;  // owner pops its head
     if (tid == 0) {
@@ -130,17 +143,17 @@ __global__ void __launch_bounds__(256) beam_select_kernel(const BeamArgs a) {
       s_tok[round] = best.i - pb * V;
       s_best[round] = best.v;
     }
-    __syncthreads();
+    __syncthreads();  // s_cand[0] read by all before the next round's writes
   }
   // ---- read everything the children inherit before any row is rewritten
   if (tid < K) s_pfin[tid] = a.finished[r * K + s_parent[tid]];
-  for (int i = tid; i < K * len; i += 256) {
+  for (int i = tid; i < K * len; i += kSelThreads) {
     const int k = i / len, s = i - k * len;
     s_indir[k * a.cap + s] = a.indir[(size_t)(r * K + k) * a.cap + s];
   }
   __syncthreads();
   const int span = min(len + 1, a.cap);
-  for (int i = tid; i < K * span; i += 256) {
+  for (int i = tid; i < K * span; i += kSelThreads) {
     const int k = i / span, s = i - k * span;
     a.indir[(size_t)(r * K + k) * a.cap + s] = (s < len) ? s_indir[s_parent[k] * a.cap + s] : k;
   }

@@ -1667,7 +1667,7 @@ void run_beam_select(const Session& s, const tf_beam_desc& d, cudaStream_t st, b
     attr = true;
   }
   TF_REQUIRE(smem <= kMaxSmem - 8192, TF_ERR_UNSUPPORTED, "beam: capacity too large");
-  launch(beam_select_kernel, dim3(a.R), dim3(256), smem, st, pdl, a);
+  launch(beam_select_kernel, dim3(a.R), dim3(kSelThreads), smem, st, pdl, a);
 }
 
 // one beam step: feed `tokens` (generated ids, no remap), last-row logits, select
