@@ -55,6 +55,23 @@ __device__ __forceinline__ void topk_insert(Cand (&t)[kMaxBeam], int K, Cand c) 
   t[j] = c;
 }
 
+// register form: a compare-and-swap pass over the (statically indexed) list;
+// `worst` tracks top[K - 1] for the cheap rejection test
+__device__ __forceinline__ void topk_insert_reg(Cand (&t)[kMaxBeam], int K, Cand c, Cand& worst) {
+  if (!cand_better(c, worst)) return;
+#pragma unroll
+  for (int j = 0; j < kMaxBeam; ++j) {
+    if (j < K && cand_better(c, t[j])) {
+      const Cand x = t[j];
+      t[j] = c;
+      c = x;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxBeam; ++j)
+    if (j == K - 1) worst = t[j];
+}
+
 __device__ __forceinline__ Cand cand_shfl_best(Cand c) {  // warp arg-best (total order: any tree)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -66,52 +83,80 @@ __device__ __forceinline__ Cand cand_shfl_best(Cand c) {  // warp arg-best (tota
 
 // blockDim = kSelThreads; dynamic smem = K * cap ints (indirection staging)
 constexpr int kSelThreads = 1024, kSelWarps = kSelThreads / 32;
+// KB = beam width (compile time: the top-K list stays in registers)
+template <int KB>
 __global__ void __launch_bounds__(kSelThreads) beam_select_kernel(const BeamArgs a) {
   pdl_wait();
-  __shared__ float s_max[kMaxBeam], s_lz[kMaxBeam], s_red[kSelWarps];
+  __shared__ float s_max[kMaxBeam], s_lz[kMaxBeam], s_red2[kMaxBeam][kSelWarps];
   __shared__ Cand s_cand[kSelWarps];
   __shared__ int s_parent[kMaxBeam], s_tok[kMaxBeam];
   __shared__ float s_best[kMaxBeam];
   __shared__ unsigned char s_pfin[kMaxBeam];
   extern __shared__ int s_indir[];  // [K][cap]
-  const int r = blockIdx.x, K = a.K, V = a.V;
+  constexpr int K = KB;
+  const int r = blockIdx.x, V = a.V;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int step = *a.len_dev - a.prompt_len;
   const int len = *a.len_dev;
 
-  // ---- per-beam max and log(sum exp(x - max)) over the f16 logits
-  for (int k = 0; k < K; ++k) {
-    const __half* row = a.logits + (size_t)(r * K + k) * a.ldl;
-    float m = -INFINITY;
-    for (int v = tid; v < V; v += kSelThreads) m = fmaxf(m, __half2float(row[v]));
-    m = warp_max(m);
-    if (lane == 0) s_red[warp] = m;
-    __syncthreads();
-    m = s_red[0];
-    for (int w = 1; w < kSelWarps; ++w) m = fmaxf(m, s_red[w]);
-    __syncthreads();
-    float z = 0.0f;
-    for (int v = tid; v < V; v += kSelThreads) z += expf(__fsub_rn(__half2float(row[v]), m));
-    z = warp_sum(z);
-    if (lane == 0) s_red[warp] = z;
-    __syncthreads();
-    if (tid == 0) {
-      float t = 0.0f;
-      for (int w = 0; w < kSelWarps; ++w) t += s_red[w];
-      s_max[k] = m;
-      s_lz[k] = logf(t);
+  // ---- per-beam max and log(sum exp(x - max)) over the f16 logits, all K
+  // rows per pass (per-row arithmetic and summation order unchanged)
+  {
+    const __half* rows = a.logits + (size_t)(r * K) * a.ldl;
+    float m[kMaxBeam], z[kMaxBeam];
+#pragma unroll
+    for (int k = 0; k < kMaxBeam; ++k) m[k] = -INFINITY, z[k] = 0.0f;
+    for (int v = tid; v < V; v += kSelThreads) {
+#pragma unroll
+      for (int k = 0; k < kMaxBeam; ++k)
+        if (k < K) m[k] = fmaxf(m[k], __half2float(rows[(size_t)k * a.ldl + v]));
     }
+#pragma unroll
+    for (int k = 0; k < kMaxBeam; ++k) {
+      m[k] = warp_max(m[k]);
+      if (k < K && lane == 0) s_red2[k][warp] = m[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kMaxBeam; ++k) {
+      if (k < K) {
+        float mm = s_red2[k][0];
+        for (int w = 1; w < kSelWarps; ++w) mm = fmaxf(mm, s_red2[k][w]);
+        m[k] = mm;
+      }
+    }
+    for (int v = tid; v < V; v += kSelThreads) {
+#pragma unroll
+      for (int k = 0; k < kMaxBeam; ++k)
+        if (k < K) z[k] += expf(__fsub_rn(__half2float(rows[(size_t)k * a.ldl + v]), m[k]));
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxBeam; ++k) z[k] = warp_sum(z[k]);
+    __syncthreads();  // every thread has read s_red2 (max)
+#pragma unroll
+    for (int k = 0; k < kMaxBeam; ++k)
+      if (k < K && lane == 0) s_red2[k][warp] = z[k];
+    __syncthreads();
+    if (tid < K) {
+      float t = 0.0f;
+      for (int w = 0; w < kSelWarps; ++w) t += s_red2[tid][w];
+      s_lz[tid] = logf(t);
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxBeam; ++k)
+      if (k < K && tid == 0) s_max[k] = m[k];
     __syncthreads();
   }
   // ---- per-thread top-K over this request's K*V candidates
   Cand top[kMaxBeam];
 #pragma unroll
   for (int j = 0; j < kMaxBeam; ++j) top[j] = Cand{-INFINITY, 0x7fffffff};
+  Cand worst = top[0];  // == top[K - 1]
   for (int k = 0; k < K; ++k) {
     const int b = r * K + k;
     const float sc = a.scores[b];
     if (a.finished[b]) {  // frozen: proposes only itself, with eos
-      if (tid == 0) topk_insert(top, K, Cand{sc, k * V + a.eos});
+      if (tid == 0) topk_insert_reg(top, K, Cand{sc, k * V + a.eos}, worst);
       continue;
     }
     if (sc == -INFINITY) continue;
@@ -119,14 +164,15 @@ __global__ void __launch_bounds__(kSelThreads) beam_select_kernel(const BeamArgs
     const __half* row = a.logits + (size_t)b * a.ldl;
     for (int v = tid; v < V; v += kSelThreads) {
       const float lp = __fsub_rn(__fsub_rn(__half2float(row[v]), m), lz);
-      topk_insert(top, K, Cand{__fadd_rn(sc, lp), k * V + v});
+      const Cand c{__fadd_rn(sc, lp), k * V + v};
+      if (cand_better(c, worst)) topk_insert_reg(top, K, c, worst);
     }
   }
   // ---- block merge: K rounds of arg-best over the per-thread list heads
   // (warp shuffles, then the warp winners; candidates are unique by index)
   int head = 0;
   for (int round = 0; round < K; ++round) {
-    const Cand mine = head < K ? top[head] : Cand{-INFINITY, 0x7fffffff};
+    const Cand mine = head < K ? top[0] : Cand{-INFINITY, 0x7fffffff};
     const Cand wb = cand_shfl_best(mine);
     if (lane == 0) s_cand[warp] = wb;
     __syncthreads();
@@ -136,7 +182,12 @@ __global__ void __launch_bounds__(kSelThreads) beam_select_kernel(const BeamArgs
     }
     __syncthreads();
     const Cand best = s_cand[0];
-    if (head < K && mine.i == best.i && mine.v == best.v) ++head;  // owner pops its head
+    if (head < K && mine.i == best.i && mine.v == best.v) {  // owner pops its head (static shift)
+      ++head;
+#pragma unroll
+      for (int j = 0; j + 1 < kMaxBeam; ++j) top[j] = top[j + 1];
+      top[kMaxBeam - 1] = Cand{-INFINITY, 0x7fffffff};
+    }
     if (tid == 0) {
       const int pb = best.i / V;
       s_parent[round] = pb;

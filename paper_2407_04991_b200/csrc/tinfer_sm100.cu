@@ -1657,17 +1657,32 @@ BeamArgs beam_args(const Session& s, const tf_beam_desc& d) {
   return a;
 }
 
-void run_beam_select(const Session& s, const tf_beam_desc& d, cudaStream_t st, bool pdl) {
-  const BeamArgs a = beam_args(s, d);
-  const size_t smem = (size_t)a.K * a.cap * sizeof(int);
+template <int KB>
+void launch_select(const BeamArgs& a, size_t smem, cudaStream_t st, bool pdl) {
   static bool attr = false;
   if (!attr) {
-    TF_CHECK_CUDA(cudaFuncSetAttribute(beam_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TF_CHECK_CUDA(cudaFuncSetAttribute(beam_select_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kMaxSmem - 8192));
     attr = true;
   }
+  launch(beam_select_kernel<KB>, dim3(a.R), dim3(kSelThreads), smem, st, pdl, a);
+}
+
+void run_beam_select(const Session& s, const tf_beam_desc& d, cudaStream_t st, bool pdl) {
+  const BeamArgs a = beam_args(s, d);
+  const size_t smem = (size_t)a.K * a.cap * sizeof(int);
   TF_REQUIRE(smem <= kMaxSmem - 8192, TF_ERR_UNSUPPORTED, "beam: capacity too large");
-  launch(beam_select_kernel, dim3(a.R), dim3(kSelThreads), smem, st, pdl, a);
+  switch (a.K) {
+    case 1: launch_select<1>(a, smem, st, pdl); break;
+    case 2: launch_select<2>(a, smem, st, pdl); break;
+    case 3: launch_select<3>(a, smem, st, pdl); break;
+    case 4: launch_select<4>(a, smem, st, pdl); break;
+    case 5: launch_select<5>(a, smem, st, pdl); break;
+    case 6: launch_select<6>(a, smem, st, pdl); break;
+    case 7: launch_select<7>(a, smem, st, pdl); break;
+    case 8: launch_select<8>(a, smem, st, pdl); break;
+    default: throw TfError{TF_ERR_UNSUPPORTED, "beam width must be in [1, 8]"};
+  }
 }
 
 // one beam step: feed `tokens` (generated ids, no remap), last-row logits, select
