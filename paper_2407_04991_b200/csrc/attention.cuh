@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const 
       unpack8(raw[g], kf);
       float acc = __fmul_rn(qr[8 * g], kf[0]);
 #pragma unroll
-      for (int e = 1; e < 8; ++e) acc = __fadd_rn(acc, __fmul_rn(qr[8 * g + e], kf[e]));
+      for (int e = 1; e < 8; ++e) acc = __fmaf_rn(qr[8 * g + e], kf[e], acc);
       ps[g] = acc;
     }
     const float d = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
@@ -578,8 +578,8 @@ __global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const 
       for (int r = 0; r < 4; ++r) {
         const float2 v = __half22float2(*reinterpret_cast<const __half2*>(Vs + (j + r) * 64 + 2 * lane));
         const float w = w0[j + r];
-        o0[r] = __fadd_rn(o0[r], __fmul_rn(w, v.x));
-        o1[r] = __fadd_rn(o1[r], __fmul_rn(w, v.y));
+        o0[r] = __fmaf_rn(w, v.x, o0[r]);
+        o1[r] = __fmaf_rn(w, v.y, o1[r]);
       }
     }
     float* dst = hf ? part_h + i * 64 : part_s + i * 66 + 2;
@@ -843,7 +843,7 @@ __global__ void __launch_bounds__(kBmThreads, 1) attn_decode_beam_kernel(const A
           unpack8(raw[g], kf);
           float acc = __fmul_rn(qr[8 * g], kf[0]);
 #pragma unroll
-          for (int e = 1; e < 8; ++e) acc = __fadd_rn(acc, __fmul_rn(qr[8 * g + e], kf[e]));
+          for (int e = 1; e < 8; ++e) acc = __fmaf_rn(qr[8 * g + e], kf[e], acc);
           ps[g] = acc;
         }
         const float d = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
@@ -875,8 +875,8 @@ __global__ void __launch_bounds__(kBmThreads, 1) attn_decode_beam_kernel(const A
         for (int q = 0; q < 4; ++q) {
           const float2 v = __half22float2(*reinterpret_cast<const __half2*>(Vs + (j + q) * 64 + 2 * lane));
           const float w = sci[j + q];
-          o0[q] = __fadd_rn(o0[q], __fmul_rn(w, v.x));
-          o1[q] = __fadd_rn(o1[q], __fmul_rn(w, v.y));
+          o0[q] = __fmaf_rn(w, v.x, o0[q]);
+          o1[q] = __fmaf_rn(w, v.y, o1[q]);
         }
       }
       float* dst = part + ((size_t)r * kBmMaxCh + c) * 66;
@@ -1078,7 +1078,7 @@ __global__ void __launch_bounds__(kBmThreads, MINB) attn_decode_beam_ring_kernel
           unpack8(raw[g], kf);
           float acc = __fmul_rn(qr[8 * g], kf[0]);
 #pragma unroll
-          for (int e = 1; e < 8; ++e) acc = __fadd_rn(acc, __fmul_rn(qr[8 * g + e], kf[e]));
+          for (int e = 1; e < 8; ++e) acc = __fmaf_rn(qr[8 * g + e], kf[e], acc);
           ps[g] = acc;
         }
         const float d = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
@@ -1111,8 +1111,8 @@ __global__ void __launch_bounds__(kBmThreads, MINB) attn_decode_beam_ring_kernel
         for (int uu = 0; uu < 4; ++uu) {
           const float2 v = __half22float2(*reinterpret_cast<const __half2*>(Vs + (j + uu) * 64 + 2 * lane));
           const float w = sci[j + uu];
-          o0[uu] = __fadd_rn(o0[uu], __fmul_rn(w, v.x));
-          o1[uu] = __fadd_rn(o1[uu], __fmul_rn(w, v.y));
+          o0[uu] = __fmaf_rn(w, v.x, o0[uu]);
+          o1[uu] = __fmaf_rn(w, v.y, o1[uu]);
         }
       }
       float* dst = part + ((size_t)r * kBmMaxCh + cc) * 66;
