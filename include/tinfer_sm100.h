@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define TF_ABI_VERSION 1
+#define TF_ABI_VERSION 2
 
 enum tf_status {
   TF_OK = 0,
@@ -91,22 +91,33 @@ typedef struct tf_gemm_desc {
                                     next kernel may launch once this one is set up),
                                     2 on, next kernel released only after this
                                     kernel's own dependency wait                   */
-  /* optional fused LayerNorm of the activation operand (swap-AB only): act is
-   * ignored and row t of the operand is q16(LN(ln_x[t*ln_src_stride+ln_src_off]))
-   * over ln_hidden features (tensor.py:153-160); ln_hidden <= 1024, % 8 == 0 */
-  const void* ln_x; int ln_ldx, ln_src_stride, ln_src_off, ln_hidden;
-  const float* ln_gamma; const float* ln_beta;
+  /* optional LayerNorm folded into the GEMM (swap-AB only; epilogues F32 /
+   * BIAS / BIAS_GELU / QKV / LOGITS): act holds the raw rows x, wt the weights
+   * with gamma folded over K (W'[n][k] = q16(W[n][k] * gamma[k])), and the
+   * accumulator becomes inv_t * (x_t . W'_n - mean_t * ln_c[n]) + ln_d[n]
+   * (= LN(x_t) . W_n, tensor.py:153-160) before the epilogue, with
+   * ln_c[n] = sum_k W'[n][k] and ln_d[n] = sum_k beta[k] W[n][k]. Row t's
+   * (mean, inv) over ln_hidden features are merged from the float pairs
+   * ln_stats[2 * (i * ln_stats_ld + t) + {0, 1}] = (mean, M2) of features
+   * [128 i, 128 i + 128) that a TF_EPI_BIAS_RESID GEMM wrote through stats_out;
+   * ln_hidden <= 2048, ln_stats_ld >= m_tok */
+  const float* ln_stats; int ln_stats_ld, ln_hidden;
+  const float* ln_c; const float* ln_d;
+  /* TF_EPI_BIAS_RESID, swap-AB split-K: also write those per-tile (mean, M2)
+   * pairs of the output rows to stats_out[2 * (tile * stats_ld + t)] */
+  float* stats_out; int stats_ld;
 } tf_gemm_desc;
 int tf_gemm(const tf_gemm_desc* d, void* stream);
 
 /* x = q16(tok_emb[id] + pos_emb[p] (+ type_emb[t])); h = q16(LN(x)) (h optional).
+ * Type rows: type_ids[tok] when given, else type_const (type_emb NULL: none).
  * Replaces the gather-sum of model.py:453-455 / embed (model.py:521-534) and the
  * first layer_norm_f32 (tensor.py:153-160). `remap` (optional) maps original ids
  * to pruned ids (pruning.py:50-52); ids outside the map go to unk_id
  * (SPEC.md:306). */
 typedef struct tf_embed_desc {
   int n_tok, hidden, vocab, max_pos;
-  const int* ids; const int* pos; const int* type_ids;
+  const int* ids; const int* pos; const int* type_ids; int type_const;
   const int* remap; int remap_n; int unk_id;
   const void* tok_emb; const void* pos_emb; const void* type_emb; int ldw;
   const float* ln_gamma; const float* ln_beta;
@@ -136,6 +147,10 @@ typedef struct tf_layer_weights {
   const float* ln2_gamma; const float* ln2_beta;
   const void* w1_t; const float* b1;     /* [F, ldk_h], [F]            */
   const void* w2_t; const float* b2;     /* [H, ldk_f], [H]            */
+  /* optional LayerNorm-folded copies for the decode path (see tf_gemm_desc):
+   * attn_norm folded into Wqkv, ffn_norm into W1 (NULL: stand-alone LN) */
+  const void* wqkv_ln_t; const float* cqkv; const float* dqkv;
+  const void* w1_ln_t; const float* c1; const float* d1;
 } tf_layer_weights;
 
 typedef struct tf_model_desc {
@@ -145,6 +160,7 @@ typedef struct tf_model_desc {
   const tf_layer_weights* layer;         /* [layers] */
   const float* final_gamma; const float* final_beta;
   const void* lm_head_t;                 /* [vocab, ldk_h] f16 */
+  const void* lm_head_ln_t; const float* c_lm; const float* d_lm; /* final_norm folded (optional) */
 } tf_model_desc;
 int tf_model_create(const tf_model_desc* d, void** model);
 int tf_model_destroy(void* model);
@@ -165,6 +181,12 @@ typedef struct tf_session_desc {
   const int* pads;                       /* [batch] left-pad offsets = first valid slot */
   const int* remap; int remap_n; int unk_id;  /* optional prompt-id remap */
   int* beam_indir; int beam;             /* beam search: [batch, capacity] slot->beam table, width */
+  /* fused decode LayerNorms: 4 * ceil(hidden/128) * batch * max_tokens floats
+   * (NULL: stand-alone LayerNorm kernels) */
+  float* ln_stats; size_t ln_stats_bytes;
+  /* type embeddings (model type_emb set): prompt rows' type ids [batch*max_tokens]
+   * (NULL: gen_type for every row) and the type of generated tokens */
+  const int* type_ids; int gen_type;
 } tf_session_desc;
 int tf_session_create(void* model, const tf_session_desc* d, void** session);
 int tf_session_destroy(void* session);
@@ -180,6 +202,12 @@ enum tf_forward_mode {
  * (T == 1): feed the previous argmax. */
 int tf_forward(void* session, const int* ids, const int* pos, int T, int mode, int pdl,
                void* stream);
+/* tf_forward that also copies the residual stream at every LayerNorm input
+ * (2L+1 taps: the embedding sum, then after each layer's Wo and FFN2 residual
+ * adds; the reference's layer_norm_f32 call sites model.py:460, 484, 497) into
+ * taps, device f16 [2L+1][batch*T][hidden]. Diagnostics for hidden-state parity. */
+int tf_forward_taps(void* session, const int* ids, const int* pos, int T, int mode, void* taps,
+                    void* stream);
 /* n greedy decode steps (model.py:651-666), each a T=1 TF_FWD_ARGMAX forward fed
  * by the previous argmax; with use_graph the step is captured once into a CUDA
  * graph and replayed. */
@@ -202,11 +230,6 @@ int tf_beam_select(void* session, const tf_beam_desc* d, void* stream);
 /* n steps of (T=1 forward of `tokens` -> last-row logits -> tf_beam_select),
  * captured once into a CUDA graph when use_graph. */
 int tf_beam_decode(void* session, const tf_beam_desc* d, int n_steps, int use_graph, void* stream);
-
-/* Diagnostics: record per-task globaltimer stamps of decode step 1 of the next
- * megakernel launch into trace_buf ([n_items + n_aux][3] int64; NULL disables);
- * reports the session's task counts and copies the plan (int4 per task). */
-int tf_debug_mk_trace(void* session, void* trace_buf, int* n_items, int* n_aux, void* plan_out);
 
 /* Diagnostics (host env TF_TRACE=1): kernels launched after a reset store
  * %globaltimer stamps of up to 8 points per CTA; reset != 0 clears them,

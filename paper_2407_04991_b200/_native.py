@@ -38,16 +38,16 @@ class GemmDesc(C.Structure):
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
         ("counters", C.c_void_p), ("n_counters", C.c_int),
         ("force_swap", C.c_int), ("splits", C.c_int), ("pdl", C.c_int),
-        ("ln_x", C.c_void_p), ("ln_ldx", C.c_int), ("ln_src_stride", C.c_int),
-        ("ln_src_off", C.c_int), ("ln_hidden", C.c_int),
-        ("ln_gamma", C.c_void_p), ("ln_beta", C.c_void_p),
+        ("ln_stats", C.c_void_p), ("ln_stats_ld", C.c_int), ("ln_hidden", C.c_int),
+        ("ln_c", C.c_void_p), ("ln_d", C.c_void_p),
+        ("stats_out", C.c_void_p), ("stats_ld", C.c_int),
     ]
 
 
 class EmbedDesc(C.Structure):
     _fields_ = [
         ("n_tok", C.c_int), ("hidden", C.c_int), ("vocab", C.c_int), ("max_pos", C.c_int),
-        ("ids", C.c_void_p), ("pos", C.c_void_p), ("type_ids", C.c_void_p),
+        ("ids", C.c_void_p), ("pos", C.c_void_p), ("type_ids", C.c_void_p), ("type_const", C.c_int),
         ("remap", C.c_void_p), ("remap_n", C.c_int), ("unk_id", C.c_int),
         ("tok_emb", C.c_void_p), ("pos_emb", C.c_void_p), ("type_emb", C.c_void_p),
         ("ldw", C.c_int),
@@ -65,6 +65,8 @@ class LayerWeights(C.Structure):
         ("ln2_gamma", C.c_void_p), ("ln2_beta", C.c_void_p),
         ("w1_t", C.c_void_p), ("b1", C.c_void_p),
         ("w2_t", C.c_void_p), ("b2", C.c_void_p),
+        ("wqkv_ln_t", C.c_void_p), ("cqkv", C.c_void_p), ("dqkv", C.c_void_p),
+        ("w1_ln_t", C.c_void_p), ("c1", C.c_void_p), ("d1", C.c_void_p),
     ]
 
 
@@ -78,6 +80,7 @@ class ModelDesc(C.Structure):
         ("layer", C.POINTER(LayerWeights)),
         ("final_gamma", C.c_void_p), ("final_beta", C.c_void_p),
         ("lm_head_t", C.c_void_p),
+        ("lm_head_ln_t", C.c_void_p), ("c_lm", C.c_void_p), ("d_lm", C.c_void_p),
     ]
 
 
@@ -93,6 +96,8 @@ class SessionDesc(C.Structure):
         ("out_tokens", C.c_void_p), ("pads", C.c_void_p),
         ("remap", C.c_void_p), ("remap_n", C.c_int), ("unk_id", C.c_int),
         ("beam_indir", C.c_void_p), ("beam", C.c_int),
+        ("ln_stats", C.c_void_p), ("ln_stats_bytes", C.c_size_t),
+        ("type_ids", C.c_void_p), ("gen_type", C.c_int),
     ]
 
 
@@ -124,15 +129,16 @@ SIGNATURES = {
     "tf_session_destroy": (C.c_int, [C.c_void_p]),
     "tf_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
                              C.c_void_p]),
+    "tf_forward_taps": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                  C.c_void_p]),
     "tf_decode": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "tf_beam_select": (C.c_int, [C.c_void_p, C.POINTER(BeamDesc), C.c_void_p]),
     "tf_beam_decode": (C.c_int, [C.c_void_p, C.POINTER(BeamDesc), C.c_int, C.c_int, C.c_void_p]),
-    "tf_debug_mk_trace": (C.c_int, [C.c_void_p, C.c_void_p, c_int_p, c_int_p, C.c_void_p]),
     "tf_debug_trace": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
     "tf_session_launches_per_step": (C.c_int, [C.c_void_p]),
 }
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # tf_epilogue / tf_forward_mode (include/tinfer_sm100.h)
 EPI_F32, EPI_BIAS, EPI_BIAS_GELU, EPI_BIAS_RESID, EPI_QKV, EPI_LOGITS = range(6)

@@ -43,16 +43,6 @@ struct AttnArgs {
   // streams its own window of them HBM -> L2 (null = off)
   const __half* pf_kc;
   const __half* pf_vc;
-  // decode prefetch kernel, whole window in one CTA: fused output projection.
-  // The CTA multiplies its head's (f16) output row by that head's K-slice of
-  // Wo (wo_t [H, ldw] K-major, columns h*D .. h*D+D) and writes the f32 partial
-  // wo_part[(b * NH + h) * H + n]; the heads are summed (in head order) with the
-  // bias and residual by resid_heads_ln_kernel (model.py:478-482).
-  const __half* wo_t;
-  int ldw, H;
-  float* wo_part;
-  const void* l2pf;  // HBM -> L2 prefetch range (the next layer's Wo)
-  unsigned long long l2pf_bytes;
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
@@ -104,7 +94,10 @@ __global__ void __launch_bounds__(256, 3) attn_decode_kernel(const AttnArgs a) {
   const __half* V = a.vc;
 
   // ---- scores
-  if ((D & 7) == 0 && D <= 256) {
+  // vector path: G = D / 8 lanes per key must be a power of two (the xor
+  // reductions below pair lanes inside aligned groups of G)
+  const bool vec = (D & 7) == 0 && D <= 256 && (((D >> 3) & ((D >> 3) - 1)) == 0);
+  if (vec) {
     const int G = D >> 3;                 // lanes per key (16 B each)
     const int kpw = 32 / G > 0 ? 32 / G : 1;  // keys per warp load
     const int sub = lane / G, gl = lane - sub * G;
@@ -164,7 +157,7 @@ __global__ void __launch_bounds__(256, 3) attn_decode_kernel(const AttnArgs a) {
   const float inv = __fdiv_rn(1.0f, z);
   __syncthreads();
   // ---- weighted sum of V
-  if ((D & 7) == 0 && D <= 256) {
+  if (vec) {
     // G lanes per value row (8 dims each, 16-byte loads), kpw rows per warp
     // load, 8 loads in flight; sub-groups and warps combined in a fixed order
     const int G = D >> 3;
@@ -231,166 +224,6 @@ __global__ void __launch_bounds__(256, 3) attn_decode_kernel(const AttnArgs a) {
   }
 }
 
-// ------------------------------------------------------------------ split-KV decode
-// grid (max_chunks, NH, B), 128 threads; chunk c covers window slots
-// [lo + 64c, lo + 64c + 64) (aligned to the row's first valid slot). Each CTA
-// writes its partial softmax state (max m, sum z, unnormalised o[64]); the last
-// chunk of a (b, h) to finish merges them in chunk order (deterministic).
-constexpr int kSplitKeys = 64;
-constexpr int kSplitThreads = 128;
-
-__global__ void __launch_bounds__(kSplitThreads) attn_decode_split_kernel(const AttnArgs a) {
-  __shared__ float qs[64], sc[kSplitKeys], red[4 * 64 + 8];
-  __shared__ int s_last;
-  TF_TRACE_INIT(tr);
-  if (threadIdx.x == 0) tr.mark(a.trace, 0);
-  pdl_wait();
-  if (threadIdx.x == 0) tr.mark(a.trace, 1);
-  pdl_trigger();
-  constexpr int D = 64;
-  const int c = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int qbase = *a.qbase_dev;
-  const int lo = a.start[b], hi = qbase;  // window [lo, hi]
-  const int n = hi - lo + 1;
-  const int nch = n > 0 ? (n + kSplitKeys - 1) / kSplitKeys : 0;
-  if (c >= nch && !(n <= 0 && c == 0)) return;
-  __half* orow = a.out + (size_t)b * a.ldo + (size_t)h * D;
-  if (n <= 0) {  // empty window: zeros
-    if (tid < D) orow[tid] = __float2half_rn(0.0f);
-    return;
-  }
-  const size_t row_stride = (size_t)a.NH * a.cap * D, head_stride = (size_t)a.cap * D;
-  const int* ind = a.indir ? a.indir + (size_t)b * a.cap : nullptr;
-  const int beam0 = a.indir ? (b / a.beam) * a.beam : b;
-  auto kv_off = [&](int s) -> size_t {
-    const int src = ind ? beam0 + ind[s] : b;
-    return (size_t)src * row_stride + (size_t)h * head_stride + (size_t)s * D;
-  };
-  if (tid < D) qs[tid] = __half2float(a.q[(size_t)b * a.ldq + (size_t)h * D + tid]);
-  const int j0 = c * kSplitKeys, cnt_keys = min(kSplitKeys, n - j0);
-  const int sub = lane >> 3, gl = lane & 7;
-  // K rows: 4 warps x 4 rows per load x 4 loads in flight = 64 keys
-  uint4 kr[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int j = warp * 16 + u * 4 + sub;
-    kr[u] = j < cnt_keys ? *reinterpret_cast<const uint4*>(a.kc + kv_off(lo + j0 + j) + gl * 8)
-                         : make_uint4(0, 0, 0, 0);
-  }
-  // V rows issued now too (independent of the scores)
-  uint4 vr[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int j = warp * 16 + u * 4 + sub;
-    vr[u] = j < cnt_keys ? *reinterpret_cast<const uint4*>(a.vc + kv_off(lo + j0 + j) + gl * 8)
-                         : make_uint4(0, 0, 0, 0);
-  }
-  __syncthreads();  // qs
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int j = warp * 16 + u * 4 + sub;
-    float kf[8], acc = 0.0f;
-    unpack8(kr[u], kf);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc = __fadd_rn(acc, __fmul_rn(qs[gl * 8 + e], kf[e]));
-    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    if (gl == 0 && j < cnt_keys) sc[j] = __fmul_rn(acc, a.scale);
-  }
-  __syncthreads();
-  // chunk max / exp / sum (64 scores: 2 per lane of warp 0.. handled by all)
-  float m = -INFINITY;
-  for (int j = tid; j < cnt_keys; j += kSplitThreads) m = fmaxf(m, sc[j]);
-  m = warp_max(m);
-  if (lane == 0) red[4 * 64 + warp] = m;
-  __syncthreads();
-  m = fmaxf(fmaxf(red[256], red[257]), fmaxf(red[258], red[259]));
-  float z = 0.0f;
-  __syncthreads();
-  for (int j = tid; j < cnt_keys; j += kSplitThreads) {
-    const float e = expf(__fsub_rn(sc[j], m));
-    sc[j] = e;
-    z += e;
-  }
-  z = warp_sum(z);
-  if (lane == 0) red[4 * 64 + 4 + warp] = z;
-  __syncthreads();
-  z = (red[260] + red[261]) + (red[262] + red[263]);
-  // unnormalised o = sum_j e_j v_j
-  float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int j = warp * 16 + u * 4 + sub;
-    if (j < cnt_keys) {
-      float vf[8];
-      unpack8(vr[u], vf);
-      const float w = sc[j];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = __fadd_rn(o[e], __fmul_rn(w, vf[e]));
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    o[e] = __fadd_rn(o[e], __shfl_xor_sync(0xffffffffu, o[e], 8));
-    o[e] = __fadd_rn(o[e], __shfl_xor_sync(0xffffffffu, o[e], 16));
-  }
-  if (sub == 0)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) red[warp * 64 + gl * 8 + e] = o[e];
-  __syncthreads();
-  // partial state [b][h][chunk] = {m, z, o[64]}
-  float* part = a.ws + (((size_t)b * a.NH + h) * a.max_chunks) * 66;
-  if (tid < D) {
-    const float ov = __fadd_rn(__fadd_rn(red[tid], red[64 + tid]), __fadd_rn(red[128 + tid], red[192 + tid]));
-    if (nch == 1) {
-      orow[tid] = f16_sat(__fdiv_rn(ov, z));
-      return;
-    }
-    __stcg(part + (size_t)c * 66 + 2 + tid, ov);
-    if (tid == 0) {
-      __stcg(part + (size_t)c * 66, m);
-      __stcg(part + (size_t)c * 66 + 1, z);
-    }
-  }
-  if (nch == 1) return;
-  fence_acq_rel_gpu();
-  __syncthreads();
-  if (tid == 0) {
-    tr.mark(a.trace, 3);
-    const int prev = atomicAdd(a.cnt + (size_t)b * a.NH + h, 1);
-    s_last = (prev == nch - 1);
-  }
-  __syncthreads();
-  if (!s_last) {
-    if (tid == 0) {
-      tr.mark(a.trace, 4);
-      tr.flush(a.trace);
-    }
-    return;
-  }
-  fence_acq_rel_gpu();
-  // merge in chunk order: M = max m_c, Z = sum z_c e^(m_c - M), O = sum o_c e^(m_c - M)
-  if (tid < D) {
-    float M = -INFINITY;
-    for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, __ldcg(part + (size_t)cc * 66));
-    float Z = 0.0f, O = 0.0f;
-    for (int cc = 0; cc < nch; ++cc) {
-      const float f = expf(__fsub_rn(__ldcg(part + (size_t)cc * 66), M));
-      Z = __fadd_rn(Z, __fmul_rn(__ldcg(part + (size_t)cc * 66 + 1), f));
-      O = __fadd_rn(O, __fmul_rn(__ldcg(part + (size_t)cc * 66 + 2 + tid), f));
-    }
-    orow[tid] = f16_sat(__fdiv_rn(O, Z));
-  }
-  if (tid == 0) {
-    a.cnt[(size_t)b * a.NH + h] = 0;  // ready for the next launch / replay
-    tr.mark(a.trace, 7);
-    tr.flush(a.trace);
-  }
-}
-
-
 // ------------------------------------------------------------------ decode, prefetching
 // head_dim 64. CTA (g, h, b) owns chunks [g*G, g*G+G) of the 64-slot chunks of
 // row b's window [start_b, len] (aligned to start_b, as in the split kernel).
@@ -408,14 +241,10 @@ constexpr int kPfMaxG = 8;  // chunks per CTA at most
 __host__ __device__ inline size_t attn_pf_smem_bytes(int G) {
   return (size_t)G * kPfChunkBytes + (size_t)G * (66 + 64) * sizeof(float);
 }
-// 128 threads (4 CTAs per SM: a batch-32 step is one wave) or 256 (one key
-// per thread for QK^T, every chunk half its own warp; large batches)
+// 128 threads (4 CTAs per SM: a batch-32 step is one wave)
 
-// WO: the fused output projection epilogue (AttnArgs::wo_t) is compiled in
-// MINB: resident CTAs per SM the register budget must allow (3 lets a
-// batch-32 step's 384 CTAs of 256 threads run in one wave)
-template <bool WO, int kPfThreads, int MINB = 1>
-__global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const AttnArgs a) {
+template <int kPfThreads>
+__global__ void __launch_bounds__(kPfThreads, 1) attn_decode_pf_kernel(const AttnArgs a) {
   extern __shared__ __align__(128) uint8_t pf_smem[];
   __shared__ __align__(16) float qs[64];
   __shared__ float sc_all[kPfMaxG * 64];
@@ -480,7 +309,6 @@ __global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const 
     const size_t off = kv_off(s0);
     l2_prefetch_bulk((tid == 0 ? a.pf_kc : a.pf_vc) + off, (uint32_t)((s1 - s0) * D * 2));
   }
-  if (tid == 32) l2_prefetch_share(a.l2pf, a.l2pf_bytes);
   pdl_trigger();
   pdl_wait();
   if (threadIdx.x == 0) tr.mark(a.trace, 1);
@@ -616,43 +444,6 @@ __global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const 
   };
   if (ngr == 1) {
     merge(part_s, nch);
-    if constexpr (WO) {
-      // o (as stored, f16-rounded: model.py:476-477) -> smem, then one 128-B Wo
-      // row segment per 8 lanes: lane part p sums its 8 products in order, the
-      // 8 parts combine by an xor butterfly (fixed order), 16 rows per pass
-      __syncthreads();
-      if (tid < D) qs[tid] = __half2float(orow[tid]);
-      __syncthreads();
-      constexpr int RPP = kPfThreads / 8;  // Wo rows per pass
-      const int part = tid & 7, r0 = tid >> 3;
-      float o8[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) o8[e] = qs[part * 8 + e];
-      const __half* wbase = a.wo_t + (size_t)h * D + part * 8;
-      float* dst = a.wo_part + ((size_t)b * a.NH + h) * a.H;
-      constexpr int U = 6;  // 128-B row segments in flight per 8 lanes
-      for (int n0 = r0; n0 < a.H; n0 += RPP * U) {
-        uint4 raw[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int n = n0 + RPP * u;
-          raw[u] = n < a.H ? __ldg(reinterpret_cast<const uint4*>(wbase + (size_t)n * a.ldw)) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int n = n0 + RPP * u;
-          float wv[8];
-          unpack8(raw[u], wv);
-          float acc = __fmul_rn(o8[0], wv[0]);
-#pragma unroll
-          for (int e = 1; e < 8; ++e) acc = __fadd_rn(acc, __fmul_rn(o8[e], wv[e]));
-          acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
-          acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
-          acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
-          if (part == 0 && n < a.H) dst[n] = acc;
-        }
-      }
-    }
   } else {
     float* part = a.ws + (((size_t)b * a.NH + h) * a.max_chunks) * 66;
     for (int e = tid; e < nc * 66; e += kPfThreads) __stcg(part + (size_t)c0 * 66 + e, part_s[e]);
@@ -685,7 +476,7 @@ __global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const 
   }
 }
 
-// ------------------------------------------------------------------ decode, beam groups
+// ------------------------------------------------------------------ decode, beam groups (ring)
 // head_dim 64, beam search (indir != null). One CTA (256 threads) per (head,
 // request) scores all R = beam rows of the request over the whole window. The
 // beams of a request share their prompt: a 64-slot chunk whose slots resolve
@@ -693,228 +484,15 @@ __global__ void __launch_bounds__(kPfThreads, MINB) attn_decode_pf_kernel(const 
 // shared generated ancestry counts too) is staged in shared memory ONCE and
 // every K row read from it serves R dot products; other chunks are staged per
 // beam. Chunks are staged in 16 KB planes (K rotated | V, as in
-// attn_decode_pf_kernel) from a pool of `planes`; windows needing more planes
-// run in several batches. Per (beam, chunk) the arithmetic -- scores, chunk
+// attn_decode_pf_kernel). Per (beam, chunk) the arithmetic -- scores, chunk
 // softmax, PV with one warp, and the merge in chunk order -- is that of
 // attn_decode_pf_kernel<.., 128>, so the output is bitwise the same as the
 // per-row kernel's (the oracle comparison and batch invariance carry over).
 constexpr int kBmThreads = 256, kBmMaxCh = 8;  // window <= 512 slots
-__host__ __device__ inline size_t attn_beam_aux_bytes(int R) {
-  // s_ind [R][512] int | sc [R][8][64] f32 | part [R][8][66] f32 | q [R][64] f32
-  return (size_t)R * (kBmMaxCh * 64 * 4 + kBmMaxCh * 64 * 4 + kBmMaxCh * 66 * 4 + 64 * 4);
-}
-__host__ __device__ inline size_t attn_beam_smem_bytes(int R, int planes) {
-  return (size_t)planes * kPfChunkBytes + attn_beam_aux_bytes(R);
-}
-
-__global__ void __launch_bounds__(kBmThreads, 1) attn_decode_beam_kernel(const AttnArgs a, int planes) {
-  extern __shared__ __align__(128) uint8_t bm_smem[];
-  __shared__ int s_sh[kBmMaxCh], s_pl[kBmMaxCh], s_bend[kBmMaxCh + 1], s_nb;
-  constexpr int D = 64;
-  TF_TRACE_INIT(tr);
-  if (threadIdx.x == 0) tr.mark(a.trace, 0);
-  const int R = a.beam;
-  __half* kvs = reinterpret_cast<__half*>(bm_smem);
-  int* s_ind = reinterpret_cast<int*>(bm_smem + (size_t)planes * kPfChunkBytes);  // [R][512]
-  float* sc = reinterpret_cast<float*>(s_ind + (size_t)R * kBmMaxCh * 64);      // [R][8][64]
-  float* part = sc + (size_t)R * kBmMaxCh * 64;                                  // [R][8][66]
-  float* qs = part + (size_t)R * kBmMaxCh * 66;                                  // [R][64]
-  const int h = blockIdx.y, rq = blockIdx.z, beam0 = rq * R;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int qbase = *a.qbase_dev;
-  const int lo = a.start[beam0], hi = qbase;  // the beams of a request share the left pad
-  const int n = hi - lo + 1;
-  const int nch = n > 0 ? (n + 63) / 64 : 0;
-  const size_t row_stride = (size_t)a.NH * a.cap * D, head_stride = (size_t)a.cap * D;
-  // ---- before the wait: indirection rows (slots < hi), sharing per chunk, plan
-  for (int i = tid; i < R * nch * 64; i += kBmThreads) {
-    const int r = i / (nch * 64), k = i % (nch * 64), s = lo + k;
-    s_ind[r * kBmMaxCh * 64 + k] = s < hi ? a.indir[(size_t)(beam0 + r) * a.cap + s] : 0;
-  }
-  __syncthreads();
-  if (warp < nch) {
-    bool same = true;
-    for (int k = warp * 64 + lane; k < warp * 64 + 64; k += 32) {
-      const int s = lo + k;
-      if (s == hi) same = false;  // the newest slot: each beam's own row
-      for (int r = 1; r < R && s < hi; ++r) same = same && s_ind[r * kBmMaxCh * 64 + k] == s_ind[k];
-    }
-    same = __all_sync(0xffffffffu, same);
-    if (lane == 0) s_sh[warp] = same;
-  }
-  __syncthreads();
-  if (tid == 0) {  // batches of consecutive chunks whose planes fit the pool
-    int nb = 0, used = 0;
-    s_bend[0] = 0;
-    for (int c = 0; c < nch; ++c) {
-      const int need = s_sh[c] ? 1 : R;
-      if (used + need > planes) {
-        s_bend[++nb] = c;
-        used = 0;
-      }
-      s_pl[c] = used;
-      used += need;
-    }
-    s_bend[++nb] = nch;
-    s_nb = nb;
-  }
-  __syncthreads();
-  const int nbatch = nch > 0 ? s_nb : 0;
-  // copies of chunks [c0, c1): plane p of chunk c holds beam p's rows (or all
-  // beams' when shared); slot hi only after the wait (after_wait)
-  auto stage = [&](int c0, int c1, bool after_wait) {
-    for (int c = c0; c < c1; ++c) {
-      const int np = s_sh[c] ? 1 : R;
-      for (int seg = tid; seg < np * 64 * 8; seg += kBmThreads) {
-        const int p = seg >> 9, j = (seg >> 3) & 63, prt = seg & 7;
-        const int k = c * 64 + j, slot = lo + k;
-        if (slot == hi && !after_wait) continue;
-        const bool ok = slot <= hi;
-        const int src = slot == hi ? beam0 + a.indir[(size_t)(beam0 + p) * a.cap + hi]
-                                   : beam0 + s_ind[p * kBmMaxCh * 64 + k];
-        const size_t off = ok ? (size_t)src * row_stride + (size_t)h * head_stride + (size_t)slot * D + prt * 8 : 0;
-        __half* pb = kvs + (size_t)(s_pl[c] + p) * (2 * 64 * 64);
-        cp_async16(smem_u32(pb + (size_t)j * 64 + ((prt + j) & 7) * 8), a.kc + off, ok);
-        cp_async16(smem_u32(pb + (size_t)(64 + j) * 64 + prt * 8), a.vc + off, ok);
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  if (threadIdx.x == 0) tr.mark(a.trace, 6);
-  if (nbatch > 0) stage(0, s_bend[1], false);
-  if (tid == 32) l2_prefetch_share(a.l2pf, a.l2pf_bytes);
-  pdl_trigger();
-  pdl_wait();
-  if (threadIdx.x == 0) tr.mark(a.trace, 1);
-  if (n <= 0) {
-    for (int i = tid; i < R * D; i += kBmThreads)
-      a.out[(size_t)(beam0 + i / D) * a.ldo + (size_t)h * D + i % D] = __float2half_rn(0.0f);
-    return;
-  }
-  if (threadIdx.x == 0) tr.mark(a.trace, 3);
-  for (int i = tid; i < R * D; i += kBmThreads)
-    qs[i] = __half2float(a.q[(size_t)(beam0 + i / D) * a.ldq + (size_t)h * D + i % D]);
-  // the newest slot of batch 0 (if there): after the wait
-  {
-    const int cl = (hi - lo) / 64;
-    if (cl < s_bend[1]) {
-      const int j = (hi - lo) % 64;
-      for (int i = tid; i < R * 16; i += kBmThreads) {
-        const int p = i >> 4, kv = (i >> 3) & 1, prt = i & 7;
-        const int src = beam0 + a.indir[(size_t)(beam0 + p) * a.cap + hi];
-        const size_t off = (size_t)src * row_stride + (size_t)h * head_stride + (size_t)hi * D + prt * 8;
-        __half* pb = kvs + (size_t)(s_pl[cl] + p) * (2 * 64 * 64);
-        __half* dst = pb + (size_t)(kv * 64 + j) * 64 + (kv ? prt : ((prt + j) & 7)) * 8;
-        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>((kv ? a.vc : a.kc) + off);
-      }
-    }
-  }
-  __syncthreads();  // qs complete
-  // QK^T: thread -> fixed beam r = tid % R (q in registers), keys strided
-  const int RT = (kBmThreads / R) * R;  // threads with a beam
-  const int my_r = tid % R;
-  float qr[64];
-#pragma unroll
-  for (int e = 0; e < 64; e += 4) {
-    const float4 q4 = *reinterpret_cast<const float4*>(qs + (tid < RT ? my_r : 0) * 64 + e);
-    qr[e] = q4.x;
-    qr[e + 1] = q4.y;
-    qr[e + 2] = q4.z;
-    qr[e + 3] = q4.w;
-  }
-  for (int bt = 0; bt < nbatch; ++bt) {
-    const int c0 = s_bend[bt], c1 = s_bend[bt + 1];
-    if (bt > 0) stage(c0, c1, true);
-    cp_async_commit_wait_all();
-    __syncthreads();
-    if (threadIdx.x == 0 && bt == 0) tr.mark(a.trace, 2);
-    const int nk = min((c1 - c0) * 64, n - c0 * 64);
-    if (tid < RT) {
-      for (int key = tid / R; key < nk; key += kBmThreads / R) {
-        const int c = c0 + (key >> 6), j = key & 63;
-        const __half* kr = kvs + (size_t)(s_pl[c] + (s_sh[c] ? 0 : my_r)) * (2 * 64 * 64) + (size_t)j * 64;
-        uint4 raw[8];
-#pragma unroll
-        for (int g = 0; g < 8; ++g) raw[g] = *reinterpret_cast<const uint4*>(kr + ((g + j) & 7) * 8);
-        float ps[8];
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          float kf[8];
-          unpack8(raw[g], kf);
-          float acc = __fmul_rn(qr[8 * g], kf[0]);
-#pragma unroll
-          for (int e = 1; e < 8; ++e) acc = __fmaf_rn(qr[8 * g + e], kf[e], acc);
-          ps[g] = acc;
-        }
-        const float d = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
-                                  __fadd_rn(__fadd_rn(ps[4], ps[5]), __fadd_rn(ps[6], ps[7])));
-        sc[((size_t)my_r * kBmMaxCh + c) * 64 + j] = __fmul_rn(d, a.scale);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && bt == 0) tr.mark(a.trace, 4);
-    // one warp per (beam, chunk): chunk softmax + PV (attn_decode_pf_kernel, WPC 1)
-    for (int u = warp; u < R * (c1 - c0); u += kBmThreads / 32) {
-      const int r = u % R, c = c0 + u / R;
-      const int cnt_keys = min(64, n - c * 64);
-      float* sci = sc + ((size_t)r * kBmMaxCh + c) * 64;
-      const float s0 = lane < cnt_keys ? sci[lane] : -INFINITY;
-      const float s1 = lane + 32 < cnt_keys ? sci[lane + 32] : -INFINITY;
-      const float m = warp_max(fmaxf(s0, s1));
-      const float e0 = lane < cnt_keys ? expf(__fsub_rn(s0, m)) : 0.0f;
-      const float e1 = lane + 32 < cnt_keys ? expf(__fsub_rn(s1, m)) : 0.0f;
-      const float z = warp_sum(__fadd_rn(e0, e1));
-      sci[lane] = e0;  // this warp alone reads / writes this row
-      sci[lane + 32] = e1;
-      __syncwarp();
-      const __half* Vs = kvs + (size_t)(s_pl[c] + (s_sh[c] ? 0 : r)) * (2 * 64 * 64) + 64 * 64;
-      float o0[4] = {0.f, 0.f, 0.f, 0.f}, o1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-      for (int j = 0; j < 64; j += 4) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float2 v = __half22float2(*reinterpret_cast<const __half2*>(Vs + (j + q) * 64 + 2 * lane));
-          const float w = sci[j + q];
-          o0[q] = __fmaf_rn(w, v.x, o0[q]);
-          o1[q] = __fmaf_rn(w, v.y, o1[q]);
-        }
-      }
-      float* dst = part + ((size_t)r * kBmMaxCh + c) * 66;
-      dst[2 + 2 * lane] = __fadd_rn(__fadd_rn(o0[0], o0[1]), __fadd_rn(o0[2], o0[3]));
-      dst[3 + 2 * lane] = __fadd_rn(__fadd_rn(o1[0], o1[1]), __fadd_rn(o1[2], o1[3]));
-      if (lane == 0) {
-        dst[0] = m;
-        dst[1] = z;
-      }
-    }
-    __syncthreads();  // planes free for the next batch
-  }
-  if (threadIdx.x == 0) tr.mark(a.trace, 5);
-  // merge in chunk order per (beam, dim)
-  for (int i = tid; i < R * D; i += kBmThreads) {
-    const int r = i / D, d = i % D;
-    const float* P = part + (size_t)r * kBmMaxCh * 66;
-    float M = -INFINITY;
-    for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, P[(size_t)cc * 66]);
-    float Z = 0.0f, O = 0.0f;
-    for (int cc = 0; cc < nch; ++cc) {
-      const float f = expf(__fsub_rn(P[(size_t)cc * 66], M));
-      Z = __fadd_rn(Z, __fmul_rn(P[(size_t)cc * 66 + 1], f));
-      O = __fadd_rn(O, __fmul_rn(P[(size_t)cc * 66 + 2 + d], f));
-    }
-    a.out[(size_t)(beam0 + r) * a.ldo + (size_t)h * D + d] = f16_sat(__fdiv_rn(O, Z));
-  }
-  if (threadIdx.x == 0) {
-    tr.mark(a.trace, 7);
-    tr.flush(a.trace);
-  }
-}
-
-// Ring-pipelined form of attn_decode_beam_kernel: chunks are processed one at a
-// time in window order, their planes taken from a ring of `planes` (one
-// cp.async group per chunk), so the copies of later chunks land while earlier
-// ones are scored, and the smaller pool lets MINB CTAs share an SM (one CTA's
-// copies overlap another's arithmetic). Same arithmetic, same result.
+// Ring pipeline: chunks are processed one at a time in window order, their
+// planes taken from a ring of `planes` (one cp.async group per chunk), so the
+// copies of later chunks land while earlier ones are scored, and the small pool
+// lets MINB CTAs share an SM (one CTA's copies overlap another's arithmetic).
 __host__ __device__ inline size_t attn_beam_ring_aux_bytes(int R) {
   // s_ind [R][512] u8 | sc [R][128] f32 | part [R][8][66] f32 | q [R][64] f32
   return (size_t)R * (kBmMaxCh * 64 + 128 * 4 + kBmMaxCh * 66 * 4 + 64 * 4);
@@ -1008,7 +586,6 @@ __global__ void __launch_bounds__(kBmThreads, MINB) attn_decode_beam_ring_kernel
     }
   };
   issue(false);
-  if (tid == 32) l2_prefetch_share(a.l2pf, a.l2pf_bytes);
   pdl_trigger();
   pdl_wait();
   if (threadIdx.x == 0) tr.mark(a.trace, 1);

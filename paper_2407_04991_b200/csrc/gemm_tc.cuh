@@ -61,36 +61,27 @@ struct GemmArgs {
   const int* qbase_dev;  // cache slot of token t = 0 (device scalar; graph-replayable)
   // EPI_LOGITS
   unsigned long long* keys;  // [m_tok] packed (value, ~id) argmax keys, or null
-  // SWAP only: B operand = LayerNorm of x rows computed in-kernel (ln_x != null);
-  // token t reads x row t * ln_src_stride + ln_src_off (full ln_H-wide row for the
-  // statistics, this CTA's K-slice written into shared memory)
-  const __half* ln_x;
-  int ln_ldx, ln_src_stride, ln_src_off, ln_H;
-  const float* ln_g;
-  const float* ln_b;
+  // SWAP consumer (LNV = 1), LayerNorm folded into the GEMM: the B operand
+  // rows are the raw residual stream x and the weights W' = q16(W * gamma)
+  // (gamma folded over K), so LN(x) . W = inv_t * (x . W' - mean_t * c) + d
+  // with c = sum_k W'[:, k], d = sum_k beta_k W[:, k] (per output feature,
+  // ln_c / ln_d). Row t's (mean, inv) come from per-128-feature-tile partials
+  // ln_stats[tile * ln_stats_ld + t] = (mean_i, M2_i) written by the residual
+  // GEMM that produced x (stats_out below), merged in the epilogue.
+  const float2* ln_stats;
+  int ln_H, ln_tiles, ln_stats_ld;
+  const float* ln_c;
+  const float* ln_d;
+  // EPI_BIAS_RESID producer (push split-K): per-token (mean, M2) of the tile's
+  // new residual values, stats_out[tile_a * stats_ld + tok]
+  float2* stats_out;
+  int stats_ld;
   int trace;  // diagnostics slot (0 = off)
   int late_trigger;  // release the next kernel only after this kernel's PDL wait
   // decode: activation-independent bytes of a later kernel (the next layer's
   // copy of this weight matrix) streamed HBM -> L2 by this launch's CTAs
   const void* l2pf;
   unsigned long long l2pf_bytes;
-  // ln_x set + ln_coop: the LayerNorm of the operand rows is computed
-  // cooperatively by the split-K cluster (each CTA loads and normalises only its
-  // own K slice; row statistics are exchanged over DSMEM), see ln_coop_build
-  int ln_coop;
-  // decode EPI_BIAS_RESID with the whole output row in one cluster (grid =
-  // cluster = tiles_a x 1 x 2): split-K pair reduction plus the LayerNorm of
-  // the new residual rows over DSMEM (gemm_rowln_epilogue); writes out (x) and
-  // lnf_h = q16(LN(x)) with lnf_g / lnf_b
-  int row_ln;
-  // RED_PUSHLN: lnf_cnt[token] counts the features of a row stored so far; the
-  // CTA that completes a row normalises it (gemm_ln_tail), writes lnf_h and
-  // resets the counter
-  int* lnf_cnt;
-  const float* lnf_g;
-  const float* lnf_b;
-  __half* lnf_h;
-  int lnf_ldh;
 };
 
 constexpr int kTileA = 128;          // MMA M
@@ -111,99 +102,64 @@ __host__ __device__ inline size_t gemm_ring_bytes(int bn, int stages, int splits
   ring = ring > part ? ring : part;
   return ring > out ? ring : out;
 }
-// LN-fused B operand: the normalised K-slice (kb_per_split tiles) plus the TMA
-// staging of the full source rows (k_blocks tiles of 64 columns)
-__host__ __device__ inline size_t gemm_ln_bytes(int bn, int kb_per_split, int k_blocks) {
-  // + gamma / beta of the CTA's K slice (f32)
-  return (size_t)(kb_per_split + k_blocks) * bn * kBK * 2 + (size_t)2 * kb_per_split * kBK * 4;
-}
-// cooperative LN operand: the CTA's K slice of the rows (kb_per_split tiles),
-// then f32 scratch: 2 exchange rounds [splits][bn], segment partials
-// [bn][ceil(kb_per_split*8/4)], mean / inv [bn] each, gamma / beta of the
-// slice [kb_per_split * 64] each
-__host__ __device__ inline int gemm_ln_coop_seg(int bn, int kb_per_split) { return bn * ((kb_per_split * 8 + 3) / 4); }
-__host__ __device__ inline size_t gemm_ln_coop_bytes(int bn, int kb_per_split, int splits) {
-  return (size_t)kb_per_split * bn * kBK * 2 +
-         (size_t)(2 * splits * bn + gemm_ln_coop_seg(bn, kb_per_split) + 2 * bn + 2 * kb_per_split * kBK) * 4;
-}
+// LN-folded epilogue (LNV = 1): (mean, inv) of the tile's bn rows, f32
+__host__ __device__ inline size_t gemm_ln_bytes(int bn) { return (size_t)2 * bn * 4 + 16; }
 // push-based split-K reduction (SWAP, splits > 1, bn <= 128): every CTA owns a
-// receive buffer for the S-1 peer slices of its 1/S share of the tile
+// receive buffer for the S-1 peer slices of its share of the tile
 __host__ __device__ inline bool gemm_push_reduce(int bn, int splits, bool swap) {
   return swap && splits > 1 && bn <= 128;
 }
+// units (4 features x 1 token) per CTA of the push reduction: whole token
+// columns (32 units each), so one warp holds all 128 features of a token
+__host__ __device__ inline int gemm_push_per(int bn, int splits) { return 32 * ((bn + splits - 1) / splits); }
 __host__ __device__ inline size_t gemm_recv_bytes(int bn, int splits, bool swap) {
   if (!gemm_push_reduce(bn, splits, swap)) return 0;
-  const int U = (kTileA / 4) * bn, per = (U + splits - 1) / splits;
-  return (size_t)splits * per * 16;
+  return (size_t)splits * gemm_push_per(bn, splits) * 16;
 }
 __host__ inline size_t gemm_smem_bytes(int bn, int stages, int splits, bool swap, size_t ln_bytes = 0) {
   return 1024 + gemm_ring_bytes(bn, stages, splits, swap) + ln_bytes + gemm_recv_bytes(bn, splits, swap) +
          (2 * stages + 3) * 8 + 16;
 }
 
-// LN-fused B operand: the CTA's bn source rows were staged in smem by TMA
-// (k_blocks swizzled 64-column tiles at `stg`). kLnTpr = 8 consecutive threads
-// own one row (NT / 8 rows per pass): each sums its 16-byte chunks q = sub,
-// sub + 8, ... in order, the 8 partials combine by an xor butterfly (fixed
-// order, independent of the batch), two passes (mean; squared deviations,
-// tensor.py:153-160); then the CTA's K slice [kb0*64, (kb0+nkb)*64) is
-// normalised with gamma / beta staged in smem (gsl / bsl) and written into
-// `bln` as nkb swizzled K-major tiles of bn rows.
-constexpr int kLnTpr = 8;
-template <int NT>
-__device__ __forceinline__ void ln_build_b(const GemmArgs& p, int tile_b, int kb0, int nkb, uint8_t* bln,
-                                           const uint8_t* stg, const float* gsl, const float* bsl) {
-  const int bn = p.bn, H = p.ln_H, C = H / 8;
-  const int tid = threadIdx.x, sub = tid % kLnTpr;
-  const float Hf = (float)H;
-  for (int r0 = 0; r0 < bn; r0 += NT / kLnTpr) {
-    const int r = r0 + tid / kLnTpr;
-    const bool rv = r < bn;
-    const int rr = rv ? r : 0;
-    auto chunk = [&](int q) {
-      return *reinterpret_cast<const uint4*>(stg + (size_t)(q >> 3) * bn * 128 + rr * 128 + (((q & 7) ^ (rr & 7)) * 16));
-    };
-    float s = 0.0f;
-    if (rv)
-      for (int q = sub; q < C; q += kLnTpr) {
-        float xv[8];
-        unpack8(chunk(q), xv);
+// Row statistics for the folded LayerNorm (LNV = 1): the reference's two-pass
+// LayerNorm (tensor.py:153-160: mean; c = x - mean; var = mean(c*c);
+// c * (1/sqrt(var + 1e-5))) restated as a merge of per-tile partials
+// (mean_i, M2_i over n_i features, written by the residual GEMM that produced
+// x): mean = sum n_i mean_i / H, M2 = sum M2_i + sum n_i (mean_i - mean)^2,
+// merged in tile order (deterministic, per row, so batch-invariant). Threads
+// [t0, t0 + nthr) fill s_mi[r] = mean, s_mi[bn + r] = inv for the tile's rows.
+__device__ __forceinline__ void ln_stats_rows(const GemmArgs& p, int tile_b, float* s_mi, int t0, int nthr) {
+  const int bn = p.bn;
+  for (int r = (int)threadIdx.x - t0; r >= 0 && r < bn; r += nthr) {
+    const int t = tile_b * bn + r;
+    float mean = 0.0f, inv = 0.0f;
+    if (t < p.m_tok) {
+      float2 st[16];
+      const int nt = p.ln_tiles;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) s = __fadd_rn(s, xv[e]);
-      }
+      for (int i = 0; i < 16; ++i)
+        if (i < nt) st[i] = p.ln_stats[(size_t)i * p.ln_stats_ld + t];
+      float s = 0.0f;
 #pragma unroll
-    for (int o = kLnTpr / 2; o > 0; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-    const float mean = __fdiv_rn(s, Hf);
-    float ss = 0.0f;
-    if (rv)
-      for (int q = sub; q < C; q += kLnTpr) {
-        float xv[8];
-        unpack8(chunk(q), xv);
+      for (int i = 0; i < 16; ++i)
+        if (i < nt) s = __fadd_rn(s, __fmul_rn((float)min(kTileA, p.ln_H - i * kTileA), st[i].x));
+      mean = __fdiv_rn(s, (float)p.ln_H);
+      float m2 = 0.0f;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float d = __fsub_rn(xv[e], mean);
-          ss = __fadd_rn(ss, __fmul_rn(d, d));
+      for (int i = 0; i < 16; ++i)
+        if (i < nt) {
+          const float d = __fsub_rn(st[i].x, mean);
+          m2 = __fadd_rn(m2, __fadd_rn(st[i].y, __fmul_rn((float)min(kTileA, p.ln_H - i * kTileA), __fmul_rn(d, d))));
         }
-      }
-#pragma unroll
-    for (int o = kLnTpr / 2; o > 0; o >>= 1) ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
-    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, Hf), 1e-5f)));
-    if (rv) {
-      const bool valid = tile_b * bn + r < p.m_tok;
-      for (int q = kb0 * 8 + sub; q < (kb0 + nkb) * 8; q += kLnTpr) {
-        float xv[8], y[8];
-        unpack8(chunk(q), xv);
-        const int f0 = (q - kb0 * 8) * 8;
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          y[e] = (valid && q * 8 + e < H) ? __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[e], mean), inv), gsl[f0 + e]), bsl[f0 + e])
-                                          : 0.0f;
-        uint8_t* dst = bln + (size_t)(q / 8 - kb0) * bn * kBK * 2 + r * 128 + (((q & 7) ^ (r & 7)) * 16);
-        *reinterpret_cast<uint4*>(dst) = pack8(y);
-      }
+      inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(m2, (float)p.ln_H), 1e-5f)));
     }
+    s_mi[r] = mean;
+    s_mi[bn + r] = inv;
   }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// folded LayerNorm of one accumulator: inv * (acc - mean * c) + d
+__device__ __forceinline__ float ln_fold(float acc, float mean, float inv, float c, float d) {
+  return __fadd_rn(__fmul_rn(__fsub_rn(acc, __fmul_rn(mean, c)), inv), d);
 }
 
 // elect.sync over the full warp (lane 0 when every lane is active)
@@ -321,9 +277,10 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs& p, int ra, int qb, con
 template <int MODE>
 // 16-column chunks c0, c0 + cstep, ... (two warps per TMEM lane quadrant split them)
 __device__ __forceinline__ void epi_swap_one(const GemmArgs& p, int f, int tok0, int bn, uint32_t trow, int c0,
-                                             int cstep) {
+                                             int cstep, const float* s_mi) {
   const bool fok = f < p.n_feat;
   const float bf = fok ? p.bias[f] : 0.0f;
+  const float lc = (s_mi && fok) ? p.ln_c[f] : 0.0f, ld = (s_mi && fok) ? p.ln_d[f] : 0.0f;
   __half* dst = nullptr;
   size_t stride = 0, tstride = 0;
   int T = 1;
@@ -346,6 +303,10 @@ __device__ __forceinline__ void epi_swap_one(const GemmArgs& p, int f, int tok0,
   for (int c = c0; c < bn; c += cstep) {
     float v[16];
     tmem_ld16(trow + (uint32_t)c, v);
+    if (s_mi) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = ln_fold(v[j], s_mi[c + j], s_mi[bn + c + j], lc, ld);
+    }
     float x[16];
     if constexpr (MODE == EPI_BIAS_RESID) {
 #pragma unroll
@@ -592,6 +553,7 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
 struct EpiPre4 {
   float b[4];  // bias
   float x[4];  // residual
+  float c[4], d[4];  // folded LayerNorm terms (LNV = 1)
 };
 
 template <bool SWAP>
@@ -602,7 +564,7 @@ __device__ __forceinline__ void unit_coords(int tile_a, int tile_b, int bn, int 
   step = SWAP ? 1 : 0;  // the 4 rows advance the feature (SWAP) or the token
 }
 
-template <int MODE, bool SWAP>
+template <int MODE, bool SWAP, bool LNF = false>
 __device__ __forceinline__ void epi_pre4(const GemmArgs& p, int tile_a, int tile_b, int u, EpiPre4& q) {
   int tok, f, st;
   unit_coords<SWAP>(tile_a, tile_b, p.bn, u, tok, f, st);
@@ -610,6 +572,10 @@ __device__ __forceinline__ void epi_pre4(const GemmArgs& p, int tile_a, int tile
   for (int j = 0; j < 4; ++j) {
     const int tj = tok + (st ? 0 : j), fj = f + (st ? j : 0);
     const bool ok = tj < p.m_tok && fj < p.n_feat;
+    if constexpr (LNF) {
+      q.c[j] = ok ? p.ln_c[fj] : 0.0f;
+      q.d[j] = ok ? p.ln_d[fj] : 0.0f;
+    }
     if constexpr (MODE == EPI_BIAS || MODE == EPI_BIAS_GELU || MODE == EPI_BIAS_RESID || MODE == EPI_QKV)
       q.b[j] = ok ? p.bias[fj] : 0.0f;
     if constexpr (MODE == EPI_BIAS_RESID)
@@ -619,7 +585,7 @@ __device__ __forceinline__ void epi_pre4(const GemmArgs& p, int tile_a, int tile
 
 template <int MODE, bool SWAP>
 __device__ __forceinline__ void epi_fin4(const GemmArgs& p, int tile_a, int tile_b, int u, const float (&acc)[4],
-                                         const EpiPre4& q, int qslot) {
+                                         const EpiPre4& q, int qslot, float (&yv)[4]) {
   int tok, f, st;
   unit_coords<SWAP>(tile_a, tile_b, p.bn, u, tok, f, st);
   if constexpr (MODE == EPI_F32) {
@@ -627,6 +593,7 @@ __device__ __forceinline__ void epi_fin4(const GemmArgs& p, int tile_a, int tile
     for (int j = 0; j < 4; ++j) {
       const int tj = tok + (st ? 0 : j), fj = f + (st ? j : 0);
       if (tj < p.m_tok && fj < p.n_feat) p.out_f32[(size_t)tj * p.ldo + fj] = acc[j];
+      yv[j] = acc[j];
     }
     return;
   }
@@ -642,6 +609,7 @@ __device__ __forceinline__ void epi_fin4(const GemmArgs& p, int tile_a, int tile
     } else {
       val[j] = f16_sat(acc[j]);
     }
+    yv[j] = __half2float(val[j]);
   }
   // destination of the 4 values: contiguous when they run along features
   __half* dst = nullptr;
@@ -688,268 +656,6 @@ __device__ __forceinline__ void epi_fin4(const GemmArgs& p, int tile_a, int tile
   }
 }
 
-__device__ __forceinline__ void st_dsmem_f32(uint32_t addr, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
-
-// Cooperative LayerNorm of the B operand across the split-K cluster. The CTA
-// holds its K slice [kb0*64, (kb0+nkb)*64) of bn rows as swizzled tiles at
-// `bln`; the S CTAs of the cluster together hold the whole rows. Two exchange
-// rounds (row sums, then sums of squared deviations from the mean), each a
-// per-CTA partial written into every peer's `red` slot [rank][row] over DSMEM
-// and summed in rank order after a cluster barrier (deterministic), give the
-// reference's two-pass statistics (tensor.py:153-160: mean; c = x - mean;
-// var = mean(c*c); c * (1/sqrt(var + 1e-5)) * g + b); the CTA then normalises
-// its slice in place (f16, rows past m_tok zero). Cluster-barrier protocol on
-// entry: with `pending_arrive` the caller has already arrived once (push
-// reduction); on exit with `rearm` one arrive is left pending for the caller.
-__device__ __forceinline__ void ln_coop_build(const GemmArgs& p, int tile_b, int nkb, uint8_t* bln, float* sc,
-                                              bool pending_arrive, bool rearm) {
-  const int bn = p.bn, S = p.splits, tid = threadIdx.x;
-  const float H = (float)p.ln_H;
-  float* red0 = sc;                   // [S][bn]
-  float* red1 = red0 + S * bn;        // [S][bn]
-  float* seg = red1 + S * bn;         // [bn][nsr]
-  float* mean_s = seg + bn * ((nkb * 8 + 3) / 4);  // [bn]
-  float* inv_s = mean_s + bn;         // [bn]
-  const float* g_s = inv_s + bn;      // [nkb*64] gamma of the slice (staged by the caller)
-  const float* b_s = g_s + nkb * kBK;  // [nkb*64]
-  const uint32_t rank = S > 1 ? cluster_ctarank() : 0u;
-  const int C = nkb * 8;  // 16-byte chunks of one row in this slice
-  auto chunk_addr = [&](int r, int c) {
-    return bln + (size_t)(c >> 3) * bn * 128 + r * 128 + ((((c & 7) ^ (r & 7))) * 16);
-  };
-  // per-(row, segment) partials over fixed 4-chunk (32-feature) segments, then
-  // the per-row total in segment order (independent of bn: batch-invariant),
-  // then one write per peer
-  const int nsr = (C + 3) / 4;
-  auto round = [&](float* red, bool second) {
-    for (int idx = tid; idx < bn * nsr; idx += 128) {
-      const int r = idx / nsr, sg = idx - r * nsr;
-      const float m = second ? mean_s[r] : 0.0f;
-      float acc = 0.0f;
-      for (int c = 4 * sg; c < min(C, 4 * sg + 4); ++c) {
-        float xv[8];
-        unpack8(*reinterpret_cast<const uint4*>(chunk_addr(r, c)), xv);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          if (second) {
-            const float d = __fsub_rn(xv[e], m);
-            acc = __fadd_rn(acc, __fmul_rn(d, d));
-          } else {
-            acc = __fadd_rn(acc, xv[e]);
-          }
-        }
-      }
-      seg[idx] = acc;
-    }
-    __syncthreads();
-    for (int r = tid; r < bn; r += 128) {
-      float tot = 0.0f;
-      for (int sg = 0; sg < nsr; ++sg) tot = __fadd_rn(tot, seg[r * nsr + sg]);
-      if (S > 1) {
-        const uint32_t a = smem_u32(red + (int)rank * bn + r);
-        for (int pr = 0; pr < S; ++pr) st_dsmem_f32(dsmem_addr(a, (uint32_t)pr), tot);
-      } else {
-        red[r] = tot;
-      }
-    }
-    __syncthreads();
-  };
-  if (S > 1) {
-    if (!pending_arrive) cluster_arrive_relaxed();
-    cluster_wait();  // every peer is running before its smem is written
-  }
-  round(red0, false);
-  if (S > 1) {
-    cluster_arrive();
-    cluster_wait();
-  }
-  for (int r = tid; r < bn; r += 128) {
-    float s = 0.0f;
-    for (int pr = 0; pr < S; ++pr) s = __fadd_rn(s, red0[pr * bn + r]);
-    mean_s[r] = __fdiv_rn(s, H);
-  }
-  __syncthreads();
-  round(red1, true);
-  if (S > 1) {
-    cluster_arrive();
-    cluster_wait();
-  }
-  for (int r = tid; r < bn; r += 128) {
-    float s = 0.0f;
-    for (int pr = 0; pr < S; ++pr) s = __fadd_rn(s, red1[pr * bn + r]);
-    inv_s[r] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(s, H), 1e-5f)));
-  }
-  __syncthreads();
-  for (int idx = tid; idx < bn * C; idx += 128) {
-    const int r = idx / C, c = idx - r * C;
-    uint8_t* a = chunk_addr(r, c);
-    float xv[8], y[8];
-    unpack8(*reinterpret_cast<const uint4*>(a), xv);
-    const bool valid = tile_b * bn + r < p.m_tok;
-    const float m = mean_s[r], iv = inv_s[r];
-#pragma unroll
-    for (int e = 0; e < 8; ++e)
-      y[e] = valid ? __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[e], m), iv), g_s[c * 8 + e]), b_s[c * 8 + e]) : 0.0f;
-    *reinterpret_cast<uint4*>(a) = pack8(y);
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  if (S > 1 && rearm) cluster_arrive_relaxed();
-  __syncthreads();
-}
-
-// Scratch the row-LN epilogue needs in the drained ring: the parked partial
-// tile [bn][128] f32, the finished values [bn/2][128] f32, exchange slots
-// [2][TA][bn/2], warp partials [2][4][bn/2], mean / inv [bn/2].
-__host__ __device__ inline size_t gemm_rowln_scratch_bytes(int bn, int tiles_a) {
-  const int bh = bn / 2;
-  return (size_t)kTileA * bn * 4 + (size_t)kTileA * bh * 4 + (size_t)(2 * tiles_a * bh + 10 * bh) * 4;
-}
-
-// Row-LN epilogue (see GemmArgs::row_ln). The cluster is the whole grid: CTA
-// (x, z) holds the f32 partial of features [128x, 128x+128) over K half z.
-// CTA (x, z) finalises tokens [z*bn/2, (z+1)*bn/2): acc = p0 + p1 (split
-// order), v = q16(x + q16(acc + b)) (model.py:478-482 / 491-494, bit-identical
-// to the other epilogues), then the LayerNorm of each token row over the TA
-// CTAs that share z (tensor.py:153-160 two-pass form: per-CTA column sums ->
-// every peer over DSMEM -> summed in CTA order after a cluster barrier; then the
-// same for the squared deviations). Deterministic; per-token, so batch-invariant.
-// Loops are kept rolled: the executed path stays short for the i-cache.
-__device__ __noinline__ void gemm_rowln_epilogue(const GemmArgs& p, uint32_t trow, uint8_t* smem) {
-  const int TA = gridDim.x, x = blockIdx.x, z = blockIdx.z;
-  const int bn = p.bn, bh = bn / 2, t0 = z * bh;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int f = x * kTileA + tid;
-  const bool fok = f < p.n_feat;
-  const float H = (float)p.n_feat;
-  float* part = reinterpret_cast<float*>(smem);  // [bn][128]
-  float* vals = part + kTileA * bn;              // [bh][128]
-  float* red = vals + kTileA * bh;               // [2][TA][bh]
-  float* wsum = red + 2 * TA * bh;               // [2][4][bh]
-  float* mean = wsum + 8 * bh;                   // [bh]
-  float* inv = mean + bh;                        // [bh]
-  for (int c = 0; c < bn; c += 16) {
-    float v[16];
-    tmem_ld16(trow + (uint32_t)c, v);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) part[(c + j) * kTileA + tid] = v[j];
-  }
-  const float bias = fok ? p.bias[f] : 0.0f;
-  cluster_arrive();
-  cluster_wait();  // every partial tile parked
-  const uint32_t loc = smem_u32(part) + (uint32_t)((t0 * kTileA + tid) * 4);
-  const uint32_t a0 = dsmem_addr(loc, (uint32_t)x), a1 = dsmem_addr(loc, (uint32_t)(x + TA));
-#pragma unroll 4
-  for (int t = 0; t < bh; ++t) {
-    const int tok = t0 + t;
-    const float p0 = ld_dsmem_f32(a0 + (uint32_t)(t * kTileA * 4));
-    const float p1 = ld_dsmem_f32(a1 + (uint32_t)(t * kTileA * 4));
-    const float xo = (fok && tok < p.m_tok) ? __half2float(p.resid[(size_t)tok * p.ldr + f]) : 0.0f;
-    const float acc = __fadd_rn(__fadd_rn(0.0f, p0), p1);
-    vals[t * kTileA + tid] = (fok && tok < p.m_tok) ? q16(__fadd_rn(xo, q16(__fadd_rn(acc, bias)))) : 0.0f;
-  }
-  for (int rnd = 0; rnd < 2; ++rnd) {
-    float* w = wsum + rnd * 4 * bh;
-    float* rr = red + rnd * TA * bh;
-    for (int t = 0; t < bh; ++t) {
-      const float v = vals[t * kTileA + tid];
-      float q = v;
-      if (rnd == 1) {
-        const float d = fok ? __fsub_rn(v, mean[t]) : 0.0f;
-        q = __fmul_rn(d, d);
-      }
-      q = warp_sum(q);
-      if (lane == 0) w[warp * bh + t] = q;
-    }
-    __syncthreads();
-    if (tid < bh) {
-      const float tot = __fadd_rn(__fadd_rn(__fadd_rn(w[tid], w[bh + tid]), w[2 * bh + tid]), w[3 * bh + tid]);
-      const uint32_t ad = smem_u32(rr + x * bh + tid);
-      for (int xx = 0; xx < TA; ++xx) st_dsmem_f32(dsmem_addr(ad, (uint32_t)(xx + TA * z)), tot);
-    }
-    cluster_arrive();
-    cluster_wait();
-    if (tid < bh) {
-      float s = 0.0f;
-      for (int xx = 0; xx < TA; ++xx) s = __fadd_rn(s, rr[xx * bh + tid]);
-      if (rnd == 0)
-        mean[tid] = __fdiv_rn(s, H);
-      else
-        inv[tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(s, H), 1e-5f)));
-    }
-    __syncthreads();
-  }
-  if (fok) {
-    const float gam = p.lnf_g[f], bet = p.lnf_b[f];
-    for (int t = 0; t < bh; ++t) {
-      const int tok = t0 + t;
-      if (tok >= p.m_tok) break;
-      const float v = vals[t * kTileA + tid];
-      p.out[(size_t)tok * p.ldo + f] = __float2half_rn(v);
-      p.lnf_h[(size_t)tok * p.lnf_ldh + f] =
-          f16_sat(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v, mean[t]), inv[t]), gam), bet));
-    }
-  }
-}
-
-// LayerNorm of the rows this CTA completes (RED_PUSHLN). [u_lo, u_hi): the
-// CTA's reduction units (unit u = token column u / 32, features 4 * (u % 32)
-// .. +3 of the tile). Release: every thread's x stores, a CTA barrier, then one
-// acq_rel fence; each touched token gets one atomicAdd (its own thread) of the
-// features this CTA stored; the add that completes n_feat makes this CTA the
-// row's normaliser (acquire fence, L2 reads of the row). Arithmetic: the
-// stand-alone LN kernel's (ln_row_apply), so h is bit-identical to it.
-template <int NT>
-__device__ __forceinline__ void gemm_ln_tail(const GemmArgs& p, int tile_a, int tile_b, int u_lo, int u_hi) {
-  __shared__ int s_rows[64];
-  __shared__ int s_nrows;
-  if (threadIdx.x == 0) s_nrows = 0;
-  __syncthreads();  // every thread's x stores happen-before the fences below
-  const int c_lo = u_lo / 32, c_hi = u_hi > u_lo ? (u_hi - 1) / 32 : c_lo - 1;
-  for (int c = c_lo + (int)threadIdx.x; c <= c_hi; c += NT) {
-    const int tok = tile_b * p.bn + c;
-    if (tok >= p.m_tok) continue;
-    int n = 0;
-    for (int u = max(u_lo, c * 32); u < min(u_hi, c * 32 + 32); ++u)
-      n += max(0, min(4, p.n_feat - (tile_a * kTileA + (u % 32) * 4)));
-    if (n == 0) continue;
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // release (cumulative over the barrier)
-    const int prev = atomicAdd(p.lnf_cnt + tok, n);
-    if (prev + n == p.n_feat) s_rows[atomicAdd(&s_nrows, 1)] = tok;
-  }
-  __syncthreads();
-  const int nl = s_nrows;
-  if (nl == 0) return;
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NC = 4;  // H <= 1024; chunks past H are skipped (same sums as NC = ceil(H/256))
-  float4 gv[NC * 2], bv[NC * 2];
-  ln_load_gb<NC>(p.n_feat, p.lnf_g, p.lnf_b, lane, gv, bv);
-  for (int i = warp; i < nl; i += NT / 32) {
-    const int tok = s_rows[i];
-    const __half* xr = p.out + (size_t)tok * p.ldo;
-    uint4 raw[NC];
-#pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      const int c = (lane + 32 * j) * 8;
-      if (c < p.n_feat) raw[j] = __ldcg(reinterpret_cast<const uint4*>(xr + c));
-    }
-    float xv[NC * 8];
-#pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      if ((lane + 32 * j) * 8 < p.n_feat) {
-        unpack8(raw[j], &xv[8 * j]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) xv[8 * j + e] = 0.0f;
-      }
-    }
-    ln_row_apply<NC>(xv, p.n_feat, gv, bv, p.lnf_h + (size_t)tok * p.lnf_ldh, lane);
-    if (lane == 0) p.lnf_cnt[tok] = 0;
-  }
-}
-
 // Reduction / epilogue path of a launch (template parameter, so every
 // instantiation carries only the code it executes: decode kernels are
 // i-cache-bound when they carry all paths)
@@ -957,17 +663,15 @@ enum GemmRed : int {
   RED_ONE = 0,    // splits == 1 (full-K tile; non-swap staged epilogue or per-chunk stores)
   RED_PUSH = 1,   // split-K cluster, push form (swap, bn <= 128)
   RED_PULL = 2,   // split-K cluster, pull form
-  RED_ROWLN = 3,  // whole-row cluster + fused LayerNorm (EPI_BIAS_RESID, swap)
-  RED_PUSHLN = 4,  // push split-K + LayerNorm of completed rows by their last CTA (EPI_BIAS_RESID)
 };
-// LayerNorm of the B operand built in-kernel: 0 none, 1 full-row staging
-// (ln_build_b), 2 cluster-cooperative (ln_coop_build)
+// LNV (operand LayerNorm): 0 none, 1 the B operand is q16(LN(x)) built in smem
+// from the raw rows and the producer's row-statistics partials (ln_stats_*).
 // threads per CTA: the prefill (non-swap, full-K) tiles run their staged
-// epilogue with eight warps; so does the decode push reduction (one pass over
-// the CTA's units instead of two at batch 32 with 6 or fewer splits)
+// epilogue with eight warps; so do the decode push reduction (one pass over
+// the CTA's units at batch 32) and the decode full-K swap epilogues
 __host__ __device__ constexpr int gemm_threads(int mode, bool swap, int red, int lnv = 0) {
-  return ((!swap && red == RED_ONE && mode != EPI_LOGITS) || (swap && (red == RED_PUSH || red == RED_PUSHLN) && lnv <= 1) ||
-          (swap && red == RED_ONE && lnv == 0 &&
+  return ((!swap && red == RED_ONE && mode != EPI_LOGITS) || (swap && red == RED_PUSH) ||
+          (swap && red == RED_ONE &&
            (mode == EPI_QKV || mode == EPI_BIAS || mode == EPI_BIAS_GELU || mode == EPI_BIAS_RESID)))
              ? 256
              : 128;
@@ -983,14 +687,10 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
   const int bn = p.bn, stages = p.stages;
   const int stage_bytes = gemm_stage_bytes(bn);
   constexpr bool ln_mode = SWAP && LNV != 0;
-  uint8_t* bln = smem + gemm_ring_bytes(bn, stages, p.splits, SWAP);
-  constexpr bool coop = ln_mode && LNV == 2;
-  uint8_t* recv = bln + (ln_mode ? (coop ? gemm_ln_coop_bytes(bn, p.kb_per_split, p.splits)
-                                         : gemm_ln_bytes(bn, p.kb_per_split, p.k_blocks))
-                                 : 0);
-  float* ln_sc = reinterpret_cast<float*>(bln + (size_t)p.kb_per_split * bn * kBK * 2);  // coop scratch
-  uint8_t* stg = bln + (size_t)p.kb_per_split * bn * kBK * 2;  // LN source rows (ln_mode)
-  constexpr bool push = RED == RED_PUSH || RED == RED_PUSHLN;
+  constexpr int NTH = gemm_threads(MODE, SWAP, RED, LNV);
+  float* s_mi = reinterpret_cast<float*>(smem + gemm_ring_bytes(bn, stages, p.splits, SWAP));  // ln_mode
+  uint8_t* recv = reinterpret_cast<uint8_t*>(s_mi) + (ln_mode ? gemm_ln_bytes(bn) : 0);
+  constexpr bool push = RED == RED_PUSH;
   uint64_t* bars = reinterpret_cast<uint64_t*>(recv + gemm_recv_bytes(bn, p.splits, SWAP));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 3);
   __shared__ unsigned long long red[64];
@@ -1037,7 +737,7 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
   // ---------------- TMA producer. Weights do not depend on the previous
   // kernel, so in decode (SWAP) mode the first ring's worth of weight tiles is
   // requested before waiting on the programmatic launch dependency.
-  const uint32_t tx = ln_mode ? (uint32_t)kABytes : (uint32_t)stage_bytes;
+  const uint32_t tx = (uint32_t)stage_bytes;
   const int pre = SWAP ? min(stages, nkb) : 0;
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < pre; ++i) {
@@ -1047,45 +747,8 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
     }
   }
   if (warp == 3 && lane == 0) l2_prefetch_share(p.l2pf, p.l2pf_bytes);
-  if constexpr (coop) {
-    // gamma / beta of this CTA's K slice are weights: staged before the wait
-    float* g_s = ln_sc + 2 * p.splits * bn + gemm_ln_coop_seg(bn, p.kb_per_split) + 2 * bn;
-    for (int i = threadIdx.x; i < nkb * kBK; i += 128) {
-      const int f = kb0 * kBK + i;
-      g_s[i] = f < p.ln_H ? p.ln_g[f] : 0.0f;
-      g_s[nkb * kBK + i] = f < p.ln_H ? p.ln_b[f] : 0.0f;
-    }
-    pdl_wait();
-    if (warp == 0 && lane == 0) {
-      mbar_expect_tx(ln_bar, (uint32_t)(nkb * bn * kBK * 2));
-      for (int kb = 0; kb < nkb; ++kb)
-        tma_load_2d(smem_u32(bln + (size_t)kb * bn * kBK * 2), &tmB, (kb0 + kb) * kBK, tile_b * bn, ln_bar);
-    }
-    mbar_wait(ln_bar, 0);
-    __syncthreads();  // g_s / b_s visible
-    ln_coop_build(p, tile_b, nkb, bln, ln_sc, push, push);
-  } else if constexpr (ln_mode) {  // stage the source rows by TMA, then every thread builds the normalised B tiles
-    // gamma / beta of this CTA's K slice are weights: staged before the wait
-    float* gsl = reinterpret_cast<float*>(stg + (size_t)p.k_blocks * bn * kBK * 2);
-    float* bsl = gsl + p.kb_per_split * kBK;
-    for (int i = threadIdx.x; i < nkb * kBK; i += gemm_threads(MODE, SWAP, RED, LNV)) {
-      const int f = kb0 * kBK + i;
-      gsl[i] = f < p.ln_H ? p.ln_g[f] : 0.0f;
-      bsl[i] = f < p.ln_H ? p.ln_b[f] : 0.0f;
-    }
-    pdl_wait();
-    if (warp == 0 && lane == 0) {
-      mbar_expect_tx(ln_bar, (uint32_t)(p.k_blocks * bn * kBK * 2));
-      for (int kb = 0; kb < p.k_blocks; ++kb)
-        tma_load_2d(smem_u32(stg + (size_t)kb * bn * kBK * 2), &tmB, kb * kBK, tile_b * bn, ln_bar);
-    }
-    mbar_wait(ln_bar, 0);
-    __syncthreads();  // gsl / bsl visible
-    ln_build_b<gemm_threads(MODE, SWAP, RED, LNV)>(p, tile_b, kb0, nkb, bln, stg, gsl, bsl);
-    __syncthreads();
-  }
   if (warp == 0 && lane == 0) {
-    if (!ln_mode) pdl_wait();
+    pdl_wait();
     tr.mark(p.trace, 1);
     for (int i = 0; i < nkb; ++i) {
       const int s = i % stages;
@@ -1097,7 +760,7 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
         mbar_expect_tx(full0 + 8 * s, tx);
         tma_load_2d(sa, &tmA, (kb0 + i) * kBK, tile_a * kTileA, full0 + 8 * s);
       }
-      if (!ln_mode) tma_load_2d(sb, &tmB, (kb0 + i) * kBK, tile_b * bn, full0 + 8 * s);
+      tma_load_2d(sb, &tmB, (kb0 + i) * kBK, tile_b * bn, full0 + 8 * s);
     }
   } else if (warp == 1) {
     // ---------------- MMA issue: the whole warp walks the k-blocks (warp-
@@ -1113,7 +776,7 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
       const uint64_t da = umma_desc_sw128(sa);
-      const uint64_t db = umma_desc_sw128(ln_mode ? smem_u32(bln + (size_t)i * bn * kBK * 2) : sa + kABytes);
+      const uint64_t db = umma_desc_sw128(sa + kABytes);
       if (elect_lane0()) {
 #pragma unroll
         for (int k = 0; k < kBK / 16; ++k) {
@@ -1133,16 +796,18 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
   if (p.late_trigger) pdl_trigger();
   // cache slot of token t = 0 (EPI_QKV): one load per thread, overlapping the MMA
   const int qslot = (MODE == EPI_QKV && p.qbase_dev != nullptr) ? *p.qbase_dev : 0;
+  // folded LayerNorm: the rows' (mean, inv), merged by the warps that neither
+  // load nor issue (they overlap the operand TMA and the MMAs)
+  if constexpr (ln_mode) ln_stats_rows(p, tile_b, s_mi, 64, NTH - 64);
   mbar_wait(done_bar, 0);
   tc_fence_after();
+  if constexpr (ln_mode) __syncthreads();
   if (threadIdx.x == 0) tr.mark(p.trace, 2);
   const int row = warp * 32 + lane;  // TMEM lane == row of the A tile
   const int ra = tile_a * kTileA + row;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   float v[16];
-  if constexpr (RED == RED_ROWLN) {
-    if constexpr (MODE == EPI_BIAS_RESID && SWAP) gemm_rowln_epilogue(p, trow, smem);
-  } else if constexpr (RED == RED_ONE && !SWAP) {
+  if constexpr (RED == RED_ONE && !SWAP) {
     if (MODE != EPI_LOGITS || p.keys == nullptr) {
       epi_tile_nonswap<MODE, false, gemm_threads(MODE, SWAP, RED)>(p, tile_a, tile_b,
                                                                    tmem + (uint32_t)((warp & 3) * 32 << 16), smem);
@@ -1157,14 +822,20 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
       constexpr int NT = gemm_threads(MODE, SWAP, RED, LNV);
       const uint32_t tq = tmem + ((uint32_t)((warp & 3) * 32) << 16);
       epi_swap_one<MODE>(p, tile_a * kTileA + (warp & 3) * 32 + lane, tile_b * bn, bn, tq, NT == 256 ? (warp >> 2) * 16 : 0,
-                         NT == 256 ? 32 : 16);
+                         NT == 256 ? 32 : 16, ln_mode ? s_mi : nullptr);
     } else {
+      const float lc = (ln_mode && ra < p.n_feat) ? p.ln_c[ra] : 0.0f;
+      const float ld = (ln_mode && ra < p.n_feat) ? p.ln_d[ra] : 0.0f;
       for (int c = 0; c < bn; c += 16) {
         tmem_ld16(trow + (uint32_t)c, v);
+        if constexpr (ln_mode) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = ln_fold(v[j], s_mi[c + j], s_mi[bn + c + j], lc, ld);
+        }
         epi_chunk<MODE, SWAP>(p, ra, tile_b * bn + c, v, reinterpret_cast<unsigned long long*>(smem));
       }
     }
-  } else if constexpr (RED == RED_PUSH || RED == RED_PUSHLN) {
+  } else if constexpr (RED == RED_PUSH) {
     // Split-K across the CTAs of one cluster, push form. Each CTA parks its f32
     // partial tile ([column][128 rows], in the drained ring), then one thread
     // bulk-copies the slice owned by every peer r (units [r*per, r*per+per),
@@ -1191,8 +862,8 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
     const uint32_t rank = cluster_ctarank();
     const int S = p.splits;
     const int U = (kTileA / 4) * bn;
-    const int per = (U + S - 1) / S;
-    const int u_lo = (int)rank * per, u_hi = min(U, u_lo + per);
+    const int per = gemm_push_per(bn, S);  // whole token columns per CTA
+    const int u_lo = min(U, (int)rank * per), u_hi = min(U, u_lo + per);
     cluster_wait();  // every peer's recv_bar is initialised
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1213,8 +884,8 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
     // peer slices are in flight
     EpiPre4 pre, pre2;
     int u = u_lo + (int)threadIdx.x;
-    if (u < u_hi) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
-    if (u + NT < u_hi) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u + NT, pre2);
+    if (u < u_hi) epi_pre4<MODE, SWAP, ln_mode>(p, tile_a, tile_b, u, pre);
+    if (u + NT < u_hi) epi_pre4<MODE, SWAP, ln_mode>(p, tile_a, tile_b, u + NT, pre2);
     mbar_wait(recv_bar, 0);
     if (threadIdx.x == 0) tr.mark(p.trace, 4);
     const float4* own = reinterpret_cast<const float4*>(part);
@@ -1222,7 +893,7 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
     for (int it = 0; u < u_hi; u += NT, ++it) {
       const bool first = it == 0;
       if (it == 1) pre = pre2;
-      if (it >= 2) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
+      if (it >= 2) epi_pre4<MODE, SWAP, ln_mode>(p, tile_a, tile_b, u, pre);
       float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
       for (int sp = 0; sp < 16; ++sp)
@@ -1233,14 +904,45 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
           acc[2] = __fadd_rn(acc[2], pv.z);
           acc[3] = __fadd_rn(acc[3], pv.w);
         }
+      if constexpr (ln_mode) {  // SWAP: the unit's 4 values share one token
+        const int tl = u / 32;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = ln_fold(acc[j], s_mi[tl], s_mi[bn + tl], pre.c[j], pre.d[j]);
+      }
       if (threadIdx.x == 0 && first) tr.mark(p.trace, 5);
-      epi_fin4<MODE, SWAP>(p, tile_a, tile_b, u, acc, pre, qslot);
+      float yv[4];
+      epi_fin4<MODE, SWAP>(p, tile_a, tile_b, u, acc, pre, qslot, yv);
+      if constexpr (MODE == EPI_BIAS_RESID && SWAP) {
+        // row statistics of the new residual values over this tile's features
+        // for the LayerNorm fused into the next GEMM (ln_stats_rows): the 32
+        // lanes of this warp hold the tile's 128 features of one token
+        // (u_lo is a multiple of 32); fixed xor tree, then the two-pass M2
+        if (p.stats_out != nullptr) {
+          int tok, f, st;
+          unit_coords<SWAP>(tile_a, tile_b, bn, u, tok, f, st);
+          const int nf = min(kTileA, p.n_feat - tile_a * kTileA);
+          float s = 0.0f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) s = __fadd_rn(s, f + j < p.n_feat ? yv[j] : 0.0f);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+          const float mean = __fdiv_rn(s, (float)nf);
+          float m2 = 0.0f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float d = f + j < p.n_feat ? __fsub_rn(yv[j], mean) : 0.0f;
+            m2 = __fadd_rn(m2, __fmul_rn(d, d));
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) m2 = __fadd_rn(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+          if (lane == 0 && tok < p.m_tok) p.stats_out[(size_t)tile_a * p.stats_ld + tok] = make_float2(mean, m2);
+        }
+      }
     }
     if (threadIdx.x == 0) {
       tr.mark(p.trace, 6);
       bulk_wait_read_all();  // outgoing slices read before this smem is released
     }
-    if constexpr (RED == RED_PUSHLN && MODE == EPI_BIAS_RESID) gemm_ln_tail<NT>(p, tile_a, tile_b, u_lo, u_hi);
   } else {
     static_assert(RED == RED_PULL, "reduction path");
     // Split-K across the CTAs of one thread-block cluster (grid.z == cluster.z
@@ -1267,7 +969,7 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
     int u = u_lo + (int)threadIdx.x;
     if (threadIdx.x == 0) tr.mark(p.trace, 3);
     cluster_arrive();  // release: this CTA's partial tile is complete
-    if (u < u_hi) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
+    if (u < u_hi) epi_pre4<MODE, SWAP, ln_mode>(p, tile_a, tile_b, u, pre);
     cluster_wait();
     if (threadIdx.x == 0) tr.mark(p.trace, 4);
     const uint32_t local = smem_u32(part);
@@ -1277,7 +979,7 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
     int it = 0;
     if (n_units == 0) cluster_arrive_any();
     for (bool first = true; u < u_hi; u += 128, first = false, ++it) {
-      if (!first) epi_pre4<MODE, SWAP>(p, tile_a, tile_b, u, pre);
+      if (!first) epi_pre4<MODE, SWAP, ln_mode>(p, tile_a, tile_b, u, pre);
       // all S loads in flight, then the sum in split order (deterministic)
       float4 pv[16];
 #pragma unroll
@@ -1292,128 +994,18 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
           acc[2] = __fadd_rn(acc[2], pv[sp].z);
           acc[3] = __fadd_rn(acc[3], pv[sp].w);
         }
+      if constexpr (ln_mode) {
+        const int tl = u / 32;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = ln_fold(acc[j], s_mi[tl], s_mi[bn + tl], pre.c[j], pre.d[j]);
+      }
       if (threadIdx.x == 0 && first) tr.mark(p.trace, 5);
       if (it == n_units - 1) cluster_arrive_any();
-      epi_fin4<MODE, SWAP>(p, tile_a, tile_b, u, acc, pre, qslot);
+      float yv[4];
+      epi_fin4<MODE, SWAP>(p, tile_a, tile_b, u, acc, pre, qslot, yv);
     }
     if (threadIdx.x == 0) tr.mark(p.trace, 6);
     cluster_wait_any();  // partial tiles stay alive until every CTA has read them
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    tr.mark(p.trace, 7);
-    tr.flush(p.trace);
-  }
-  if (warp == 2) tmem_dealloc(tmem, ncols);
-}
-
-// ---------------------------------------------------------------- persistent prefill GEMM
-// Non-swap (token-major) GEMM for prefill-sized M: one CTA per SM loops over
-// output tiles; warp 0 streams A/B k-blocks through a `stages`-deep TMA ring
-// across tile boundaries, warp 1 issues tcgen05.mma into one of TWO TMEM
-// accumulators, warps 2-5 run the staged epilogue of the previous tile from the
-// other accumulator (released to the MMA warp as soon as its TMEM reads are
-// done). Tiles are visited token-tile-fastest so the CTAs running at the same
-// time share the weight tile (L2 reuse).
-constexpr int kPfThreadsGemm = 192;
-__host__ __device__ inline size_t gemm_pf_smem_bytes(int bn, int stages, bool f32out) {
-  return 1024 + (size_t)stages * gemm_stage_bytes(bn) + (size_t)kTileA * (bn * (f32out ? 4 : 2) + 16) +
-         (size_t)(2 * stages + 4) * 8 + 16;
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(kPfThreadsGemm, 1)
-    gemm_pf_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const GemmArgs p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  constexpr bool F32OUT = MODE == EPI_F32;
-  const int bn = p.bn, stages = p.stages;
-  const int stage_bytes = gemm_stage_bytes(bn);
-  uint8_t* out_stage = smem + (size_t)stages * stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(out_stage + (size_t)kTileA * (bn * (F32OUT ? 4 : 2) + 16));
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 4);
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + stages);
-  const uint32_t accf0 = smem_u32(bars + 2 * stages), acce0 = smem_u32(bars + 2 * stages + 2);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles_a = (p.m_tok + kTileA - 1) / kTileA, tiles_b = (p.n_feat + bn - 1) / bn;
-  const int n_tiles = tiles_a * tiles_b, nkb = p.k_blocks;
-  const uint32_t ncols = 2 * bn <= 32 ? 32u : (2 * bn <= 64 ? 64u : (2 * bn <= 128 ? 128u : (2 * bn <= 256 ? 256u : 512u)));
-  TF_TRACE_INIT(tr);
-  if (threadIdx.x == 0) tr.mark(p.trace, 0);
-  if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(accf0 + 8 * b, 1);
-      mbar_init(acce0 + 8 * b, 1);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc(smem_u32(tmem_slot), ncols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_trigger();
-  pdl_wait();
-  if (threadIdx.x == 0) tr.mark(p.trace, 1);
-  if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer, continuous over tiles
-      int it = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int ta = t % tiles_a, tb = t / tiles_a;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % stages;
-          const uint32_t ph = (uint32_t)(it / stages) & 1u;
-          mbar_wait(empty0 + 8 * s, ph ^ 1u);
-          const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
-          mbar_expect_tx(full0 + 8 * s, (uint32_t)stage_bytes);
-          tma_load_2d(sa, &tmA, kb * kBK, ta * kTileA, full0 + 8 * s);
-          tma_load_2d(sa + kABytes, &tmB, kb * kBK, tb * bn, full0 + 8 * s);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer, two TMEM accumulators
-      const uint32_t idesc = idesc_f16_m128((uint32_t)bn);
-      int it = 0, tc = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tc) {
-        const int b = tc & 1, use = tc >> 1;
-        mbar_wait(acce0 + 8 * b, ((uint32_t)use & 1u) ^ 1u);
-        tc_fence_after();
-        const uint32_t acc = tmem + (uint32_t)(b * bn);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % stages;
-          const uint32_t ph = (uint32_t)(it / stages) & 1u;
-          mbar_wait(full0 + 8 * s, ph);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + (size_t)s * stage_bytes);
-          const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + kABytes);
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) tc_mma_f16(acc, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
-          tc_commit(empty0 + 8 * s);
-        }
-        tc_commit(accf0 + 8 * b);
-      }
-    }
-  } else {  // ---- epilogue warps 2..5 (TMEM lane quadrant = warp % 4)
-    const int q = warp & 3, row = q * 32 + lane;
-    int tc = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tc) {
-      const int ta = t % tiles_a, tb = t / tiles_a;
-      const int b = tc & 1, use = tc >> 1;
-      mbar_wait(accf0 + 8 * b, (uint32_t)use & 1u);
-      tc_fence_after();
-      const uint32_t trow = tmem + (uint32_t)(b * bn) + ((uint32_t)(q * 32) << 16);
-      epi_tile_nonswap<MODE, true>(p, ta, tb, trow, out_stage, row, acce0 + 8 * b);
-    }
   }
   tc_fence_before();
   __syncthreads();

@@ -21,7 +21,8 @@ struct EmbedArgs {
   const int* pos;            // [n_tok] positions, or null -> (*len_dev - pads[row])
   const int* len_dev;
   const int* pads;
-  const int* type_ids;       // optional [n_tok]
+  const int* type_ids;       // optional [n_tok] (null: every row uses type_const)
+  int type_const;            // type row of rows without type_ids (generated tokens)
   const __half* tok_emb;     // [V, ldw]
   const __half* pos_emb;     // [P, ldw]
   const __half* type_emb;    // optional [n_types, ldw]
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(256) embed_ln_vec_kernel(const EmbedArgs a) {
   const int p = (a.pos != nullptr) ? a.pos[row] : (*a.len_dev - a.pads[row]);
   const __half* tr = a.tok_emb + (size_t)id * a.ldw;
   const __half* pr = a.pos_emb + (size_t)p * a.ldw;
-  const __half* yr = a.type_emb ? a.type_emb + (size_t)a.type_ids[row] * a.ldw : nullptr;
+  const __half* yr = a.type_emb ? a.type_emb + (size_t)(a.type_ids ? a.type_ids[row] : a.type_const) * a.ldw : nullptr;
   uint4 tv[NC], pv[NC], yv[NC];
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(const EmbedArgs a) {
   const int p = (a.pos != nullptr) ? a.pos[row] : (*a.len_dev - a.pads[row]);
   const __half* tr = a.tok_emb + (size_t)id * a.ldw;
   const __half* pr = a.pos_emb + (size_t)p * a.ldw;
-  const __half* yr = a.type_emb ? a.type_emb + (size_t)a.type_ids[row] * a.ldw : nullptr;
+  const __half* yr = a.type_emb ? a.type_emb + (size_t)(a.type_ids ? a.type_ids[row] : a.type_const) * a.ldw : nullptr;
   __half* xr = a.x + (size_t)row * a.ldx;
   float xv[VPL];
 #pragma unroll
@@ -287,112 +288,6 @@ __global__ void __launch_bounds__(256) layernorm_vec_kernel(const LnArgs a) {
       }
     }
     ln_row_apply<NC>(xv, a.H, gv, bv, a.h + (size_t)row * a.ldh, lane);
-  }
-  if (a.trace) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tr.mark(a.trace, 7);
-      tr.flush(a.trace);
-    }
-  }
-}
-
-// Head reduction of the attention-fused output projection + residual +
-// LayerNorm (decode): one CTA per row b, kResThreads threads, feature n owned by
-// thread n % kResThreads.
-//   o_n   = q16(sum_h part[b][h][n] (head order) + bo[n])     (model.py:478-480)
-//   x_n   = q16(x_n + o_n)                                    (model.py:481)
-//   h     = q16(LN(x))                                        (model.py:484-486)
-// LN: two-pass (mean; var of the deviations) with per-thread sequential
-// partials, warp xor-butterflies and the warps in order (deterministic).
-constexpr int kResThreads = 256;
-struct ResLnArgs {
-  int B, NH, H;
-  const float* part;  // [B][NH][H]
-  const float* bias;  // [H]
-  __half* x;          // [B, ldx] residual stream (in/out)
-  int ldx;
-  const float* g;
-  const float* b;
-  __half* h;  // [B, ldh]
-  int ldh;
-  int trace;
-};
-
-__global__ void __launch_bounds__(kResThreads) resid_heads_ln_kernel(const ResLnArgs a) {
-  constexpr int MAXC = 8;  // H <= 2048
-  __shared__ float red[kResThreads / 32];
-  __shared__ float stat[2];
-  TF_TRACE_INIT(tr);
-  if (threadIdx.x == 0) tr.mark(a.trace, 0);
-  const int row = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  float bias[MAXC], gam[MAXC], bet[MAXC];
-#pragma unroll
-  for (int i = 0; i < MAXC; ++i) {
-    const int n = tid + kResThreads * i;
-    const bool ok = n < a.H;
-    bias[i] = ok ? a.bias[n] : 0.0f;
-    gam[i] = ok ? a.g[n] : 0.0f;
-    bet[i] = ok ? a.b[n] : 0.0f;
-  }
-  pdl_wait();
-  if (threadIdx.x == 0) tr.mark(a.trace, 1);
-  pdl_trigger();
-  const float* pr = a.part + (size_t)row * a.NH * a.H;
-  __half* xr = a.x + (size_t)row * a.ldx;
-  float xv[MAXC];
-  constexpr int MAXH = 16;  // heads <= 16: every partial load issued before the sums
-#pragma unroll
-  for (int i = 0; i < MAXC; ++i) {
-    const int n = tid + kResThreads * i;
-    xv[i] = 0.0f;
-    if (n < a.H) {
-      float pv[MAXH];
-#pragma unroll
-      for (int hh = 0; hh < MAXH; ++hh) pv[hh] = hh < a.NH ? __ldcg(pr + (size_t)hh * a.H + n) : 0.0f;
-      const float xo = __half2float(xr[n]);
-      float acc = 0.0f;
-#pragma unroll
-      for (int hh = 0; hh < MAXH; ++hh)
-        if (hh < a.NH) acc = __fadd_rn(acc, pv[hh]);
-      const float o = q16(__fadd_rn(acc, bias[i]));
-      const __half xn = f16_sat(__fadd_rn(xo, o));
-      xr[n] = xn;
-      xv[i] = __half2float(xn);
-    }
-  }
-  for (int pass = 0; pass < 2; ++pass) {
-    float s = 0.0f;
-    const float m = pass ? stat[0] : 0.0f;
-#pragma unroll
-    for (int i = 0; i < MAXC; ++i)
-      if (tid + kResThreads * i < a.H) {
-        if (pass) {
-          const float d = __fsub_rn(xv[i], m);
-          s = __fadd_rn(s, __fmul_rn(d, d));
-        } else {
-          s = __fadd_rn(s, xv[i]);
-        }
-      }
-    s = warp_sum(s);
-    if (lane == 0) red[warp] = s;
-    __syncthreads();
-    if (tid == 0) {
-      float t = 0.0f;
-      for (int w = 0; w < kResThreads / 32; ++w) t = __fadd_rn(t, red[w]);
-      if (pass)
-        stat[1] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(t, (float)a.H), 1e-5f)));
-      else
-        stat[0] = __fdiv_rn(t, (float)a.H);
-    }
-    __syncthreads();
-  }
-  const float mean = stat[0], inv = stat[1];
-  __half* hr = a.h + (size_t)row * a.ldh;
-#pragma unroll
-  for (int i = 0; i < MAXC; ++i) {
-    const int n = tid + kResThreads * i;
-    if (n < a.H) hr[n] = f16_sat(__fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv[i], mean), inv), gam[i]), bet[i]));
   }
   if (a.trace) {
     __syncthreads();

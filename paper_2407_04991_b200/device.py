@@ -43,6 +43,21 @@ def _f32_vec(v: np.ndarray) -> np.ndarray:
     return round_to(np.asarray(v, dtype=np.float32), DType.F16).astype(np.float32)
 
 
+def _fold_ln(w_t: np.ndarray, k: int, gamma: np.ndarray, beta: np.ndarray):
+    """LayerNorm folded into the following projection (decode path,
+    gemm_tc.cuh ln_fold): W'[n, k] = q16(W[n, k] * gamma[k]) (the f16 x f16
+    product is exact in f32, then one saturating RNE), c[n] = sum_k W'[n, k],
+    d[n] = sum_k beta[k] W[n, k] (fp64 sums rounded to f32), so that
+    LN(x) . W[n] = inv * (x . W'[n] - mean * c[n]) + d[n]."""
+    w = w_t[:, :k].astype(np.float32)
+    wf = round_to(w * gamma[None, :k].astype(np.float32), DType.F16)
+    buf = np.zeros_like(w_t)
+    buf[:, :k] = wf
+    c = wf.astype(np.float64).sum(axis=1).astype(np.float32)
+    d = (w.astype(np.float64) @ beta[:k].astype(np.float64)).astype(np.float32)
+    return buf, c, d
+
+
 class DeviceModel:
     """Packed, device-resident weights + the native ``tf_model`` handle."""
 
@@ -70,22 +85,31 @@ class DeviceModel:
             p = f"layers.{i}."
             wqkv = np.concatenate([f32[p + "attn.wq"], f32[p + "attn.wk"], f32[p + "attn.wv"]], axis=1)
             bqkv = np.concatenate([f32[p + "attn.bq"], f32[p + "attn.bk"], f32[p + "attn.bv"]])
+            g1, be1 = _f32_vec(f32[p + "attn_norm.gamma"]), _f32_vec(f32[p + "attn_norm.beta"])
+            g2, be2 = _f32_vec(f32[p + "ffn_norm.gamma"]), _f32_vec(f32[p + "ffn_norm.beta"])
+            wqkv_t = _f16_kmajor(wqkv, self.ldk_h)
+            w1_t = _f16_kmajor(f32[p + "ffn.w1"], self.ldk_h)
+            wqkv_ln, cqkv, dqkv = _fold_ln(wqkv_t, self.H, g1, be1)
+            w1_ln, c1, d1 = _fold_ln(w1_t, self.H, g2, be2)
             lw = dict(
-                ln1_gamma=up16(_f32_vec(f32[p + "attn_norm.gamma"])),
-                ln1_beta=up16(_f32_vec(f32[p + "attn_norm.beta"])),
-                wqkv_t=up16(_f16_kmajor(wqkv, self.ldk_h)), bqkv=up16(_f32_vec(bqkv)),
+                ln1_gamma=up16(g1), ln1_beta=up16(be1),
+                wqkv_t=up16(wqkv_t), bqkv=up16(_f32_vec(bqkv)),
                 wo_t=up16(_f16_kmajor(f32[p + "attn.wo"], self.ldk_h)), bo=up16(_f32_vec(f32[p + "attn.bo"])),
-                ln2_gamma=up16(_f32_vec(f32[p + "ffn_norm.gamma"])),
-                ln2_beta=up16(_f32_vec(f32[p + "ffn_norm.beta"])),
-                w1_t=up16(_f16_kmajor(f32[p + "ffn.w1"], self.ldk_h)), b1=up16(_f32_vec(f32[p + "ffn.b1"])),
+                ln2_gamma=up16(g2), ln2_beta=up16(be2),
+                w1_t=up16(w1_t), b1=up16(_f32_vec(f32[p + "ffn.b1"])),
                 w2_t=up16(_f16_kmajor(f32[p + "ffn.w2"], self.ldk_f)), b2=up16(_f32_vec(f32[p + "ffn.b2"])),
+                wqkv_ln_t=up16(wqkv_ln), cqkv=up16(cqkv), dqkv=up16(dqkv),
+                w1_ln_t=up16(w1_ln), c1=up16(c1), d1=up16(d1),
             )
             self.layers.append(lw)
             for k, t in lw.items():
                 setattr(layers[i], k, t.data_ptr())
         self.final_gamma = keep(up16(_f32_vec(f32["final_norm.gamma"])))
         self.final_beta = keep(up16(_f32_vec(f32["final_norm.beta"])))
-        self.lm_head_t = keep(up16(_f16_kmajor(f32["lm_head"], self.ldk_h)))
+        lm_t = _f16_kmajor(f32["lm_head"], self.ldk_h)
+        self.lm_head_t = keep(up16(lm_t))
+        lm_ln, c_lm, d_lm = _fold_ln(lm_t, self.H, _f32_vec(f32["final_norm.gamma"]), _f32_vec(f32["final_norm.beta"]))
+        self.lm_head_ln_t, self.c_lm, self.d_lm = keep(up16(lm_ln)), keep(up16(c_lm)), keep(up16(d_lm))
         self._layer_structs = layers
         d = N.ModelDesc()
         d.vocab, d.hidden, d.layers, d.heads = self.V, self.H, self.L, self.NH
@@ -96,6 +120,7 @@ class DeviceModel:
         d.layer = layers
         d.final_gamma, d.final_beta = self.final_gamma.data_ptr(), self.final_beta.data_ptr()
         d.lm_head_t = self.lm_head_t.data_ptr()
+        d.lm_head_ln_t, d.c_lm, d.d_lm = self.lm_head_ln_t.data_ptr(), self.c_lm.data_ptr(), self.d_lm.data_ptr()
         h = C.c_void_p()
         N.check(N.lib().tf_model_create(C.byref(d), C.byref(h)), "tf_model_create")
         self.handle = h
@@ -188,14 +213,17 @@ class Session:
         d.ffn = self.ffn.data_ptr()
         d.logits = self.logits.data_ptr() if logits else None
         # split-KV decode attention scratch: per (row, head, 64-slot chunk) {m, z, o[64]}
+        # and one arrival counter per (row, head)
         chunks = (capacity + 63) // 64
-        # (also the per-head partials of the attention-fused output projection)
-        self.att_ws = torch.empty(max(1, batch * dm.NH * chunks * 66, batch * dm.NH * dm.H), dtype=torch.float32,
-                                  device=dev)
-        # (+ one row-completion counter per token for the last-arriver LayerNorm)
-        self.att_cnt = torch.zeros(batch * dm.NH + batch * max(1, max_tokens), dtype=torch.int32, device=dev)
+        self.att_ws = torch.empty(max(1, batch * dm.NH * chunks * 66), dtype=torch.float32, device=dev)
+        self.att_cnt = torch.zeros(batch * dm.NH, dtype=torch.int32, device=dev)
         d.workspace, d.workspace_bytes = self.att_ws.data_ptr(), self.att_ws.numel() * 4
         d.counters, d.n_counters = self.att_cnt.data_ptr(), self.att_cnt.numel()
+        # row statistics of the residual stream for the LayerNorms fused into the
+        # decode GEMMs: two [ceil(H/128), rows] arrays of (mean, M2) pairs
+        tiles = (dm.H + 127) // 128
+        self.ln_stats = torch.zeros(4 * tiles * rows, dtype=torch.float32, device=dev)
+        d.ln_stats, d.ln_stats_bytes = self.ln_stats.data_ptr(), self.ln_stats.numel() * 4
         d.keys = self.keys.data_ptr()
         d.len_dev, d.step_dev = self.len_dev.data_ptr(), self.step_dev.data_ptr()
         d.out_tokens = self.out_tokens.data_ptr()
@@ -257,6 +285,16 @@ class Session:
                 "tf_forward")
         self.len += T
         return N.lib().tf_session_launches_per_step(self.handle)
+
+    def forward_taps(self, T: int, mode: int) -> torch.Tensor:
+        """forward() that also returns the residual stream at every LayerNorm
+        input, f16 [2L+1, batch*T, H] (tf_forward_taps)."""
+        dm = self.dm
+        taps = torch.empty((2 * dm.L + 1, self.batch * T, dm.H), dtype=torch.float16, device=self.k_cache.device)
+        N.check(N.lib().tf_forward_taps(self.handle, C.c_void_p(self.ids.data_ptr()), C.c_void_p(self.pos.data_ptr()),
+                                        T, mode, C.c_void_p(taps.data_ptr()), self.stream()), "tf_forward_taps")
+        self.len += T
+        return taps
 
     def decode(self, n_steps: int, use_graph: bool = True) -> int:
         if n_steps <= 0:

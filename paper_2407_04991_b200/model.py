@@ -439,6 +439,33 @@ def forward_full(model: Model, token_ids, fused: bool = True) -> Tensor:
     return _host_logits(out, c.dtype)
 
 
+def hidden_states(model: Model, token_ids) -> Tensor:
+    """Extension (no reference counterpart; the parity tap of SURVEY appendix B):
+    the residual stream at every LayerNorm input of one causal forward over
+    ``token_ids``, shape [2L+1, T, H] in the model dtype. ``[0]`` is
+    ``embed(token_ids)``; ``[2l+1]`` is layer l's ffn_norm input (after the
+    attention residual, model.py:481-484); ``[2l+2]`` the next attn_norm input
+    (after the FFN residual, model.py:493 -> 460), the last one the final_norm
+    input (model.py:497)."""
+    import torch
+
+    from . import _native as N
+
+    c = model.config
+    ids = _check_ids(c, token_ids)
+    t = len(ids)
+    if t == 0:
+        raise ParameterError("hidden_states requires at least one token")
+    if t > c.max_position:
+        raise PositionError(f"sequence length {t} exceeds max_position")
+    dm = model.device_model()
+    with dm.lock, torch.cuda.device(dm.device):
+        s = dm.session(1, t, t, 1, logits=True)
+        s.load_inputs(np.asarray(ids, np.int32), np.arange(t, dtype=np.int32), np.zeros(1, np.int32))
+        taps = s.forward_taps(t, N.FWD_LOGITS_LAST).cpu().numpy()
+    return _host_logits(taps, c.dtype)
+
+
 def decode_step(model: Model, token_id: int, cache: KVCache, fused: bool = True) -> Tensor:
     """Incremental decode of one token into ``cache``; returns [1, V] logits."""
     import torch

@@ -58,8 +58,15 @@ class Scratch:
 
 def gemm(act: torch.Tensor, wt: torch.Tensor, k: int, epilogue: int, *, out=None, bias=None,
          resid=None, scratch: Scratch | None = None, force_swap: int = -1, splits: int = 0,
-         keys=None, qkv=None, m_tok: int | None = None, n_feat: int | None = None):
-    """out[m, n] = epilogue(act[m, :k] . wt[n, :k]^T) on the current stream."""
+         keys=None, qkv=None, m_tok: int | None = None, n_feat: int | None = None, ln=None,
+         stats=None):
+    """out[m, n] = epilogue(act[m, :k] . wt[n, :k]^T) on the current stream.
+
+    ``ln = (stats, stats_ld, hidden, c, d)``: LayerNorm folded into the GEMM
+    (swap-AB only): ``wt`` holds gamma-folded weights and the accumulator
+    becomes inv * (acc - mean * c) + d, row statistics from ``stats``;
+    ``stats = (buffer, stats_ld)``: an EPI_BIAS_RESID GEMM also writes the
+    per-128-feature-tile (mean, M2) pairs of its output rows there."""
     m = act.shape[0] if m_tok is None else m_tok
     n = wt.shape[0] if n_feat is None else n_feat
     d = N.GemmDesc()
@@ -83,6 +90,12 @@ def gemm(act: torch.Tensor, wt: torch.Tensor, k: int, epilogue: int, *, out=None
     if scratch is not None:
         d.workspace, d.workspace_bytes = _ptr(scratch.ws), scratch.workspace_bytes
         d.counters, d.n_counters = _ptr(scratch.counters), scratch.n_counters
+    if ln is not None:
+        st, st_ld, hidden, lc, ld = ln
+        d.ln_stats, d.ln_stats_ld, d.ln_hidden = _ptr(st), st_ld, hidden
+        d.ln_c, d.ln_d = _ptr(lc), _ptr(ld)
+    if stats is not None:
+        d.stats_out, d.stats_ld = _ptr(stats[0]), stats[1]
     d.force_swap, d.splits, d.pdl = force_swap, splits, 0
     N.check(N.lib().tf_gemm(C.byref(d), _stream()), "tf_gemm")
     return out
@@ -107,13 +120,13 @@ def attention(q, ldq_rows_view, k_cache, v_cache, start, qbase, scale, out, *, b
 
 
 def embed_ln(ids, pos, tok_emb, pos_emb, hidden, x, h=None, gamma=None, beta=None, *,
-             remap=None, unk_id=0, type_ids=None, type_emb=None, ids_out=None):
+             remap=None, unk_id=0, type_ids=None, type_emb=None, type_const=0, ids_out=None):
     if ids.shape != pos.shape:
         raise DimensionError("ids/pos shape mismatch")
     d = N.EmbedDesc()
     d.n_tok, d.hidden = ids.numel(), hidden
     d.vocab, d.max_pos = tok_emb.shape[0], pos_emb.shape[0]
-    d.ids, d.pos, d.type_ids = _ptr(ids), _ptr(pos), _ptr(type_ids)
+    d.ids, d.pos, d.type_ids, d.type_const = _ptr(ids), _ptr(pos), _ptr(type_ids), type_const
     if remap is not None:
         d.remap, d.remap_n = _ptr(remap), remap.numel()
     d.unk_id = unk_id

@@ -161,31 +161,47 @@ def test_embed_gather_sum_bit_exact_and_remap(cuda_device):
     assert torch.equal(x.cpu(), ref)  # bit-exact gather-sum
 
 
-@pytest.mark.parametrize("m,n,k", [(32, 2304, 768), (5, 200, 128), (32, 1000, 768)])
-def test_gemm_fused_layernorm_operand(cuda_device, m, n, k):
-    """Swap-AB GEMM whose activation operand is LN(x) built in-kernel matches
-    LN kernel + GEMM. The in-kernel LN sums each row with 8 threads (fixed
-    order) instead of the LN kernel's 32 lanes, so an f16-rounded LN value can
-    differ by one ulp: compared within 5e-3 absolute."""
-    x = rand16(m, k, seed=20).to(cuda_device)
-    g = (1 + 0.05 * torch.randn(k)).half().float().to(cuda_device)
-    b = (0.05 * torch.randn(k)).half().float().to(cuda_device)
-    w = rand16(n, ops.pad64(k), scale=0.05, seed=21).to(cuda_device)
-    h = torch.empty_like(x)
-    ops.layernorm(x, k, g, b, h)
-    ref = torch.empty(m, n, dtype=torch.float32, device=cuda_device)
-    ops.gemm(h, w, k, N.EPI_F32, out=ref, force_swap=1)
-    got = torch.empty_like(ref)
-    d = N.GemmDesc()
-    d.m_tok, d.n_feat, d.k = m, n, k
-    d.act, d.lda = x.data_ptr(), x.stride(0)
-    d.wt, d.ldw = w.data_ptr(), w.stride(0)
-    d.epilogue = N.EPI_F32
-    d.out, d.ldo = got.data_ptr(), got.stride(0)
-    d.force_swap = 1
-    d.ln_x, d.ln_ldx, d.ln_src_stride, d.ln_src_off, d.ln_hidden = x.data_ptr(), x.stride(0), 1, 0, k
-    d.ln_gamma, d.ln_beta = g.data_ptr(), b.data_ptr()
-    import ctypes as C
-    N.check(N.lib().tf_gemm(C.byref(d), C.c_void_p(torch.cuda.current_stream().cuda_stream)), "tf_gemm")
+@pytest.mark.parametrize("m,n,h", [(32, 2304, 768), (5, 200, 256), (64, 3072, 768), (100, 640, 384),
+                                   (256, 2304, 768), (16, 384, 200)])
+def test_fused_layernorm_statistics(cuda_device, m, n, h):
+    """The decode LayerNorm fusion (tensor.py:153-160 restated over tiles): a
+    residual GEMM (swap-AB split-K) writes per-128-feature (mean, M2) pairs of
+    its output rows; a consuming GEMM with gamma folded into its weights applies
+    inv * (x . W' - mean * c) + d. The pairs match numpy (fp64) per tile; the
+    consumer matches LN(x) . W in fp64 within 5e-3 (the folded weights are
+    f16-rounded and the LN output is not)."""
+    kin = 256
+    tiles = (h + 127) // 128
+    a = rand16(m, kin, seed=30).to(cuda_device)
+    wo = rand16(h, kin, scale=0.05, seed=31).to(cuda_device)
+    bo = (0.1 * torch.randn(h, generator=torch.Generator().manual_seed(3))).half().float().to(cuda_device)
+    hp = ops.pad64(h)
+    x = torch.zeros(m, hp, dtype=torch.half)
+    x[:, :h] = rand16(m, h, seed=32)
+    x = x.to(cuda_device)
+    stats = torch.full((2 * tiles * m,), float("nan"), dtype=torch.float32, device=cuda_device)
+    ops.gemm(a, wo, kin, N.EPI_BIAS_RESID, out=x, bias=bo, resid=x, force_swap=1, stats=(stats, m))
     torch.cuda.synchronize()
-    assert (got - ref).abs().max().item() <= 5e-3
+    xs = x[:, :h].double().cpu().numpy()
+    got = stats.view(tiles, m, 2).double().cpu().numpy()
+    for i in range(tiles):
+        seg = xs[:, 128 * i:min(h, 128 * i + 128)]
+        mu = seg.mean(axis=1)
+        m2 = ((seg - mu[:, None]) ** 2).sum(axis=1)
+        assert np.allclose(got[i, :, 0], mu, rtol=1e-5, atol=1e-6)
+        assert np.allclose(got[i, :, 1], m2, rtol=1e-4, atol=1e-5)
+    from paper_2407_04991_b200.device import _fold_ln
+    g = (1 + 0.05 * torch.randn(h, generator=torch.Generator().manual_seed(4))).half().float()
+    b = (0.05 * torch.randn(h, generator=torch.Generator().manual_seed(5))).half().float()
+    w = rand16(n, hp, scale=0.05, seed=33)
+    wf, c, dd = _fold_ln(w.numpy(), h, g.numpy(), b.numpy())
+    wf, c, dd = (torch.from_numpy(v).to(cuda_device) for v in (wf, c, dd))
+    out = torch.full((m, n), float("nan"), dtype=torch.float32, device=cuda_device)
+    ops.gemm(x, wf, h, N.EPI_F32, out=out, force_swap=1, ln=(stats, m, h, c, dd))
+    torch.cuda.synchronize()
+    xd = x[:, :h].double().cpu()
+    mu = xd.mean(dim=1, keepdim=True)
+    var = ((xd - mu) ** 2).mean(dim=1, keepdim=True)
+    ln = (xd - mu) / torch.sqrt(var + 1e-5) * g.double() + b.double()
+    ref = (ln @ w[:, :h].double().T).float().to(cuda_device)
+    assert (out - ref).abs().max().item() <= 5e-3
