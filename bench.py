@@ -251,12 +251,19 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+# C2 / C3: every GPU runs its own batch (weak scaling); C4 (64 requests) and
+# C5 (20k requests) are one fixed job sharded across the GPUs (strong scaling,
+# BASELINE configs[3] / [4])
+STRONG = ("c4", "c5")
+
+
 def base_line(args, w, world, value, ms_per_step):
+    strong = args.workload in STRONG
     return {"metric": "generated tokens/s", "value": value, "unit": "generated tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f16", "data": "synthetic",
-            "config": {"workload": w["text"], "global_batch": w["batch"] * (1 if args.workload == "c5" else world),
+            "config": {"workload": w["text"], "global_batch": w["batch"] * (1 if strong else world),
                        "seq_len": w["src"] or "32-512", "new_tokens": w["new"], "beam": w["beam"],
                        "parallelism": f"dp{world} (independent requests, no collective)",
                        "l2": "flushed between timed steps (256 MB write); the per-step working set "
@@ -360,7 +367,13 @@ def run_ours(args):
     if args.workload == "c5":
         return run_sweep(args, w, model, dm, rank, world, dev)
 
-    prompts = make_prompts(c.vocab_size, w, rank)
+    if args.workload in STRONG:  # one job of w["batch"] requests, contiguous shard per rank
+        allp = make_prompts(c.vocab_size, w, 0)
+        per = (len(allp) + world - 1) // world
+        prompts = allp[rank * per:(rank + 1) * per]
+        assert prompts, "more ranks than requests"
+    else:
+        prompts = make_prompts(c.vocab_size, w, rank)
     run = Runner(model, prompts, w)
     for _ in range(max(args.warmup, 3)):
         run.stage()
@@ -394,8 +407,10 @@ def run_ours(args):
         t = torch.tensor([total], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total = float(t.item())
-    gen_per_step = w["batch"] * w["new"]
-    value = gen_per_step * args.steps * world / total
+    # whole-job generated tokens per step: every rank's batch (weak) or the one
+    # sharded job (strong)
+    gen_per_step = w["batch"] * w["new"] * (1 if args.workload in STRONG else world)
+    value = gen_per_step * args.steps / total
 
     # ---------------- end-to-end through the public API
     for _ in range(2):
@@ -413,22 +428,35 @@ def run_ours(args):
     st = PM.LAST_STATS
     if not run.beam:
         assert [r[w["src"]:] for r in out] == [list(map(int, r)) for r in last], "API/device mismatch"
+    # ---------------- latency: p50 of 20 repeated generate calls (public API,
+    # wall clock incl. host copies) and the p50 device decode step (below)
+    gen_ms = []
+    for _ in range(20):
+        t1 = time.perf_counter()
+        run.api_step()
+        gen_ms.append((time.perf_counter() - t1) * 1e3)
 
     # ---------------- rooflines
     H, F, V, L = c.hidden_size, c.ffn_size, c.vocab_size, c.num_layers
-    S = w["batch"] * w["beam"]
+    nb = len(prompts)  # this rank's requests
+    S = nb * w["beam"]
     # live context: the prompt once per request (beams share it: SURVEY 8d shared
     # prefix, read from beam 0's rows) + the generated slots per row
-    step_bytes = [decode_step_bytes(L, H, F, V, S, w["batch"] * w["src"] + S * i) for i in range(1, w["new"])]
+    step_bytes = [decode_step_bytes(L, H, F, V, S, nb * w["src"] + S * i) for i in range(1, w["new"])]
     t_step = probe_decode_step(torch, run, flush, stream, w)
     step_bw = float(np.mean(step_bytes)) / t_step / 1e9
+    latency = {"p50_generate_ms": float(np.percentile(gen_ms, 50)), "p90_generate_ms": float(np.percentile(gen_ms, 90)),
+               "generate_calls": len(gen_ms), "p50_decode_step_us": t_step * 1e6,
+               "note": "generate = one public-API call (this rank's batch, prefill + all decode steps, host "
+                       "copies included); decode step = CUDA-event median of graph-replayed steps"}
+    prefill = probe_prefill(torch, run, dm, flush, stream, w, peaks()[1])
     kern = probe_dominant_kernel(torch, dm, run.sess, flush, stream, S)
     n_launch = int(N.lib().tf_session_launches_per_step(run.sess.handle))
 
     if rank == 0:
         line = base_line(args, w, world, value, 1e3 * total / args.steps)
         line.update({
-            "e2e": {"value": gen_per_step * args.steps * world / e2e_t, "unit": "generated tokens/s",
+            "e2e": {"value": gen_per_step * args.steps / e2e_t, "unit": "generated tokens/s",
                     "h2d_bytes_per_step": int(st.h2d_bytes), "d2h_bytes_per_step": int(st.d2h_bytes)},
             "gpu_launches": int(run.launches() * args.steps),
             # the roofline unit is the decode step (north star: fraction of the
@@ -448,6 +476,8 @@ def run_ours(args):
                                "traffic": ncu_traffic() if args.workload == "c2" else None},
             "clocks": clk.summary(),
         })
+        line["latency"] = latency
+        line["prefill"] = prefill
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(args.workload)
         print(json.dumps(line), flush=True)
@@ -488,6 +518,67 @@ def probe_decode_step(torch, run, flush, stream, w):
         e1.synchronize()
         ts.append(e0.elapsed_time(e1) / 1e3 / (w["new"] - 1))
     return float(statistics.median(ts))
+
+
+def prefill_flops(L, H, F, V, B, T, pads_sum=0):
+    """Prefill of B prompts of T tokens: the GEMMs (QKV, Wo, FFN1, FFN2 over
+    every token; lm_head over the last position) + causal attention QK^T and
+    PV over each row's valid window."""
+    gemm = 2 * B * T * L * (4 * H * H + 2 * H * F) + 2 * B * H * V
+    ctx = B * T * (T + 1) // 2 - pads_sum * T
+    return gemm, 4 * L * H * ctx
+
+
+def probe_prefill(torch, run, dm, flush, stream, w, tflops_peak):
+    """Prefill forward (CUDA events, L2 flushed before each of 5 runs) and its
+    largest GEMM alone (FFN1, tokens x F x H, 20 back-to-back launches in a
+    CUDA graph): tensor-pipe throughput vs the measured dense bf16/f16 peak."""
+    from paper_2407_04991_b200 import _native as N
+    from paper_2407_04991_b200 import ops
+    if run.beam:
+        return None
+    B, T = run.ids.shape
+    ts = []
+    for _ in range(5):
+        run.stage()
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run.sess.forward(T, N.FWD_ARGMAX)
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    t = float(statistics.median(ts))
+    gf, af = prefill_flops(dm.L, dm.H, dm.F, dm.V, B, T, int(run.pads.sum()))
+    M = B * T
+    act = torch.randn(M, dm.ldk_h, device=dm.device).half()
+    out = torch.empty(M, dm.ldk_f, dtype=torch.float16, device=dm.device)
+    w1, b1 = dm.layers[0]["w1_t"], dm.layers[0]["b1"]
+    gs = torch.cuda.Stream()
+    with torch.cuda.stream(gs):
+        ops.gemm(act, w1, dm.H, N.EPI_BIAS_GELU, out=out, bias=b1)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            for _ in range(20):
+                ops.gemm(act, w1, dm.H, N.EPI_BIAS_GELU, out=out, bias=b1)
+    torch.cuda.synchronize()
+    gts = []
+    with torch.cuda.stream(gs):
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(gs)
+            graph.replay()
+            e1.record(gs)
+            e1.synchronize()
+            gts.append(e0.elapsed_time(e1) / 1e3 / 20)
+    tg = float(statistics.median(gts))
+    g_tf = 2 * M * dm.F * dm.H / tg / 1e12
+    return {"us": t * 1e6, "gemm_flops": gf, "attn_flops": af,
+            "achieved_tflops": (gf + af) / t / 1e12, "frac_of_tensor_peak": (gf + af) / t / 1e12 / tflops_peak,
+            "largest_gemm": {"kernel": f"gemm_tc_kernel<EPI_BIAS_GELU> FFN1 {M}x{dm.F}x{dm.H}", "us": tg * 1e6,
+                             "achieved_tflops": g_tf, "frac_of_tensor_peak": g_tf / tflops_peak},
+            "peak_tflops": tflops_peak, "peak_kind": "MEASURED_PEAKS.json bf16_tflops (dense, burst)"}
 
 
 def probe_dominant_kernel(torch, dm, sess, flush, stream, batch):
@@ -590,9 +681,40 @@ def run_sweep(args, w, model, dm, rank, world, dev):
         dist.destroy_process_group()
 
 
+def relaunch_distributed(n):
+    """`bench.py --gpus N` (N > 1) without a torchrun environment: re-exec this
+    command under torch.distributed.run with N local ranks (127.0.0.1)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
+def run_dry(args):
+    """--dry-run: the launch and rendezvous only (gloo, no GPU work); rank 0
+    prints how many ranks joined."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    joined = 1
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        joined = int(t.item())
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_joined": joined, "workload": args.workload}),
+              flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--dry-run", action="store_true", help="launch + rendezvous only (CPU, gloo)")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
@@ -600,6 +722,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch_distributed(args.gpus)
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', '1')}")
+    if args.dry_run:
+        run_dry(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -202,10 +202,11 @@ class Cache:
 
 
 def forward_tokens(w, c: Config, ids, pos, cache: Cache, start, all_logits=False,
-                   taps=None):
+                   taps=None, types=None):
     """model.py:440-504. ids/pos [B,T] int; returns logits [B,V] (last row) or
     [B,T,V]. ``taps`` (list) collects the 2L+1 residual-stream LN inputs
-    (SURVEY appendix B)."""
+    (SURVEY appendix B). ``types`` [B,T] (extension, no reference code): adds
+    w["type_embedding"][types] to the f32 gather-sum before the rounding."""
     f16 = c.f16
     B, T = ids.shape
     H, NH, D = c.hidden_size, c.num_heads, c.head_dim
@@ -214,8 +215,10 @@ def forward_tokens(w, c: Config, ids, pos, cache: Cache, start, all_logits=False
     if length > cache.k.shape[3]:
         raise OverflowError("cache capacity exceeded")
     scale = 1.0 / math.sqrt(D)
-    x = quant(w["token_embedding"][ids.reshape(-1)] + w["position_embedding"][pos.reshape(-1)],
-              f16).reshape(B, T, H)
+    x = w["token_embedding"][ids.reshape(-1)] + w["position_embedding"][pos.reshape(-1)]
+    if types is not None:
+        x = x + w["type_embedding"][np.asarray(types).reshape(-1)]
+    x = quant(x, f16).reshape(B, T, H)
     for li in range(c.num_layers):
         p = f"layers.{li}."
         if taps is not None:
@@ -299,10 +302,12 @@ def left_pad(c: Config, prompts):
 
 
 def batched_greedy_decode(w, c: Config, prompts, max_new, step_logits=None,
-                          teacher=None):
+                          teacher=None, type_ids=None, gen_type=0):
     """model.py:613-667. ``step_logits`` (list) collects per-step [B,V] logits;
     ``teacher`` ([B, max_new] ids) forces the fed tokens (teacher forcing) while
-    still recording the argmax as the output."""
+    still recording the argmax as the output. ``type_ids`` (per-prompt lists) /
+    ``gen_type`` (extension): token types of the prompts (pads: 0) and of every
+    generated token."""
     if not prompts:
         return []
     ids, pos, pads, lens = left_pad(c, prompts)
@@ -311,7 +316,12 @@ def batched_greedy_decode(w, c: Config, prompts, max_new, step_logits=None,
     seqs = [list(map(int, p)) for p in prompts]
     if max_new == 0:
         return seqs
-    logits = forward_tokens(w, c, ids, pos, cache, pads)
+    types = None
+    if type_ids is not None:
+        types = np.zeros((B, L), np.int64)
+        for i, tp in enumerate(type_ids):
+            types[i, pads[i]:] = tp
+    logits = forward_tokens(w, c, ids, pos, cache, pads, types=types)
     done = [False] * B
     for step in range(max_new):
         if step_logits is not None:
@@ -329,7 +339,8 @@ def batched_greedy_decode(w, c: Config, prompts, max_new, step_logits=None,
             newpos[i, 0] = cache.len - pads[i]
         if all(done) or step == max_new - 1:
             break
-        logits = forward_tokens(w, c, feed, newpos, cache, pads)
+        logits = forward_tokens(w, c, feed, newpos, cache, pads,
+                                types=None if type_ids is None else np.full((B, 1), gen_type, np.int64))
     return seqs
 
 

@@ -61,6 +61,8 @@ class BeamRun:
         c = model.config
         if not 1 <= beam_width <= 8:
             raise ParameterError("beam_width must be in [1, 8]")
+        if beam_width > c.vocab_size:
+            raise ParameterError("beam_width must not exceed vocab_size")
         self.model, self.c = model, c
         self.prompts = _validate_prompts(c, prompts, max_new_tokens)
         self.new, self.K, self.R = max_new_tokens, beam_width, len(self.prompts)
@@ -134,11 +136,14 @@ def beam_search_decode(model: Model, prompts: list[list[int]], max_new_tokens: i
         return []
     if not 1 <= beam_width <= 8:
         raise ParameterError("beam_width must be in [1, 8]")
+    if beam_width > c.vocab_size:
+        raise ParameterError("beam_width must not exceed vocab_size")
     checked = _validate_prompts(c, prompts, max_new_tokens)
     if max_new_tokens == 0:
         return [list(p) for p in checked]
-    run = BeamRun(model, checked, max_new_tokens, beam_width)
-    with run.dm.lock, torch.cuda.device(run.dm.device):
+    dm = model.device_model()
+    with dm.lock, torch.cuda.device(dm.device):  # the session is created and used under the lock
+        run = BeamRun(model, checked, max_new_tokens, beam_width)
         h2d = run.stage_inputs()
         run.run_device(use_graph)
         seqs, d2h = run.finish()

@@ -68,7 +68,9 @@ class DeviceModel:
         self.H, self.F, self.V = c.hidden_size, c.ffn_size, c.vocab_size
         self.L, self.NH, self.D, self.P = c.num_layers, c.num_heads, c.head_dim, c.max_position
         self.ldk_h, self.ldk_f = pad64(self.H), pad64(self.F)
-        self.lock = threading.Lock()
+        # re-entrant: session() takes it too, so a session can never be evicted
+        # (and closed) while another thread holding the lock uses it
+        self.lock = threading.RLock()
         f32 = {name: t.array.astype(np.float32) for name, t in model.named_tensors()}
         up16 = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
         self._keep = []
@@ -78,6 +80,9 @@ class DeviceModel:
             return t
 
         self.tok_emb = keep(up16(round_to(f32["token_embedding"], DType.F16)))
+        self.type_emb = None
+        if model.type_embedding is not None:  # extension: word + position + type gather-sum
+            self.type_emb = keep(up16(round_to(model.type_embedding.array.astype(np.float32), DType.F16)))
         self.pos_emb = keep(up16(round_to(f32["position_embedding"], DType.F16)))
         layers = (N.LayerWeights * self.L)()
         self.layers = []
@@ -115,7 +120,9 @@ class DeviceModel:
         d.vocab, d.hidden, d.layers, d.heads = self.V, self.H, self.L, self.NH
         d.head_dim, d.ffn, d.max_pos = self.D, self.F, self.P
         d.ldk_h, d.ldk_f = self.ldk_h, self.ldk_f
-        d.tok_emb, d.pos_emb, d.type_emb, d.n_types = self.tok_emb.data_ptr(), self.pos_emb.data_ptr(), None, 0
+        d.tok_emb, d.pos_emb = self.tok_emb.data_ptr(), self.pos_emb.data_ptr()
+        if self.type_emb is not None:
+            d.type_emb, d.n_types = self.type_emb.data_ptr(), self.type_emb.shape[0]
         d.ldw = self.tok_emb.stride(0)
         d.layer = layers
         d.final_gamma, d.final_beta = self.final_gamma.data_ptr(), self.final_beta.data_ptr()
@@ -142,14 +149,15 @@ class DeviceModel:
     def session(self, batch: int, capacity: int, max_tokens: int, max_new: int,
                 logits=False, beam: int = 0) -> "Session":
         key = (batch, capacity, max_tokens, max_new, logits, beam)
-        s = self._sessions.get(key)
-        if s is None:
-            if len(self._sessions) >= 16:  # bound the cache; drop the oldest
-                old = next(iter(self._sessions))
-                self._sessions.pop(old).close()
-            s = Session(self, batch, capacity, max_tokens, max_new, logits, beam=beam)
-            self._sessions[key] = s
-        return s
+        with self.lock:
+            s = self._sessions.get(key)
+            if s is None:
+                if len(self._sessions) >= 16:  # bound the cache; drop the oldest
+                    old = next(iter(self._sessions))
+                    self._sessions.pop(old).close()
+                s = Session(self, batch, capacity, max_tokens, max_new, logits, beam=beam)
+                self._sessions[key] = s
+            return s
 
     def close(self):
         for s in self._sessions.values():
@@ -188,12 +196,13 @@ class Session:
         logit_rows = batch if logits == "last" else rows
         self.logits = z16(logit_rows, dm.V) if logits else None
         self.keys = torch.zeros(batch, dtype=torch.int64, device=dev)
-        # int32 state: [len, step] + pads[B] + ids[rows] + pos[rows]
-        self.state = torch.zeros(2 + batch + 2 * rows, dtype=torch.int32, device=dev)
+        # int32 state: [len, step] + pads[B] + ids[rows] + pos[rows] + types[rows]
+        self.state = torch.zeros(2 + batch + 3 * rows, dtype=torch.int32, device=dev)
         self.len_dev, self.step_dev = self.state[0:1], self.state[1:2]
         self.pads = self.state[2:2 + batch]
         self.ids = self.state[2 + batch:2 + batch + rows]
-        self.pos = self.state[2 + batch + rows:]
+        self.pos = self.state[2 + batch + rows:2 + batch + 2 * rows]
+        self.types = self.state[2 + batch + 2 * rows:]
         self.out_tokens = torch.zeros((batch, self.max_new), dtype=torch.int32, device=dev)
         self.host_in = torch.zeros(self.state.numel(), dtype=torch.int32).pin_memory()
         self.host_out = torch.zeros((batch, self.max_new), dtype=torch.int32).pin_memory()
@@ -231,6 +240,8 @@ class Session:
         d.remap, d.remap_n, d.unk_id = None, 0, 0
         if beam:
             d.beam_indir, d.beam = self.indir.data_ptr(), beam
+        if dm.type_emb is not None:
+            d.type_ids, d.gen_type = self.types.data_ptr(), 0
         self.desc = d
         h = C.c_void_p()
         N.check(N.lib().tf_session_create(dm.handle, C.byref(d), C.byref(h)), "tf_session_create")
@@ -252,6 +263,12 @@ class Session:
         self.desc.remap, self.desc.remap_n, self.desc.unk_id = t.data_ptr(), t.numel(), 0
         self._push_desc()
 
+    def set_gen_type(self, gen_type: int):
+        """Type row of generated tokens (models with a type table)."""
+        if self.dm.type_emb is not None and self.desc.gen_type != gen_type:
+            self.desc.gen_type = gen_type
+            self._push_desc()
+
     def _push_desc(self):
         """Re-create the native session with the updated descriptor (buffers kept)."""
         N.lib().tf_session_destroy(self.handle)
@@ -265,18 +282,23 @@ class Session:
     def stream():
         return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
-    def load_inputs(self, ids: np.ndarray, pos: np.ndarray, pads: np.ndarray, length: int = 0):
-        """One H2D copy of [len, step, pads, ids, pos] from pinned memory."""
-        B, rows = self.batch, ids.size
+    def load_inputs(self, ids: np.ndarray, pos: np.ndarray, pads: np.ndarray, length: int = 0,
+                    types: np.ndarray | None = None):
+        """One H2D copy of [len, step, pads, ids, pos(, types)] from pinned memory."""
+        B, rows, R = self.batch, ids.size, self.batch * self.max_tokens
         buf = self.host_in.numpy()
         buf[0], buf[1] = length, 0
         buf[2:2 + B] = pads
         buf[2 + B:2 + B + rows] = ids.reshape(-1)
-        buf[2 + B + self.batch * self.max_tokens:2 + B + self.batch * self.max_tokens + rows] = pos.reshape(-1)
-        self.state.copy_(self.host_in, non_blocking=True)
+        buf[2 + B + R:2 + B + R + rows] = pos.reshape(-1)
+        n = 2 + B + R + rows
+        if self.dm.type_emb is not None:
+            buf[2 + B + 2 * R:2 + B + 2 * R + rows] = 0 if types is None else np.asarray(types).reshape(-1)
+            n = 2 + B + 2 * R + rows
+        self.state[:n].copy_(self.host_in[:n], non_blocking=True)
         self.keys.zero_()
         self.len = length
-        return (2 + B + 2 * rows) * 4
+        return (2 + B + (3 if self.dm.type_emb is not None else 2) * rows) * 4
 
     def forward(self, T: int, mode: int, use_ids: bool = True, pdl: bool = True):
         ids = C.c_void_p(self.ids.data_ptr()) if use_ids else None

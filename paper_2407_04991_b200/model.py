@@ -32,7 +32,7 @@ from .errors import (
     PositionError,
     VocabError,
 )
-from .rng import SplitMix64
+from .rng import SplitMix64, derive_seed
 from .tensor import DType, Tensor, read_tinf, round_to, write_tinf
 
 WEIGHT_SCALE = 0.05
@@ -163,6 +163,10 @@ class Model:
         self.lm_head = lm_head
         self._f32: dict[str, np.ndarray] | None = None
         self._device = None  # (memo token, {device index: DeviceModel})
+        # extension (north star: word/position/TYPE gather-sum): optional
+        # [n_types, H] table, kept outside named_tensors / ModelConfig so the
+        # reference's TINF layout and JSON field set are unchanged
+        self.type_embedding: Tensor | None = None
         self._check_shapes()
 
     def _check_shapes(self):
@@ -213,6 +217,46 @@ class Model:
             with torch.cuda.device(dev):
                 mirrors[dev.index] = DeviceModel(self, dev)
         return mirrors[dev.index]
+
+
+def set_type_embedding(model: Model, table) -> Model:
+    """Attach (or clear, ``table=None``) a token-type embedding [n_types, H]
+    (extension: the reference embeds token + position only, model.py:453-455).
+    Rounded to the model dtype; invalidates the device mirror like a weight
+    mutation."""
+    if table is None:
+        model.type_embedding = None
+    else:
+        arr = np.asarray(table.array if isinstance(table, Tensor) else table, dtype=np.float32)
+        if arr.ndim != 2 or arr.shape[0] < 1 or arr.shape[1] != model.config.hidden_size:
+            raise ParameterError(f"type embedding must be [n_types >= 1, {model.config.hidden_size}]")
+        model.type_embedding = Tensor(round_to(arr, model.config.dtype), model.config.dtype)
+    model._f32 = None
+    return model
+
+
+def init_type_embedding(model: Model, n_types: int, seed: int) -> Model:
+    """Random type table with the init_random distribution (uniform [-0.05,
+    0.05) from SplitMix64(derive_seed(seed, "type_embedding")))."""
+    if n_types < 1:
+        raise ParameterError("n_types must be >= 1")
+    s = SplitMix64(derive_seed(seed, "type_embedding"))
+    vals = s.uniform(n_types * model.config.hidden_size, -0.05, 0.05).astype(np.float32)
+    return set_type_embedding(model, vals.reshape(n_types, model.config.hidden_size))
+
+
+def _check_types(model: Model, type_ids, n: int) -> np.ndarray | None:
+    if type_ids is None:
+        return None
+    if model.type_embedding is None:
+        raise ParameterError("type_ids given but the model has no type embedding")
+    t = np.asarray(list(map(int, type_ids)), np.int32)
+    if t.size != n:
+        raise ParameterError("type_ids must have one entry per token")
+    nt = model.type_embedding.shape[0]
+    if t.size and (t.min() < 0 or t.max() >= nt):
+        raise VocabError(f"type id out of range [0, {nt})")
+    return t
 
 
 def init_random(config: ModelConfig, seed: int) -> Model:
@@ -389,8 +433,9 @@ def _host_logits(arr_f16: np.ndarray, dtype: DType) -> Tensor:
 # ---------------------------------------------------------------------------
 # public single-sequence operations (reference model.py:521-606)
 # ---------------------------------------------------------------------------
-def embed(model: Model, token_ids, start_position: int = 0) -> Tensor:
-    """Token rows plus position rows [start, start+T), rounded to the model dtype."""
+def embed(model: Model, token_ids, start_position: int = 0, type_ids=None) -> Tensor:
+    """Token rows plus position rows [start, start+T) (plus type rows when
+    ``type_ids`` is given; extension), rounded to the model dtype."""
     import torch
 
     from . import ops
@@ -408,7 +453,10 @@ def embed(model: Model, token_ids, start_position: int = 0) -> Tensor:
         dev_ids = torch.tensor(ids, dtype=torch.int32, device=dm.device)
         dev_pos = torch.arange(start_position, start_position + t, dtype=torch.int32, device=dm.device)
         x = torch.empty((t, c.hidden_size), dtype=torch.float16, device=dm.device)
-        ops.embed_ln(dev_ids, dev_pos, dm.tok_emb, dm.pos_emb, c.hidden_size, x)
+        types = _check_types(model, type_ids, t)
+        dev_types = None if types is None else torch.from_numpy(types).to(dm.device)
+        ops.embed_ln(dev_ids, dev_pos, dm.tok_emb, dm.pos_emb, c.hidden_size, x, type_ids=dev_types,
+                     type_emb=dm.type_emb if types is not None else None)
         COUNTERS.launches += 1
         arr = x.cpu().numpy()
     # the device stores f16 (F32 models are rounded on upload): an F16 model's
@@ -416,7 +464,7 @@ def embed(model: Model, token_ids, start_position: int = 0) -> Tensor:
     return _host_logits(arr, c.dtype)
 
 
-def forward_full(model: Model, token_ids, fused: bool = True) -> Tensor:
+def forward_full(model: Model, token_ids, fused: bool = True, type_ids=None) -> Tensor:
     """Full-recompute causal forward; next-token logits for every position [T, V]."""
     import torch
 
@@ -432,7 +480,8 @@ def forward_full(model: Model, token_ids, fused: bool = True) -> Tensor:
     dm = model.device_model()
     with dm.lock, torch.cuda.device(dm.device):
         s = dm.session(1, t, t, 1, logits=True)
-        s.load_inputs(np.asarray(ids, np.int32), np.arange(t, dtype=np.int32), np.zeros(1, np.int32))
+        s.load_inputs(np.asarray(ids, np.int32), np.arange(t, dtype=np.int32), np.zeros(1, np.int32),
+                      types=_check_types(model, type_ids, t))
         n = s.forward(t, N.FWD_LOGITS_ALL)
         out = s.logits[:t].cpu().numpy()
     _count_forward(c, 1, t, 0, 0, t, n)
@@ -491,7 +540,7 @@ def decode_step(model: Model, token_id: int, cache: KVCache, fused: bool = True)
 
 
 def greedy_decode(model: Model, prompt, max_new_tokens: int, use_cache: bool = True,
-                  fused: bool = True) -> list[int]:
+                  fused: bool = True, type_ids=None, gen_type_id: int = 0) -> list[int]:
     """Greedy generation; stops at eos_token or after max_new_tokens."""
     c = model.config
     ids = _check_ids(c, prompt)
@@ -504,8 +553,10 @@ def greedy_decode(model: Model, prompt, max_new_tokens: int, use_cache: bool = T
                             f"exceeds max_position {c.max_position}")
     if max_new_tokens == 0:
         return list(ids)
-    if use_cache:
-        return batched_greedy_decode(model, [ids], max_new_tokens, fused=fused)[0]
+    if use_cache or type_ids is not None:
+        return batched_greedy_decode(model, [ids], max_new_tokens, fused=fused,
+                                     type_ids=None if type_ids is None else [type_ids],
+                                     gen_type_id=gen_type_id)[0]
     seq = list(ids)
     for _ in range(max_new_tokens):
         logits = forward_full(model, seq, fused).array
@@ -573,7 +624,8 @@ LAST_STATS = GenerateStats()
 
 
 def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens: int,
-                          fused: bool = True, prompt_vocab_map=None) -> list[list[int]]:
+                          fused: bool = True, prompt_vocab_map=None, type_ids=None,
+                          gen_type_id: int = 0) -> list[list[int]]:
     """KV-cached greedy generation for a group of prompts in lockstep.
 
     Prompts are left-padded; padded slots are masked out of attention. The whole
@@ -587,7 +639,12 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
     reference): the prompts are in the ORIGINAL vocabulary of a pruned model and
     are remapped on the device by the embedding kernel (ids outside the kept set
     become the model's unk id 0); returned prompts stay as given and
-    generated ids are in the pruned vocabulary."""
+    generated ids are in the pruned vocabulary.
+
+    ``type_ids`` / ``gen_type_id`` (extension; the model needs a type table,
+    :func:`set_type_embedding`): one type id per prompt token, and the type of
+    every generated token; the embedding adds the type row (word + position +
+    type gather-sum)."""
     import torch
 
     from . import _native as N
@@ -611,13 +668,23 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
         return seqs
     ids, pos, pads, lens = _left_pad(c, checked)
     B, L = ids.shape
+    types = None
+    if type_ids is not None:
+        if len(type_ids) != len(checked):
+            raise ParameterError("type_ids must have one list per prompt")
+        types = np.zeros((B, L), np.int32)  # pad slots: type 0 (masked out of attention)
+        for i, (tp, p) in enumerate(zip(type_ids, checked)):
+            types[i, pads[i]:] = _check_types(model, tp, len(p))
+    if model.type_embedding is not None:
+        _check_types(model, [gen_type_id], 1)
     cap, max_tokens = _session_shape(c, L, max_new_tokens)
     dm = model.device_model()
     stats = GenerateStats()
     with dm.lock, torch.cuda.device(dm.device):
         s = dm.session(B, cap, max_tokens, max_new_tokens)
         s.set_remap(table)
-        stats.h2d_bytes = s.load_inputs(ids, pos, pads)
+        s.set_gen_type(gen_type_id)
+        stats.h2d_bytes = s.load_inputs(ids, pos, pads, types=types)
         n_pre = s.forward(L, N.FWD_ARGMAX)
         n_dec = s.decode(max_new_tokens - 1)
         toks = s.fetch_tokens(max_new_tokens)

@@ -77,14 +77,113 @@ def test_batched_equals_single_bitwise(cuda_device, small_model):
     assert batched == single
 
 
+def oracle_margins(args, seed, prompts, new):
+    """Per-(step, row) top-1 margins of the oracle restatement's own greedy run
+    (F16 numerics), for margin-gating token comparisons."""
+    oc = O.Config(*args, True, 1, 2)
+    rec = []
+    O.batched_greedy_decode(O.init_weights(oc, seed), oc, prompts, new, step_logits=rec)
+    return np.stack([np.sort(r, axis=-1)[:, -1] - np.sort(r, axis=-1)[:, -2] for r in rec])
+
+
 def test_batched_matches_reference(cuda_device, small_model):
+    """Reference batched_greedy_decode (model.py:613-667) golden, F16 model:
+    every generated token compared, margin-gated (a row stops being compared
+    after its first step whose oracle margin is below 2 x LOGIT_TOL)."""
     g = golden("small.npz")
     prompts = [[5, 9, 11], [7, 3, 3, 3, 20, 21], [50], [12, 13, 14, 15]]
     got = P.batched_greedy_decode(P.cast_model(small_model, P.DType.F16), prompts, 8)
     ref = [[t for t in row if t >= 0] for row in g["batched16"].tolist()]
-    for gr, rr, p in zip(got, ref, prompts):
+    margins = oracle_margins((64, 32, 2, 2, 16, 64, 64), 7, prompts, 8)
+    n_cmp = 0
+    for b, (gr, rr, p) in enumerate(zip(got, ref, prompts)):
         assert gr[:len(p)] == p
         assert len(gr) == len(rr)
+        for s in range(len(rr) - len(p)):
+            if gr[len(p) + s] != rr[len(p) + s]:
+                assert margins[s, b] < MARGIN, (b, s, gr[len(p) + s], rr[len(p) + s], margins[s, b])
+                break
+            n_cmp += 1
+    assert n_cmp >= 16
+
+
+def test_causality_bit_exact(cuda_device, small_model):
+    """Reference test_model.py:164-168: changing token 3 leaves rows 0-2 of the
+    logits bit-identical (causal masking, per-row arithmetic)."""
+    for m in (small_model, P.cast_model(small_model, P.DType.F16)):
+        base = P.forward_full(m, [3, 5, 7, 9]).array
+        perturbed = P.forward_full(m, [3, 5, 7, 2]).array
+        assert np.array_equal(base[:3], perturbed[:3])
+        assert not np.array_equal(base[3], perturbed[3])
+
+
+def test_cache_equivalence_sweep(cuda_device):
+    """Reference test_model.py:270-288 (randomised layers / heads / head_dim in
+    {4, 8, 16}): cached (device decode loop) == uncached (full recompute per
+    token) greedy generation. The reference asserts equality in F32; the device
+    computes in f16, so equality is required up to the first step whose oracle
+    margin is below 2 x LOGIT_TOL."""
+    g = np.random.default_rng(42)
+    n = 0
+    for layers in (1, 2, 4):
+        for rep in range(3):
+            heads = int(g.choice([1, 2, 4]))
+            hd = int(g.choice([4, 8, 16]))
+            hidden = heads * hd
+            if hidden > 64:
+                continue
+            seed = int(g.integers(1 << 30))
+            prompt = [int(x) for x in g.integers(0, 32, g.integers(1, 12))]
+            args = (32, hidden, layers, heads, hd, 2 * hidden, 48)
+            m = P.init_random(P.ModelConfig(*args, P.DType.F32, 1, 2), seed)
+            a = P.greedy_decode(m, prompt, 10, use_cache=True)
+            b = P.greedy_decode(m, prompt, 10, use_cache=False)
+            margins = oracle_margins(args, seed, [prompt], 10)
+            assert_tokens_margin_gated([a], [b], margins, len(prompt))
+            n += 1
+    assert n >= 5
+
+
+@pytest.mark.parametrize("heads,hd", [(2, 48), (1, 96), (3, 40), (2, 24)])
+def test_non_power_of_two_head_dims(cuda_device, heads, hd):
+    """head_dim values whose 16-byte lane groups are not a power of two take the
+    scalar paths of the generic decode attention: decode logits match the
+    oracle within tolerance and tokens margin-gated."""
+    args = (512, heads * hd, 2, heads, hd, 4 * heads * hd, 128)
+    m = P.init_random(P.ModelConfig(*args, P.DType.F16, 1, 2), 9)
+    oc = O.Config(*args, True, 1, 2)
+    w = O.init_weights(oc, 9)
+    prompts = [[5, 9, 11, 20, 7, 8], [3, 4, 100], [42] * 17]
+    got = P.batched_greedy_decode(m, prompts, 10)
+    rec = []
+    want = O.batched_greedy_decode(w, oc, prompts, 10, step_logits=rec)
+    margins = np.stack([np.sort(r, axis=-1)[:, -1] - np.sort(r, axis=-1)[:, -2] for r in rec])
+    for b, p in enumerate(prompts):
+        assert_tokens_margin_gated([got[b]], [want[b]], margins[:, b:b + 1], len(p))
+    cache = P.KVCache(m.config)
+    for t in prompts[0]:
+        lg = P.decode_step(m, t, cache).array[0].astype(np.float32)
+    ref = O.forward_full(w, oc, prompts[0])[-1]
+    assert np.max(np.abs(lg - ref)) <= LOGIT_TOL
+
+
+def test_pruned_generation_matches_reference(cuda_device):
+    """Reference pruned run (pruning.npz:c1_pruned_tokens: C1 F32 model, token
+    embedding / lm_head pruned to a kept set covering prompt and output,
+    positions trimmed to 128; test_pruning.py:127-137) on the device, tokens
+    margin-gated by the oracle's unpruned margins (restricting the vocabulary
+    can only widen a margin)."""
+    from paper_2407_04991_b200 import pruning as PR
+    g = golden("pruning.npz")
+    kept = tuple(int(t) for t in g["c1_kept"])
+    p1 = g["c1_prompt"].tolist()
+    m1 = P.init_random(c1_cfg(P.DType.F32), seed=42)
+    pm = PR.prune_token_embedding(m1, PR.PrunedVocabMap(kept_old_ids=kept, threshold=len(kept)))
+    pm = PR.prune_position_embedding(pm, 128)
+    got = P.greedy_decode(pm, [kept.index(t) for t in p1], 12)
+    margins = oracle_margins((8192, 256, 2, 4, 64, 1024, 512), 42, [p1], 12)
+    assert_tokens_margin_gated([got], [g["c1_pruned_tokens"].tolist()], margins, len(p1))
+    assert got[:len(p1)] == [kept.index(t) for t in p1]
 
 
 def test_c1_prefill_logits_and_tokens(cuda_device):

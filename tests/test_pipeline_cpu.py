@@ -120,3 +120,23 @@ def test_run_sharded_worker_failure_names_device():
     with pytest.raises(P.TinferError, match="cpu"):
         PL.run_sharded(requests(6), spec, PL.PipelineSettings(max_new_tokens=2), devices=["cpu"],
                        runner=_failing_runner, timeout=120)
+
+
+def test_bench_gpus_flag_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks
+    (never silently one): the dry run rendezvouses over gloo and rank 0
+    reports both ranks; a WORLD_SIZE that disagrees with --gpus is an error."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["ranks_joined"] == 2
+    bad = dict(env, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--dry-run"], cwd=root, env=bad,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
