@@ -32,9 +32,13 @@ own batch, no collective): "scaling": "weak".
   graph-replayed step, against MEASURED_PEAKS.json; ``traffic`` = ncu DRAM bytes
   of one step (profiles/r1_ncu_step_<w>.json). ``largest_launch``: the lm_head
   GEMM + argmax alone (rotating weight copies, HBM-streamed).
-* ``cpu_baseline`` — the oracle port (oracle/tinfer_oracle.py, numpy) on this
-  host's cores, bounded sample (prefill + a few decode steps, extrapolated).
-  ``--impl reference`` prints that arm alone (rank 0; other ranks exit 0).
+* ``cpu_baseline`` — the reference's own CPU path (unmodified tinfer model +
+  numba kernels, staged under oracle/_ref by oracle/make_ref.py) on this host's
+  cores, bounded sample (prefill + a few decode steps, extrapolated; c2/c3);
+  ``cpu_baseline_port`` — the oracle numpy port, same sample shape. c4/c5 report
+  the port (the reference has no beam search; its c5 prefill sample would run
+  minutes). ``--impl reference`` prints the reference arm alone (rank 0; other
+  ranks exit 0).
 """
 
 from __future__ import annotations
@@ -216,6 +220,72 @@ def cpu_threads():
         return os.cpu_count()
 
 
+def cpu_baseline_reference(wname="c2", samples=1, n_decode=4):
+    """The reference's OWN CPU path (unmodified tinfer model/kernels, numba, from the
+    copy oracle/make_ref.py stages under oracle/_ref) on this host's cores.
+
+    Sample: S = min(B*beam, 32) rows of the workload's prompts; per sample one
+    prefill-only call and one call with ``n_decode`` decode steps through the
+    reference's batched_greedy_decode (model.py:613-667), so t_dec = (t_full -
+    t_pre) / n_decode. Extrapolated to the workload: prefill time x (rows / S)
+    (prefill is GEMM-bound, linear in rows), decode step time as measured at S
+    rows (a lower bound for more rows -> the reported CPU throughput is an upper
+    bound). Returns None when the reference copy is absent."""
+    threads = len(os.sched_getaffinity(0))
+    os.environ.setdefault("NUMBA_NUM_THREADS", str(threads))
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/tinfer_ref_numba_cache")
+    try:
+        from oracle import ref_loader
+        T = ref_loader.load()
+    except Exception:
+        return None
+    import numba
+    M, PR = T.model, T.pruning
+    w = WORKLOADS[wname]
+    cfg = M.ModelConfig(vocab_size=40000, hidden_size=768, num_layers=12, num_heads=12, head_dim=64,
+                        ffn_size=3072, max_position=1024, dtype=T.tensor.DType.F16, eos_token=1, pad_token=2)
+    model = M.init_random(cfg, SEED)
+    if w["vocab"] == "pruned":
+        model = PR.prune_token_embedding(model, PR.build_pruned_vocab(zipf_keep_ids(), 10000, specials=[0, 1, 2]))
+    model = PR.prune_position_embedding(model, w["positions"])
+    rows = w["batch"] * w["beam"]
+    S = min(rows, 32)
+    src = w["src"] or 272  # c5: mean prompt length
+    from oracle import tinfer_oracle as O  # prompt stream only (the reference's SplitMix64 restated)
+    prompts = O.synthetic_prompts(model.config.vocab_size, S, src, seed=SEED)
+    T.kernels.warmup()
+    M.batched_greedy_decode(model, [p[:8] for p in prompts[:2]], 2)  # strided-view specialisation
+    t_pre, t_dec = [], []
+    for _ in range(samples):
+        t0 = time.perf_counter()
+        M.batched_greedy_decode(model, prompts, 1)
+        t1 = time.perf_counter()
+        M.batched_greedy_decode(model, prompts, 1 + n_decode)
+        t2 = time.perf_counter()
+        t_pre.append(t1 - t0)
+        t_dec.append(max((t2 - t1) - (t1 - t0), 1e-9) / n_decode)
+    tp, td = statistics.median(t_pre) * rows / S, statistics.median(t_dec)
+    total = tp + (w["new"] - 1) * td
+    return {"value": w["batch"] * w["new"] / total, "unit": "generated tokens/s", "cores": threads,
+            "numba_threads": int(numba.get_num_threads()), "cpu_model": cpu_model(), "kind": "reference",
+            "sample": f"unmodified reference (tinfer.model.batched_greedy_decode, numba kernels, F16 storage) "
+                      f"on {S} of {rows} rows, src {src}: prefill {statistics.median(t_pre):.2f}s + decode "
+                      f"step {td * 1e3:.0f} ms (median of {samples}); extrapolated to 1 prefill x {rows}/{S} + "
+                      f"{w['new'] - 1} steps" + (" (greedy proxy for beam: no reference beam search)"
+                                                 if w["beam"] > 1 else "")}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(wname="c2", n_decode=3):
     from oracle import tinfer_oracle as O
     w = WORKLOADS[wname]
@@ -271,15 +341,20 @@ def base_line(args, w, world, value, ms_per_step):
 
 
 def run_reference(args):
+    """The reference arm: the reference's own numba CPU path (oracle/_ref copy);
+    the oracle numpy port only if that copy is absent. At most 2 samples of the
+    workload (each a prefill + a few decode steps) keep the run within minutes."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     w = WORKLOADS[args.workload]
-    for _ in range(args.warmup):
-        cpu_baseline(args.workload, n_decode=1)
-    vals = [cpu_baseline(args.workload, n_decode=2) for _ in range(args.steps)]
-    v = float(statistics.median(x["value"] for x in vals))
-    base = dict(vals[-1], value=v)
+    base = cpu_baseline_reference(args.workload, samples=max(1, min(args.steps, 2)))
+    if base is None:
+        for _ in range(args.warmup):
+            cpu_baseline(args.workload, n_decode=1)
+        vals = [cpu_baseline(args.workload, n_decode=2) for _ in range(args.steps)]
+        base = dict(vals[-1], value=float(statistics.median(x["value"] for x in vals)))
+    v = float(base["value"])
     line = base_line(args, w, args.gpus, v, 1e3 * w["batch"] * w["new"] / v)
     line["impl"] = "reference"
     line["config"]["parallelism"] = "cpu (rank 0 only)"
@@ -444,6 +519,7 @@ def run_ours(args):
     # prefix, read from beam 0's rows) + the generated slots per row
     step_bytes = [decode_step_bytes(L, H, F, V, S, nb * w["src"] + S * i) for i in range(1, w["new"])]
     t_step = probe_decode_step(torch, run, flush, stream, w)
+    n_launch = int(N.lib().tf_session_launches_per_step(run.sess.handle))  # the decode graph's kernels
     step_bw = float(np.mean(step_bytes)) / t_step / 1e9
     latency = {"p50_generate_ms": float(np.percentile(gen_ms, 50)), "p90_generate_ms": float(np.percentile(gen_ms, 90)),
                "generate_calls": len(gen_ms), "p50_decode_step_us": t_step * 1e6,
@@ -451,7 +527,6 @@ def run_ours(args):
                        "copies included); decode step = CUDA-event median of graph-replayed steps"}
     prefill = probe_prefill(torch, run, dm, flush, stream, w, peaks()[1])
     kern = probe_dominant_kernel(torch, dm, run.sess, flush, stream, S)
-    n_launch = int(N.lib().tf_session_launches_per_step(run.sess.handle))
 
     if rank == 0:
         line = base_line(args, w, world, value, 1e3 * total / args.steps)
@@ -479,7 +554,11 @@ def run_ours(args):
         line["latency"] = latency
         line["prefill"] = prefill
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(args.workload)
+            ref = cpu_baseline_reference(args.workload) if args.workload in ("c2", "c3") else None
+            port = cpu_baseline(args.workload)
+            line["cpu_baseline"] = ref or port
+            if ref:
+                line["cpu_baseline_port"] = port
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -2,8 +2,9 @@
 
 Used by ``tests/golden/make_golden.py`` inside the build container to import the
 UNMODIFIED reference modules from ``/root/reference/pkg/src/tinfer`` and generate
-golden vectors. Never imported by the product package, ``bench.py`` or anything
-that runs on the GPU box (``/root/reference`` does not exist there).
+golden vectors, and by ``bench.py``'s reference arm / cpu_baseline on the GPU box
+(from the byte-identical copy ``oracle/make_ref.py`` stages under ``oracle/_ref``)
+to time the reference's own numba CPU path. Never imported by the product package.
 
 Why a loader: the reference ``tinfer/__init__.py:41`` imports ``tinfer.tokenizer``,
 which is missing from the mount, so ``import tinfer`` fails. The
@@ -19,8 +20,18 @@ import os
 import sys
 import types
 
-REF_SRC = "/root/reference/pkg/src/tinfer"
 PKG = "tinfer_ref"
+
+
+def _ref_src() -> str:
+    """The reference package: the mount (build container) or the copy staged by
+    oracle/make_ref.py under oracle/_ref (travels to the GPU box)."""
+    from oracle import make_ref
+    root = make_ref.ref_root()
+    return os.path.join(root, "src", "tinfer") if root else "/root/reference/pkg/src/tinfer"
+
+
+REF_SRC = _ref_src()
 
 
 def load(with_pruning: bool = True):

@@ -54,6 +54,18 @@ class CorrectnessError(TinferError):
     """An equivalence check failed; results must not be trusted or timed."""
 
 
+class BindingError(TinferError):
+    """Reference graph-optimizer error (graphopt); defined for ``except`` compatibility."""
+
+
+class GraphError(TinferError):
+    """Reference graph-optimizer error (graphopt); defined for ``except`` compatibility."""
+
+
+class PlanError(TinferError):
+    """Reference arena-planner error (graphopt); defined for ``except`` compatibility."""
+
+
 class DeviceError(TinferError):
     """The CUDA extension is missing, or a kernel launch / CUDA call failed."""
 

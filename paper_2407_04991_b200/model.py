@@ -27,6 +27,7 @@ import numpy as np
 from .errors import (
     CapacityError,
     ConfigError,
+    DimensionError,
     FormatError,
     ParameterError,
     PositionError,
@@ -361,33 +362,78 @@ class KVCache:
         self.capacity = capacity
         self.len = 0
         self._sess = None  # (DeviceModel, Session) bound on first use
+        self._own = None  # (k, v) device storage written before a session is bound
 
     def _session(self, dm):
         if self._sess is None or self._sess[0] is not dm:
             from .device import Session
-            kc = vc = None
+            kc, vc = self._own if self._own is not None else (None, None)
             if self._sess is not None:  # rebinding keeps the stored slots
                 kc, vc = self._sess[1].k_cache, self._sess[1].v_cache
             s = Session(dm, self.batch, self.capacity, 1, 1, logits=True, k_cache=kc, v_cache=vc)
             s.len = self.len
             self._sess = (dm, s)
+            self._own = None
         return self._sess[1]
 
-    def _storage(self, which: str) -> np.ndarray | None:
-        if self._sess is None:
-            return None
-        t = self._sess[1].k_cache if which == "k" else self._sess[1].v_cache
-        return t.cpu().numpy()
+    def _device_storage(self, create: bool = False):
+        """(k, v) device tensors [L, B, NH, cap, D] f16: the bound session's, or
+        storage of this cache alone (``write`` before any forward)."""
+        if self._sess is not None:
+            return self._sess[1].k_cache, self._sess[1].v_cache
+        if self._own is None and create:
+            import torch
+            from .errors import DeviceError
+            if not torch.cuda.is_available():
+                raise DeviceError("CUDA device required: the KV cache lives in device memory")
+            c = self.config
+            shape = (c.num_layers, self.batch, c.num_heads, self.capacity, c.head_dim)
+            self._own = (torch.zeros(shape, dtype=torch.float16, device="cuda"),
+                         torch.zeros(shape, dtype=torch.float16, device="cuda"))
+        return self._own if self._own is not None else (None, None)
+
+    def write(self, layer: int, k: np.ndarray, v: np.ndarray) -> None:
+        """Store f32 K/V rows [B, NH, T, D] at slots [len, len+T), rounded to f16
+        (model.py:326-342: saturating RNE); ``commit`` advances len."""
+        import torch
+        k, v = np.asarray(k, np.float32), np.asarray(v, np.float32)
+        c = self.config
+        want = (self.batch, c.num_heads, k.shape[2] if k.ndim == 4 else -1, c.head_dim)
+        if k.ndim != 4 or k.shape != want or v.shape != want:
+            raise DimensionError(f"write expects K/V of shape {list(want)}")
+        if not 0 <= layer < c.num_layers:
+            raise ParameterError(f"layer {layer} out of range")
+        lo, hi = self.len, self.len + k.shape[2]
+        if hi > self.capacity:
+            raise CapacityError(f"cache capacity {self.capacity} exceeded")
+        kc, vc = self._device_storage(create=True)
+        kc[layer, :, :, lo:hi] = torch.from_numpy(round_to(k, DType.F16)).to(kc.device)
+        vc[layer, :, :, lo:hi] = torch.from_numpy(round_to(v, DType.F16)).to(vc.device)
+
+    def commit(self, t: int) -> None:
+        self.len += t
+
+    def view(self, layer: int, length: int) -> tuple[np.ndarray, np.ndarray]:
+        """f32 copies of slots [0, length) of one layer, [B, NH, length, D]
+        (model.py:347-348; f16 -> f32 is exact)."""
+        kc, vc = self._device_storage()
+        c = self.config
+        if kc is None:
+            z = np.zeros((self.batch, c.num_heads, length, c.head_dim), np.float32)
+            return z, z.copy()
+        return (kc[layer, :, :, :length].float().cpu().numpy(), vc[layer, :, :, :length].float().cpu().numpy())
 
     def _accessor(self, which: str, layer: int) -> Tensor:
         c = self.config
-        arr = self._storage(which)
-        if arr is None:
-            arr = np.zeros((c.num_layers, self.batch, c.num_heads, self.capacity, c.head_dim), np.float16)
-        sel = arr[layer, 0]
+        kc, vc = self._device_storage()
+        t = kc if which == "k" else vc
+        if t is None:
+            sel = np.zeros((c.num_heads, self.capacity, c.head_dim), np.float16)
+        else:
+            sel = t[layer, 0].cpu().numpy()  # one layer of one sequence crosses the bus
         if c.dtype is DType.F32:
             return Tensor(sel.astype(np.float32), DType.F32)
-        return Tensor(sel.copy(), DType.F16)
+        return Tensor(sel, DType.F16)
 
     def keys(self, layer: int) -> Tensor:
         return self._accessor("k", layer)
@@ -396,10 +442,13 @@ class KVCache:
         return self._accessor("v", layer)
 
     def fingerprint(self) -> bytes:
-        """Filled-slot bytes in slot-major order (reference model.py:359-369)."""
-        ks, vs = self._storage("k"), self._storage("v")
-        if ks is None:
+        """Filled-slot bytes in slot-major order (reference model.py:359-369);
+        only the filled slots are copied to the host."""
+        kc, vc = self._device_storage()
+        if kc is None or self.len == 0:
             return b""
+        ks = kc[:, :, :, :self.len].cpu().numpy()
+        vs = vc[:, :, :, :self.len].cpu().numpy()
         if self.config.dtype is DType.F32:
             ks, vs = ks.astype(np.float32), vs.astype(np.float32)
         parts = []

@@ -137,3 +137,10 @@ def embed_ln(ids, pos, tok_emb, pos_emb, hidden, x, h=None, gamma=None, beta=Non
     d.ids_out = _ptr(ids_out)
     N.check(N.lib().tf_embed_ln(C.byref(d), _stream()), "tf_embed_ln")
     return x
+
+
+def warmup() -> None:
+    """Reference kernels.warmup() (kernels.py:236-252) JIT-compiles every numba
+    kernel up front; here the kernels are compiled ahead of time, so warming up
+    means loading the sm_100a library (raises if it is missing)."""
+    N.load_library()

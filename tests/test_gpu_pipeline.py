@@ -22,7 +22,7 @@ def test_run_sharded_cuda_workers_match_sequential(cuda_device):
     reqs = [reqs[sum(lens[:i]):sum(lens[:i + 1])] for i in range(len(lens))]
     settings = PL.PipelineSettings(max_batch_size=16, bucket_width=8, max_new_tokens=12)
     got, stats = PL.run_sharded(reqs, spec, settings, devices=["cuda:0", "cuda:0"], timeout=600)
-    seq, _ = PL.run_sequential(reqs, spec.build(), settings)
+    seq, _ = PL.run_sequential_ids(reqs, spec.build(), settings)
     assert got == seq
     assert len(stats.per_worker_seconds) == 2 and all(t > 0 for t in stats.per_worker_seconds)
     assert stats.generated_tokens == sum(len(g) - len(r) for g, r in zip(got, reqs))

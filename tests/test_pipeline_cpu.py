@@ -79,7 +79,7 @@ def _gloo_rank(rank, world, port, out_path):
     t = PL.max_over_ranks(float(rank + 1))
     merged = PL.gather_outputs(local, len(reqs), world)
     if rank == 0:
-        seq, _ = PL.run_sequential(reqs, model, settings, runner=cpu_runner)
+        seq, _ = PL.run_sequential_ids(reqs, model, settings, runner=cpu_runner)
         with open(out_path, "w") as fh:
             fh.write(f"{int(merged == seq)} {t}")
     dist.barrier()
@@ -103,7 +103,7 @@ def test_run_sharded_two_workers_matches_sequential():
     settings = PL.PipelineSettings(max_batch_size=8, bucket_width=4, max_new_tokens=5)
     got, stats = PL.run_sharded(reqs, spec, settings, devices=["cpu", "cpu"], runner=cpu_runner,
                                 timeout=300)
-    seq, _ = PL.run_sequential(reqs, spec.build(), settings, runner=cpu_runner)
+    seq, _ = PL.run_sequential_ids(reqs, spec.build(), settings, runner=cpu_runner)
     assert got == seq
     assert stats.generated_tokens == 30 * 5 - sum(  # eos may cut rows short
         5 - (len(s) - len(r)) for s, r in zip(seq, reqs))
