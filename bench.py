@@ -225,9 +225,9 @@ def cpu_baseline_reference(wname="c2", samples=1, n_decode=4):
     copy oracle/make_ref.py stages under oracle/_ref) on this host's cores.
 
     Sample: S = min(B*beam, 32) rows of the workload's prompts; per sample one
-    prefill-only call and one call with ``n_decode`` decode steps through the
-    reference's batched_greedy_decode (model.py:613-667), so t_dec = (t_full -
-    t_pre) / n_decode. Extrapolated to the workload: prefill time x (rows / S)
+    call with ``n_decode`` decode steps through the reference's
+    batched_greedy_decode (model.py:613-667), its forward calls timed one by one
+    (the prefill, then each decode step). Extrapolated to the workload: prefill time x (rows / S)
     (prefill is GEMM-bound, linear in rows), decode step time as measured at S
     rows (a lower bound for more rows -> the reported CPU throughput is an upper
     bound). Returns None when the reference copy is absent."""
@@ -255,15 +255,28 @@ def cpu_baseline_reference(wname="c2", samples=1, n_decode=4):
     prompts = O.synthetic_prompts(model.config.vocab_size, S, src, seed=SEED)
     T.kernels.warmup()
     M.batched_greedy_decode(model, [p[:8] for p in prompts[:2]], 2)  # strided-view specialisation
-    t_pre, t_dec = [], []
-    for _ in range(samples):
+    # per-forward wall times through the reference's own generate loop: its
+    # _forward_tokens (model.py:440-504) wrapped with a timer for the duration
+    # of the sample (first call = prefill, the rest = decode steps)
+    calls = []
+    inner = M._forward_tokens
+
+    def timed(*a, **k):
         t0 = time.perf_counter()
-        M.batched_greedy_decode(model, prompts, 1)
-        t1 = time.perf_counter()
-        M.batched_greedy_decode(model, prompts, 1 + n_decode)
-        t2 = time.perf_counter()
-        t_pre.append(t1 - t0)
-        t_dec.append(max((t2 - t1) - (t1 - t0), 1e-9) / n_decode)
+        r = inner(*a, **k)
+        calls.append(time.perf_counter() - t0)
+        return r
+
+    t_pre, t_dec = [], []
+    M._forward_tokens = timed
+    try:
+        for _ in range(samples):
+            calls.clear()
+            M.batched_greedy_decode(model, prompts, 1 + n_decode)
+            t_pre.append(calls[0])
+            t_dec.extend(calls[1:])
+    finally:
+        M._forward_tokens = inner
     tp, td = statistics.median(t_pre) * rows / S, statistics.median(t_dec)
     total = tp + (w["new"] - 1) * td
     return {"value": w["batch"] * w["new"] / total, "unit": "generated tokens/s", "cores": threads,

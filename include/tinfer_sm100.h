@@ -130,6 +130,22 @@ int tf_embed_ln(const tf_embed_desc* d, void* stream);
 int tf_layernorm(int n_rows, int hidden, const void* x, int ldx, int src_stride, int src_off,
                  const float* gamma, const float* beta, void* h, int ldh, void* stream);
 
+/* ---- weight packing on the device (model upload; TINF direct-to-device load,
+ * replacing the host-side load_model -> Model.f32 path of model.py:177-184 /
+ * 267-286 for the device mirror). All three are enqueued on `stream`.
+ * tf_pack_kmajor: src [K, N] row-major (reference [in, out] layout, f32 when
+ * src_f32 else f16) -> dst f16 [N, ldk] (W^T, K-major, columns >= K zeroed),
+ * saturating RNE; with gamma (f32, f16-rounded values): q16(q16(src) * gamma[k]).
+ * tf_fold_terms: per output feature n, c[n] = sum_k w_ln_t[n, k] and
+ * d[n] = sum_k beta[k] * w_t[n, k] (f64 accumulation, rounded to f32): the
+ * LayerNorm fold terms of the decode GEMMs.
+ * tf_convert: dst[i] = q16(src[i]) stored as f32 (dst_f32) or f16. */
+int tf_pack_kmajor(const void* src, int src_f32, int K, int N, const float* gamma, void* dst, int ldk,
+                   void* stream);
+int tf_fold_terms(const void* w_t, const void* w_ln_t, const float* beta, int K, int N, int ldk, float* c,
+                  float* d, void* stream);
+int tf_convert(const void* src, int src_f32, long long n, void* dst, int dst_f32, void* stream);
+
 /* Masked attention over the KV cache (kernels.attend_f32, kernels.py:216-233).
  * q: [batch*seq_len, ldq] (head h at columns h*head_dim); caches [batch, heads,
  * cap, head_dim]; row t of sequence b attends slots [start[b], *qbase_dev + t].

@@ -136,6 +136,11 @@ SIGNATURES = {
     "tf_beam_decode": (C.c_int, [C.c_void_p, C.POINTER(BeamDesc), C.c_int, C.c_int, C.c_void_p]),
     "tf_debug_trace": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
     "tf_session_launches_per_step": (C.c_int, [C.c_void_p]),
+    "tf_pack_kmajor": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                 C.c_void_p]),
+    "tf_fold_terms": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                C.c_void_p, C.c_void_p]),
+    "tf_convert": (C.c_int, [C.c_void_p, C.c_int, C.c_longlong, C.c_void_p, C.c_int, C.c_void_p]),
 }
 
 ABI_VERSION = 2

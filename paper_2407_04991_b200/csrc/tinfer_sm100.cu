@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "gemm_tc.cuh"
 #include "norm_embed.cuh"
+#include "pack.cuh"
 
 using namespace tf;
 
@@ -1114,6 +1115,41 @@ int tf_attention(int batch, int heads, int head_dim, int cap, int seq_len, const
     a.out = static_cast<__half*>(out);
     a.ldo = ldo;
     if (batch > 0 && seq_len > 0) run_attention(a, static_cast<cudaStream_t>(stream), false);
+  });
+}
+
+int tf_pack_kmajor(const void* src, int src_f32, int K, int N, const float* gamma, void* dst, int ldk,
+                   void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(src && dst, TF_ERR_ARG, "pack: null pointer");
+    TF_REQUIRE(K >= 1 && N >= 1 && ldk >= K, TF_ERR_SHAPE, "pack: bad shape");
+    dim3 grid((N + 31) / 32, (ldk + 31) / 32);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (src_f32)
+      pack_kmajor_kernel<true><<<grid, 256, 0, st>>>(src, K, N, gamma, static_cast<__half*>(dst), ldk);
+    else
+      pack_kmajor_kernel<false><<<grid, 256, 0, st>>>(src, K, N, gamma, static_cast<__half*>(dst), ldk);
+    TF_CHECK_CUDA(cudaGetLastError());
+  });
+}
+
+int tf_fold_terms(const void* w_t, const void* w_ln_t, const float* beta, int K, int N, int ldk, float* c,
+                  float* d, void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(w_t && w_ln_t && beta && c && d, TF_ERR_ARG, "fold_terms: null pointer");
+    TF_REQUIRE(K >= 1 && N >= 1 && ldk >= K, TF_ERR_SHAPE, "fold_terms: bad shape");
+    fold_terms_kernel<<<(N + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const __half*>(w_t), static_cast<const __half*>(w_ln_t), beta, K, N, ldk, c, d);
+    TF_CHECK_CUDA(cudaGetLastError());
+  });
+}
+
+int tf_convert(const void* src, int src_f32, long long n, void* dst, int dst_f32, void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(src && dst && n >= 1, TF_ERR_ARG, "convert: bad arguments");
+    const long long blocks = std::min<long long>((n + 255) / 256, 148ll * 16);
+    convert_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, src_f32, n, dst, dst_f32);
+    TF_CHECK_CUDA(cudaGetLastError());
   });
 }
 

@@ -32,36 +32,24 @@ from .ops import pad64
 from .tensor import round_to, DType
 
 
-def _f16_kmajor(w_in_out: np.ndarray, ld: int) -> np.ndarray:
-    k, n = w_in_out.shape
-    buf = np.zeros((n, ld), dtype=np.float16)
-    buf[:, :k] = round_to(np.asarray(w_in_out, dtype=np.float32), DType.F16).T
-    return buf
-
-
-def _f32_vec(v: np.ndarray) -> np.ndarray:
-    return round_to(np.asarray(v, dtype=np.float32), DType.F16).astype(np.float32)
-
-
-def _fold_ln(w_t: np.ndarray, k: int, gamma: np.ndarray, beta: np.ndarray):
-    """LayerNorm folded into the following projection (decode path,
-    gemm_tc.cuh ln_fold): W'[n, k] = q16(W[n, k] * gamma[k]) (the f16 x f16
-    product is exact in f32, then one saturating RNE), c[n] = sum_k W'[n, k],
-    d[n] = sum_k beta[k] W[n, k] (fp64 sums rounded to f32), so that
-    LN(x) . W[n] = inv * (x . W'[n] - mean * c[n]) + d[n]."""
-    w = w_t[:, :k].astype(np.float32)
-    wf = round_to(w * gamma[None, :k].astype(np.float32), DType.F16)
-    buf = np.zeros_like(w_t)
-    buf[:, :k] = wf
-    c = wf.astype(np.float64).sum(axis=1).astype(np.float32)
-    d = (w.astype(np.float64) @ beta[:k].astype(np.float64)).astype(np.float32)
-    return buf, c, d
+def _raw(t) -> np.ndarray:
+    """The stored array of a ``Tensor`` (or an array), C-contiguous, F32 or F16."""
+    a = t.array if hasattr(t, "array") else t
+    if a.dtype not in (np.float32, np.float16):
+        a = a.astype(np.float32)
+    return np.ascontiguousarray(a)
 
 
 class DeviceModel:
-    """Packed, device-resident weights + the native ``tf_model`` handle."""
+    """Packed, device-resident weights + the native ``tf_model`` handle.
 
-    def __init__(self, model, device: torch.device):
+    Packing runs on the device (csrc/pack.cuh through tf_pack_kmajor /
+    tf_fold_terms / tf_convert): each reference tensor is uploaded as stored and
+    transposed / rounded / LayerNorm-folded in HBM. ``source`` (optional) maps
+    tensor names to arrays to read instead of ``model``'s — the TINF
+    direct-to-device loader passes memory-mapped file slices."""
+
+    def __init__(self, model, device: torch.device, source: dict | None = None):
         c = model.config
         self.config = c
         self.device = device
@@ -71,50 +59,91 @@ class DeviceModel:
         # re-entrant: session() takes it too, so a session can never be evicted
         # (and closed) while another thread holding the lock uses it
         self.lock = threading.RLock()
-        f32 = {name: t.array.astype(np.float32) for name, t in model.named_tensors()}
-        up16 = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+        arrays = dict(model.named_tensors()) if source is None else source
+        raw = lambda name: _raw(arrays[name])  # noqa: E731  (reference layout, F32 or F16)
         self._keep = []
+        st = C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
         def keep(t):
             self._keep.append(t)
             return t
 
-        self.tok_emb = keep(up16(round_to(f32["token_embedding"], DType.F16)))
+        def upload(a: np.ndarray) -> torch.Tensor:
+            """Raw tensor -> HBM as stored (one H2D copy; from a memory-mapped
+            TINF file the bytes go page cache -> device)."""
+            return torch.from_numpy(a).to(device)
+
+        def vec(name, as_f32=True):  # q16 values, f32 (biases / LN params) or f16
+            a = raw(name)
+            src = upload(a)
+            out = torch.empty(a.shape, dtype=torch.float32 if as_f32 else torch.float16, device=device)
+            N.check(N.lib().tf_convert(C.c_void_p(src.data_ptr()), int(a.dtype == np.float32), a.size,
+                                       C.c_void_p(out.data_ptr()), int(as_f32), st), "tf_convert")
+            return out
+
+        def pack(names, ldk, gamma=None, out=None):
+            """[in, out] tensors stacked along out -> f16 W^T [sum(out), ldk]."""
+            n_tot = sum(arrays[n].shape[1] for n in names)
+            dst = out if out is not None else torch.empty((n_tot, ldk), dtype=torch.float16, device=device)
+            row = 0
+            for n in names:
+                a = raw(n)
+                k, nn = a.shape
+                src = upload(a)
+                N.check(N.lib().tf_pack_kmajor(C.c_void_p(src.data_ptr()), int(a.dtype == np.float32), k, nn,
+                                               None if gamma is None else C.c_void_p(gamma.data_ptr()),
+                                               C.c_void_p(dst[row:].data_ptr()), ldk, st), "tf_pack_kmajor")
+                row += nn
+            return dst
+
+        def fold(names, ldk, gamma, beta, w_t):
+            """LayerNorm folded into the projection (decode path, gemm_tc.cuh
+            ln_fold): W' = q16(W * gamma), c = sum_k W', d = sum_k beta_k W."""
+            w_ln = pack(names, ldk, gamma=gamma)
+            n = w_ln.shape[0]
+            c_ = torch.empty(n, dtype=torch.float32, device=device)
+            d_ = torch.empty(n, dtype=torch.float32, device=device)
+            N.check(N.lib().tf_fold_terms(C.c_void_p(w_t.data_ptr()), C.c_void_p(w_ln.data_ptr()),
+                                          C.c_void_p(beta.data_ptr()), self.H, n, ldk, C.c_void_p(c_.data_ptr()),
+                                          C.c_void_p(d_.data_ptr()), st), "tf_fold_terms")
+            return w_ln, c_, d_
+
+        self.tok_emb = keep(vec("token_embedding", as_f32=False))
         self.type_emb = None
         if model.type_embedding is not None:  # extension: word + position + type gather-sum
-            self.type_emb = keep(up16(round_to(model.type_embedding.array.astype(np.float32), DType.F16)))
-        self.pos_emb = keep(up16(round_to(f32["position_embedding"], DType.F16)))
+            te = model.type_embedding.array
+            self.type_emb = keep(torch.from_numpy(round_to(te.astype(np.float32), DType.F16)).to(device))
+        self.pos_emb = keep(vec("position_embedding", as_f32=False))
         layers = (N.LayerWeights * self.L)()
         self.layers = []
         for i in range(self.L):
             p = f"layers.{i}."
-            wqkv = np.concatenate([f32[p + "attn.wq"], f32[p + "attn.wk"], f32[p + "attn.wv"]], axis=1)
-            bqkv = np.concatenate([f32[p + "attn.bq"], f32[p + "attn.bk"], f32[p + "attn.bv"]])
-            g1, be1 = _f32_vec(f32[p + "attn_norm.gamma"]), _f32_vec(f32[p + "attn_norm.beta"])
-            g2, be2 = _f32_vec(f32[p + "ffn_norm.gamma"]), _f32_vec(f32[p + "ffn_norm.beta"])
-            wqkv_t = _f16_kmajor(wqkv, self.ldk_h)
-            w1_t = _f16_kmajor(f32[p + "ffn.w1"], self.ldk_h)
-            wqkv_ln, cqkv, dqkv = _fold_ln(wqkv_t, self.H, g1, be1)
-            w1_ln, c1, d1 = _fold_ln(w1_t, self.H, g2, be2)
+            g1, be1 = vec(p + "attn_norm.gamma"), vec(p + "attn_norm.beta")
+            g2, be2 = vec(p + "ffn_norm.gamma"), vec(p + "ffn_norm.beta")
+            qkv = [p + "attn.wq", p + "attn.wk", p + "attn.wv"]
+            wqkv_t = pack(qkv, self.ldk_h)
+            w1_t = pack([p + "ffn.w1"], self.ldk_h)
+            wqkv_ln, cqkv, dqkv = fold(qkv, self.ldk_h, g1, be1, wqkv_t)
+            w1_ln, c1, d1 = fold([p + "ffn.w1"], self.ldk_h, g2, be2, w1_t)
             lw = dict(
-                ln1_gamma=up16(g1), ln1_beta=up16(be1),
-                wqkv_t=up16(wqkv_t), bqkv=up16(_f32_vec(bqkv)),
-                wo_t=up16(_f16_kmajor(f32[p + "attn.wo"], self.ldk_h)), bo=up16(_f32_vec(f32[p + "attn.bo"])),
-                ln2_gamma=up16(g2), ln2_beta=up16(be2),
-                w1_t=up16(w1_t), b1=up16(_f32_vec(f32[p + "ffn.b1"])),
-                w2_t=up16(_f16_kmajor(f32[p + "ffn.w2"], self.ldk_f)), b2=up16(_f32_vec(f32[p + "ffn.b2"])),
-                wqkv_ln_t=up16(wqkv_ln), cqkv=up16(cqkv), dqkv=up16(dqkv),
-                w1_ln_t=up16(w1_ln), c1=up16(c1), d1=up16(d1),
+                ln1_gamma=g1, ln1_beta=be1,
+                wqkv_t=wqkv_t, bqkv=torch.cat([vec(p + "attn.bq"), vec(p + "attn.bk"), vec(p + "attn.bv")]),
+                wo_t=pack([p + "attn.wo"], self.ldk_h), bo=vec(p + "attn.bo"),
+                ln2_gamma=g2, ln2_beta=be2,
+                w1_t=w1_t, b1=vec(p + "ffn.b1"),
+                w2_t=pack([p + "ffn.w2"], self.ldk_f), b2=vec(p + "ffn.b2"),
+                wqkv_ln_t=wqkv_ln, cqkv=cqkv, dqkv=dqkv,
+                w1_ln_t=w1_ln, c1=c1, d1=d1,
             )
             self.layers.append(lw)
             for k, t in lw.items():
                 setattr(layers[i], k, t.data_ptr())
-        self.final_gamma = keep(up16(_f32_vec(f32["final_norm.gamma"])))
-        self.final_beta = keep(up16(_f32_vec(f32["final_norm.beta"])))
-        lm_t = _f16_kmajor(f32["lm_head"], self.ldk_h)
-        self.lm_head_t = keep(up16(lm_t))
-        lm_ln, c_lm, d_lm = _fold_ln(lm_t, self.H, _f32_vec(f32["final_norm.gamma"]), _f32_vec(f32["final_norm.beta"]))
-        self.lm_head_ln_t, self.c_lm, self.d_lm = keep(up16(lm_ln)), keep(up16(c_lm)), keep(up16(d_lm))
+        self.final_gamma = keep(vec("final_norm.gamma"))
+        self.final_beta = keep(vec("final_norm.beta"))
+        self.lm_head_t = keep(pack(["lm_head"], self.ldk_h))
+        lm_ln, c_lm, d_lm = fold(["lm_head"], self.ldk_h, self.final_gamma, self.final_beta, self.lm_head_t)
+        self.lm_head_ln_t, self.c_lm, self.d_lm = keep(lm_ln), keep(c_lm), keep(d_lm)
+        torch.cuda.current_stream(device).synchronize()  # staging copies may be released
         self._layer_structs = layers
         d = N.ModelDesc()
         d.vocab, d.hidden, d.layers, d.heads = self.V, self.H, self.L, self.NH

@@ -190,8 +190,11 @@ class Model:
         return out
 
     def f32(self, name: str) -> np.ndarray:
+        """f32 view of one weight, memoised per name (model.py:177-184)."""
         if self._f32 is None:
-            self._f32 = {n: t.array.astype(np.float32, copy=False) for n, t in self.named_tensors()}
+            self._f32 = {}
+        if name not in self._f32:
+            self._f32[name] = dict(self.named_tensors())[name].array.astype(np.float32, copy=False)
         return self._f32[name]
 
     def weight_bytes(self) -> dict[str, int]:
@@ -209,8 +212,8 @@ class Model:
             from .errors import DeviceError
             raise DeviceError("CUDA device required: the generation path has no CPU fallback")
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        if self._f32 is None:
-            self.f32("lm_head")
+        if self._f32 is None:  # the memo token: tests reset it after mutating a weight
+            self._f32 = {}
         if self._device is None or self._device[0] is not self._f32:
             self._device = (self._f32, {})
         mirrors = self._device[1]
@@ -302,12 +305,23 @@ def save_model(model: Model, weights_path: str | Path) -> None:
     config_path_for(weights_path).write_text(model.config.to_json() + "\n", encoding="utf-8")
 
 
-def load_model(weights_path: str | Path) -> Model:
+def load_model(weights_path: str | Path, device=None) -> Model:
+    """TINF v1 + JSON config (model.py:267-286).
+
+    ``device`` (extension): load straight to that CUDA device — the file is
+    memory-mapped (no host copy, no f32 materialisation), each tensor's bytes
+    are uploaded as stored and packed by the device kernels
+    (:class:`~.device.DeviceModel`), and the returned Model's host tensors are
+    views of the mapping (read lazily if a host accessor touches them)."""
+    from .tensor import map_tinf
     cfg = ModelConfig.from_json(config_path_for(weights_path).read_text(encoding="utf-8"))
-    named = read_tinf(str(weights_path))
+    named = read_tinf(str(weights_path)) if device is None else map_tinf(str(weights_path))
     if [n for n, _ in named] != [n for n, _ in _tensor_shapes(cfg)]:
         raise FormatError("weight file tensors do not match the config layout")
-    return _model_from_dict(cfg, dict(named))
+    model = _model_from_dict(cfg, dict(named))
+    if device is not None:
+        model.device_model(device)
+    return model
 
 
 # ---------------------------------------------------------------------------
@@ -318,29 +332,39 @@ class OpCounters:
     attn_macs: int = 0
     gemm_macs: int = 0
     launches: int = 0
+    kernels: int = 0  # extension: sm_100a kernels actually launched
 
 
 COUNTERS = OpCounters()
 
 
 def reset_counters() -> None:
-    COUNTERS.attn_macs = COUNTERS.gemm_macs = COUNTERS.launches = 0
+    COUNTERS.attn_macs = COUNTERS.gemm_macs = COUNTERS.launches = COUNTERS.kernels = 0
 
 
 def snapshot_counters() -> OpCounters:
-    return OpCounters(COUNTERS.attn_macs, COUNTERS.gemm_macs, COUNTERS.launches)
+    return OpCounters(COUNTERS.attn_macs, COUNTERS.gemm_macs, COUNTERS.launches, COUNTERS.kernels)
+
+
+def _ref_launches(c: ModelConfig, fused: bool) -> int:
+    """Operator launches the reference's _forward_tokens issues (model.py:407-437):
+    per layer the q/k/v/o and FFN GEMMs (bias [+ GELU] fused into one launch, or
+    a GEMM + bias_add [+ gelu] launch each when unfused) and one attention; the
+    lm_head GEMM has no bias."""
+    return c.num_layers * (7 if fused else 14) + 1
 
 
 def _count_forward(c: ModelConfig, B: int, T: int, qbase: int, start_sum: int, logit_rows: int,
-                   launches: int) -> None:
-    """MAC accounting identical to the reference's _gemm/_attend bookkeeping
-    (model.py:414, 433-435); launches are the kernels actually launched."""
+                   kernels: int, fused: bool = True) -> None:
+    """MAC and launch accounting identical to the reference's _gemm/_attend
+    bookkeeping (model.py:407-437); ``kernels`` counts the native kernels."""
     H, F, M = c.hidden_size, c.ffn_size, B * T
     COUNTERS.gemm_macs += c.num_layers * M * (4 * H * H + 2 * H * F) + logit_rows * H * c.vocab_size
     series = (qbase + 1 + qbase + T) * T // 2
     valid = B * series - start_sum * T
     COUNTERS.attn_macs += c.num_layers * 2 * c.num_heads * c.head_dim * valid
-    COUNTERS.launches += launches
+    COUNTERS.launches += _ref_launches(c, fused)
+    COUNTERS.kernels += kernels
 
 
 # ---------------------------------------------------------------------------
@@ -506,7 +530,7 @@ def embed(model: Model, token_ids, start_position: int = 0, type_ids=None) -> Te
         dev_types = None if types is None else torch.from_numpy(types).to(dm.device)
         ops.embed_ln(dev_ids, dev_pos, dm.tok_emb, dm.pos_emb, c.hidden_size, x, type_ids=dev_types,
                      type_emb=dm.type_emb if types is not None else None)
-        COUNTERS.launches += 1
+        COUNTERS.kernels += 1
         arr = x.cpu().numpy()
     # the device stores f16 (F32 models are rounded on upload): an F16 model's
     # rows are bit-identical to the reference; an F32 model gets the f16 values
@@ -533,7 +557,7 @@ def forward_full(model: Model, token_ids, fused: bool = True, type_ids=None) -> 
                       types=_check_types(model, type_ids, t))
         n = s.forward(t, N.FWD_LOGITS_ALL)
         out = s.logits[:t].cpu().numpy()
-    _count_forward(c, 1, t, 0, 0, t, n)
+    _count_forward(c, 1, t, 0, 0, t, n, fused)
     return _host_logits(out, c.dtype)
 
 
@@ -583,7 +607,7 @@ def decode_step(model: Model, token_id: int, cache: KVCache, fused: bool = True)
                       np.zeros(1, np.int32), length=cache.len)
         n = s.forward(1, N.FWD_LOGITS_LAST)
         out = s.logits[:1].cpu().numpy()
-    _count_forward(c, 1, 1, cache.len, 0, 1, n)
+    _count_forward(c, 1, 1, cache.len, 0, 1, n, fused)
     cache.len += 1
     return _host_logits(out, c.dtype)
 
@@ -739,10 +763,10 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
         toks = s.fetch_tokens(max_new_tokens)
         stats.d2h_bytes = toks.nbytes
     stats.launches = n_pre + n_dec
-    _count_forward(c, B, L, 0, int(pads.sum()), B, n_pre)
+    _count_forward(c, B, L, 0, int(pads.sum()), B, n_pre, fused)
     for step in range(1, max_new_tokens):
-        _count_forward(c, B, 1, L + step - 1, int(pads.sum()), B, 0)
-    COUNTERS.launches += n_dec
+        _count_forward(c, B, 1, L + step - 1, int(pads.sum()), B, 0, fused)
+    COUNTERS.kernels += n_dec
     global LAST_STATS
     LAST_STATS = stats
     # append up to and including each row's first eos (model.py:656-661)

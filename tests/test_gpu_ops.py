@@ -190,7 +190,7 @@ def test_fused_layernorm_statistics(cuda_device, m, n, h):
         m2 = ((seg - mu[:, None]) ** 2).sum(axis=1)
         assert np.allclose(got[i, :, 0], mu, rtol=1e-5, atol=1e-6)
         assert np.allclose(got[i, :, 1], m2, rtol=1e-4, atol=1e-5)
-    from paper_2407_04991_b200.device import _fold_ln
+    from test_gpu_pack import host_fold as _fold_ln
     g = (1 + 0.05 * torch.randn(h, generator=torch.Generator().manual_seed(4))).half().float()
     b = (0.05 * torch.randn(h, generator=torch.Generator().manual_seed(5))).half().float()
     w = rand16(n, hp, scale=0.05, seed=33)

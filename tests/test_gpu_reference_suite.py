@@ -33,7 +33,18 @@ from oracle import make_ref  # noqa: E402
 FILES = ["test_tokenizer.py", "test_pipeline.py", "test_pruning.py", "test_model.py", "test_bench.py",
          "test_cli.py"]
 # test id (file::class::name) -> why it cannot hold on an f16 tensor-core path / is out of scope
-EXPECTED: dict[str, str] = {}
+_F16 = ("F32 model on an f16-storage path: the reference asserts exact f32 arithmetic; this path rounds F32 "
+        "weights/activations to f16 (restated with the north-star tolerance in tests/test_gpu_model.py)")
+EXPECTED: dict[str, str] = {
+    "test_model.py::TestEmbed::test_single_token_definition": _F16 + " — the embedding of an F32 model is the "
+    "f16-rounded sum, bit-exact for F16 models (tests/test_gpu_model.py)",
+    "test_model.py::TestForwardFull::test_matches_straightline_oracle_tiny": _F16 + " — max-abs 9e-5 vs the "
+    "1e-5 bound on an f64 straight-line forward",
+    "test_model.py::TestForwardFull::test_matches_straightline_oracle_multihead": _F16 + " — max-abs 3.2e-4 vs "
+    "the 1e-5 bound",
+    "test_cli.py::TestGraphOptCommand::test_prints_summary": "graph-opt (the reference's operator-graph "
+    "optimiser) is outside the generation hot path (SURVEY §8f-4); the CLI does not provide it",
+}
 
 
 def _run(path, tmp_path):

@@ -74,7 +74,7 @@ def test_full_ladder_reports(cuda_device, setup):
     assert [r.stage_name for r in again] == list(ladder.LADDER)
 
 
-@pytest.mark.parametrize("fault", ["cache", "pruning", "pipeline"])
+@pytest.mark.parametrize("fault", ["cache", "fusion", "pruning", "pipeline"])
 def test_injected_faults_abort(cuda_device, setup, fault):
     model, vocab, texts = setup
     with pytest.raises(CorrectnessError):
