@@ -895,6 +895,220 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const AttnArgs a)
   }
 }
 
+// ------------------------------------------------------------------ prefill, tcgen05
+// head_dim 64. One CTA = 128 query rows of one (head, sequence); query row r =
+// TMEM lane r. Key chunks of 64 slots aligned to start[b] (as in every other
+// attention kernel: a row's arithmetic never depends on its batch's padding).
+// One pass over the chunks (flash form, the tensor-core analogue of
+// attn_prefill_mma_kernel):
+//   S_j = Q K_j^T   tcgen05.mma kind::f16 M=128 N=64 K=64, f32 in TMEM (issued
+//                   as soon as every thread has read S_{j-1}, so it runs while
+//                   chunk j-1's P is computed; 128 TMEM columns per CTA keep
+//                   three CTAs per SM);
+//   P_j = exp(s - m) with a per-row reference max m that is raised only when a
+//        chunk's max exceeds it by more than kTcRescale (then O and the sums
+//        are rescaled in place: tcgen05.ld / st of the O columns), rounded to
+//        f16 into a K-major SW128 tile;
+//   O  += P_j V_j   tcgen05.mma with V read MN-major (the cache's [slot][d]
+//                   rows, no transpose);
+//   out = q16(O / sum).
+// 8 warps: warps w and w + 4 share TMEM lane quadrant w % 4 and take the column
+// halves w / 4 of every chunk (and of O); the halves of a row agree on m
+// through shared memory once per chunk.
+constexpr int kTcRows = 128, kTcKeys = 64, kTcThreads = 256;
+constexpr int kTcTile = 128 * 128;  // Q or P tile bytes (128 rows x 64 f16)
+constexpr int kTcChunk = 64 * 128;  // K or V chunk bytes (64 slots x 64 f16)
+constexpr size_t kTcSmem = 1024 + 2 * kTcTile + 4 * kTcChunk + 64 + 2 * 128 * 8;
+constexpr float kTcRescale = 5.0f;  // P <= e^5 between rescales
+
+__device__ __forceinline__ uint32_t sw128_off(int row, int chunk16) {  // byte offset of 16-B chunk
+  return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((chunk16 ^ (row & 7)) << 4));
+}
+
+__global__ void __launch_bounds__(kTcThreads) attn_prefill_tc_kernel(const AttnArgs a) {
+  extern __shared__ uint8_t tc_smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* qs = sm;
+  uint8_t* ps = sm + kTcTile;
+  uint8_t* kbuf = sm + 2 * kTcTile;                // [2][kTcChunk]
+  uint8_t* vbuf = sm + 2 * kTcTile + 2 * kTcChunk;  // [2][kTcChunk]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 2 * kTcTile + 4 * kTcChunk);  // [0]: S, [2]: PV
+  float* stat = reinterpret_cast<float*>(sm + 2 * kTcTile + 4 * kTcChunk + 64);   // [2 halves][128 rows]
+  __shared__ uint32_t tmem_slot;
+  constexpr int D = 64;
+  const int qblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbar0 = smem_u32(bar), pvbar = smem_u32(bar + 2);
+  if (tid == 0) {
+    mbar_init(sbar0, 1);
+    mbar_init(sbar0 + 8, 1);
+    mbar_init(pvbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(smem_u32(&tmem_slot), 128);  // S [0,64) O [64,128)
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+  const int qbase = *a.qbase_dev;
+  const int lo = a.start[b];
+  const int t0 = qblk * kTcRows;
+  const int rows = min(kTcRows, a.T - t0);
+  const int hi_blk = qbase + t0 + rows - 1;
+  const int nch = hi_blk >= lo ? (hi_blk - lo) / kTcKeys + 1 : 0;
+  const size_t head_off = ((size_t)b * a.NH + h) * a.cap * D;
+  const __half* K = a.kc + head_off;
+  const __half* V = a.vc + head_off;
+  for (int i = tid; i < kTcRows * 8; i += kTcThreads) {
+    const int r = i >> 3, c = i & 7;
+    const bool ok = r < rows;
+    cp_async16(smem_u32(qs + sw128_off(r, c)),
+               ok ? (const void*)(a.q + (size_t)(b * a.T + t0 + r) * a.ldq + h * D + c * 8) : (const void*)a.q, ok);
+  }
+  auto load = [&](const __half* src, uint8_t* base, int j) {  // one 64-slot chunk, rows = slots
+    for (int i = tid; i < kTcKeys * 8; i += kTcThreads) {
+      const int kk = i >> 3, c = i & 7, slot = lo + j * kTcKeys + kk;
+      const bool ok = slot <= hi_blk && slot < a.cap;
+      cp_async16(smem_u32(base + sw128_off(kk, c)), ok ? (const void*)(src + (size_t)slot * D + c * 8) : (const void*)src,
+                 ok);
+    }
+  };
+  const int r = (warp & 3) * 32 + lane;  // query row = TMEM lane
+  const int half = warp >> 2;            // column half of each chunk and of O
+  const bool row_ok = r < rows;
+  const int hi_r = qbase + t0 + r;  // last visible slot of this row
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(32 * half);
+  const uint32_t idesc = idesc_f16_m128(64);
+  const uint32_t idesc_pv = idesc | (1u << 16);  // B (= V [slot][d]) MN-major
+  uint32_t sph = 0u, pvph = 0u;
+  auto issue_qk = [&](int j) {  // S = Q K_j^T (tid 0)
+    if (tid == 0) {
+      tc_fence_after();
+      const uint64_t da = umma_desc_sw128(smem_u32(qs));
+      const uint64_t db = umma_desc_sw128(smem_u32(kbuf + (j & 1) * kTcChunk));
+#pragma unroll
+      for (int k = 0; k < D / 16; ++k) tc_mma_f16(tmem, da + 2 * k, db + 2 * k, idesc, k != 0 ? 1u : 0u);
+      tc_commit(sbar0);
+    }
+  };
+  auto publish = [&]() {  // this thread's cp.async data and smem stores -> visible to the tensor core
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+  };
+  int pv_waited = 0;  // PV commits observed
+  auto wait_pv = [&](int k) {
+    while (pv_waited <= k) {
+      mbar_wait(pvbar, pvph);
+      pvph ^= 1u;
+      ++pv_waited;
+    }
+    tc_fence_after();
+  };
+  float m = -INFINITY, l = 0.0f;  // reference max of the row; exp-sum of this half's columns
+  if (nch > 0) {
+    load(K, kbuf, 0);
+    load(V, vbuf, 0);
+  }
+  if (nch > 1) load(K, kbuf + kTcChunk, 1);
+  publish();
+  if (nch > 0) issue_qk(0);
+  for (int j = 0; j < nch; ++j) {
+    mbar_wait(sbar0, sph);
+    sph ^= 1u;
+    tc_fence_after();
+    float s[32];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      float v[16];
+      tmem_ld16(trow + (uint32_t)(16 * q), v);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int slot = lo + j * kTcKeys + 32 * half + 16 * q + e;
+        s[16 * q + e] = (row_ok && slot <= hi_r) ? __fmul_rn(v[e], a.scale) : -INFINITY;
+      }
+    }
+    float cm = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) cm = fmaxf(cm, s[e]);
+    stat[half * 128 + r] = cm;
+    if (j > 0) wait_pv(j - 1);  // the P tile, V buffer (j - 1) & 1 and O are stable
+    publish();                  // S read by all; K(j+1) and V(j) landed
+    if (j + 1 < nch) issue_qk(j + 1);  // runs while P(j) is computed
+    cm = fmaxf(cm, stat[(half ^ 1) * 128 + r]);  // the row's chunk max (both halves)
+    const bool raise = cm != -INFINITY && (m == -INFINITY || cm > m + kTcRescale);
+    float alpha = 1.0f;
+    if (raise) {
+      alpha = m == -INFINITY ? 0.0f : expf(__fsub_rn(m, cm));
+      l = __fmul_rn(l, alpha);
+      m = cm;
+    }
+    if (j > 0 && __any_sync(0xffffffffu, raise)) {  // rescale this warp's O rows (warp-collective TMEM ops)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        float v[16];
+        tmem_ld16(trow + 64u + (uint32_t)(16 * q), v);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = __fmul_rn(v[e], alpha);
+        tmem_st16(trow + 64u + (uint32_t)(16 * q), v);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float pv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float x = s[8 * c + e];
+        pv[e] = x == -INFINITY ? 0.0f : expf(__fsub_rn(x, m));
+        l = __fadd_rn(l, pv[e]);
+      }
+      *reinterpret_cast<uint4*>(ps + sw128_off(r, 4 * half + c)) = pack8(pv);
+    }
+    publish();  // P(j) written, V(j) landed, O rescaled
+    if (tid == 0) {
+      tc_fence_after();
+      const uint64_t da = umma_desc_sw128(smem_u32(ps));
+      const uint64_t db = umma_desc_sw128(smem_u32(vbuf + (j & 1) * kTcChunk));
+#pragma unroll
+      for (int k = 0; k < kTcKeys / 16; ++k)  // 16 slots = two 1024-B row groups of the MN-major V tile
+        tc_mma_f16(tmem + 64, da + 2 * k, db + (uint64_t)(128 * k), idesc_pv, (j | k) != 0 ? 1u : 0u);
+      tc_commit(pvbar);
+    }
+    if (j + 2 < nch) load(K, kbuf + (j & 1) * kTcChunk, j + 2);        // QK(j) done
+    if (j + 1 < nch) load(V, vbuf + ((j + 1) & 1) * kTcChunk, j + 1);  // PV(j-1) done
+  }
+  // the row's exp-sum: both halves (half 0's term first in both threads)
+  stat[half * 128 + r] = l;
+  if (nch > 0) wait_pv(nch - 1);
+  __syncthreads();
+  const float lo_sum = stat[r], hi_sum = stat[128 + r];
+  const float tot = __fadd_rn(lo_sum, hi_sum);
+  const float inv = tot > 0.0f ? __fdiv_rn(1.0f, tot) : 0.0f;
+  __half* orow = a.out + (size_t)(b * a.T + t0 + r) * a.ldo + h * D + 32 * half;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    float v[16];
+    if (nch > 0) {  // CTA-uniform: tcgen05.ld is warp-collective, every lane takes part
+      tmem_ld16(trow + 64u + (uint32_t)(16 * q), v);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = 0.0f;
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = __fmul_rn(v[e], inv);
+    if (row_ok) {
+      *reinterpret_cast<uint4*>(orow + 16 * q) = pack8(v);
+      *reinterpret_cast<uint4*>(orow + 16 * q + 8) = pack8(v + 8);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 128);
+}
+
 // ------------------------------------------------------------------ prefill
 // blockDim = 128 (4 warps x 4 query rows). Dynamic smem: 16 * D floats (q rows)
 // + 2 * 64 * (D + 1) halves (K/V chunk).

@@ -123,9 +123,10 @@ def _attn_ref(q, kc, vc, start, qbase, T, scale):
 
 
 @pytest.mark.parametrize("T,D,qbase", [(1, 64, 40), (1, 16, 5), (1, 4, 3), (16, 64, 0), (37, 64, 0),
-                                       (5, 32, 7), (130, 64, 0)])
+                                       (5, 32, 7), (130, 64, 0), (128, 64, 0), (200, 64, 60), (300, 64, 0)])
 def test_attention(cuda_device, T, D, qbase):
-    B, NH, cap = 3, 2, 192
+    """T > 1 with D = 64 runs the tcgen05 prefill kernel (S, O in TMEM)."""
+    B, NH, cap = 3, 2, max(192, qbase + T + 8)
     H = NH * D
     q = rand16(B * T, H, seed=9).to(cuda_device)
     kc = rand16(B, NH, cap, D, seed=10).to(cuda_device)
