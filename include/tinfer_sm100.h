@@ -130,6 +130,17 @@ int tf_embed_ln(const tf_embed_desc* d, void* stream);
 int tf_layernorm(int n_rows, int hidden, const void* x, int ldx, int src_stride, int src_off,
                  const float* gamma, const float* beta, void* h, int ldh, void* stream);
 
+/* Beam-search decode attention (one query row per beam; no reference
+ * counterpart: SPEC.md:14 lists beam search as a non-goal, the semantics are the
+ * oracle's restatement on attend_f32, kernels.py:148-180). Rows of request r are
+ * beams r*beam .. r*beam+beam-1; slot s (< *qbase_dev) of row b is read from row
+ * (b / beam) * beam + indir[b * cap + s] (the cache indirection the beam select
+ * maintains), the newest slot *qbase_dev from indir[b * cap + *qbase_dev]; every
+ * beam of a request shares the window [start[r * beam], *qbase_dev]. */
+int tf_attention_beam(int requests, int beam, int heads, int head_dim, int cap, const void* q, int ldq,
+                      const void* k_cache, const void* v_cache, const int* start, const int* qbase_dev,
+                      const int* indir, float scale, void* out, int ldo, void* stream);
+
 /* ---- weight packing on the device (model upload; TINF direct-to-device load,
  * replacing the host-side load_model -> Model.f32 path of model.py:177-184 /
  * 267-286 for the device mirror). All three are enqueued on `stream`.

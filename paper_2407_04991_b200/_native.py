@@ -136,6 +136,9 @@ SIGNATURES = {
     "tf_beam_decode": (C.c_int, [C.c_void_p, C.POINTER(BeamDesc), C.c_int, C.c_int, C.c_void_p]),
     "tf_debug_trace": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_void_p]),
     "tf_session_launches_per_step": (C.c_int, [C.c_void_p]),
+    "tf_attention_beam": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float,
+                                    C.c_void_p, C.c_int, C.c_void_p]),
     "tf_pack_kmajor": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
                                  C.c_void_p]),
     "tf_fold_terms": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,

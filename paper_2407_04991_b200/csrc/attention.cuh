@@ -476,254 +476,6 @@ __global__ void __launch_bounds__(kPfThreads, 1) attn_decode_pf_kernel(const Att
   }
 }
 
-// ------------------------------------------------------------------ decode, beam groups (ring)
-// head_dim 64, beam search (indir != null). One CTA (256 threads) per (head,
-// request) scores all R = beam rows of the request over the whole window. The
-// beams of a request share their prompt: a 64-slot chunk whose slots resolve
-// to the same source row for every beam (checked on the indirection table, so
-// shared generated ancestry counts too) is staged in shared memory ONCE and
-// every K row read from it serves R dot products; other chunks are staged per
-// beam. Chunks are staged in 16 KB planes (K rotated | V, as in
-// attn_decode_pf_kernel). Per (beam, chunk) the arithmetic -- scores, chunk
-// softmax, PV with one warp, and the merge in chunk order -- is that of
-// attn_decode_pf_kernel<.., 128>, so the output is bitwise the same as the
-// per-row kernel's (the oracle comparison and batch invariance carry over).
-constexpr int kBmThreads = 256, kBmMaxCh = 8;  // window <= 512 slots
-// Ring pipeline: chunks are processed one at a time in window order, their
-// planes taken from a ring of `planes` (one cp.async group per chunk), so the
-// copies of later chunks land while earlier ones are scored, and the small pool
-// lets MINB CTAs share an SM (one CTA's copies overlap another's arithmetic).
-__host__ __device__ inline size_t attn_beam_ring_aux_bytes(int R) {
-  // s_ind [R][512] u8 | sc [R][128] f32 | part [R][8][66] f32 | q [R][64] f32
-  return (size_t)R * (kBmMaxCh * 64 + 128 * 4 + kBmMaxCh * 66 * 4 + 64 * 4);
-}
-__device__ __forceinline__ void cp_async_wait_upto(int n) {  // allow <= n pending groups
-  switch (n) {
-    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
-    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
-    case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
-    case 5: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
-    case 6: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
-    default: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
-  }
-}
-
-template <int MINB>
-__global__ void __launch_bounds__(kBmThreads, MINB) attn_decode_beam_ring_kernel(const AttnArgs a, int planes) {
-  extern __shared__ __align__(128) uint8_t bm_smem[];
-  __shared__ int s_sh[kBmMaxCh];
-  constexpr int D = 64;
-  TF_TRACE_INIT(tr);
-  if (threadIdx.x == 0) tr.mark(a.trace, 0);
-  const int R = a.beam;
-  __half* kvs = reinterpret_cast<__half*>(bm_smem);
-  float* part = reinterpret_cast<float*>(bm_smem + (size_t)planes * kPfChunkBytes);  // [R][8][66]
-  float* qs = part + (size_t)R * kBmMaxCh * 66;                                        // [R][64]
-  float* sc = qs + (size_t)R * 64;                                                     // [R][128]
-  uint8_t* s_ind = reinterpret_cast<uint8_t*>(sc + (size_t)R * 128);                  // [R][512]
-  const int h = blockIdx.y, rq = blockIdx.z, beam0 = rq * R;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int qbase = *a.qbase_dev;
-  const int lo = a.start[beam0], hi = qbase;  // the beams of a request share the left pad
-  const int n = hi - lo + 1;
-  const int nch = n > 0 ? (n + 63) / 64 : 0;
-  const size_t row_stride = (size_t)a.NH * a.cap * D, head_stride = (size_t)a.cap * D;
-  // ---- before the wait: indirection rows (slots < hi), sharing per chunk
-  for (int i = tid; i < R * nch * 64; i += kBmThreads) {
-    const int r = i / (nch * 64), k = i - r * (nch * 64), s = lo + k;
-    s_ind[r * kBmMaxCh * 64 + k] = (uint8_t)(s < hi ? a.indir[(size_t)(beam0 + r) * a.cap + s] : 0);
-  }
-  __syncthreads();
-  if (warp < nch) {
-    bool same = true;
-    for (int k = warp * 64 + lane; k < warp * 64 + 64; k += 32) {
-      const int s = lo + k;
-      if (s == hi) same = false;  // the newest slot: each beam's own row
-      for (int r = 1; r < R && s < hi; ++r) same = same && s_ind[r * kBmMaxCh * 64 + k] == s_ind[k];
-    }
-    same = __all_sync(0xffffffffu, same);
-    if (lane == 0) s_sh[warp] = same;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) tr.mark(a.trace, 6);
-  // ring state (uniform across the CTA): chunk c's planes start at pl_of(c)
-  int next = 0, used = 0, head = 0;
-  int pl[kBmMaxCh];
-#pragma unroll
-  for (int c = 0; c < kBmMaxCh; ++c) pl[c] = 0;
-  const int cl = n > 0 ? (hi - lo) / 64 : -1;  // chunk holding the newest slot
-  bool newest_pending = false;                 // its chunk was staged before the wait
-  auto issue = [&](bool after_wait) {
-    while (next < nch) {
-      const int np = s_sh[next] ? 1 : R;
-      if (used + np > planes) break;
-      const int c = next;
-#pragma unroll
-      for (int cc = 0; cc < kBmMaxCh; ++cc)
-        if (cc == c) pl[cc] = head;
-      for (int seg = tid; seg < np * 64 * 8; seg += kBmThreads) {
-        const int p = seg >> 9, j = (seg >> 3) & 63, prt = seg & 7;
-        const int k = c * 64 + j, slot = lo + k;
-        if (slot == hi && !after_wait) continue;
-        const bool ok = slot <= hi;
-        const int src = slot == hi ? beam0 + a.indir[(size_t)(beam0 + p) * a.cap + hi]
-                                   : beam0 + s_ind[p * kBmMaxCh * 64 + k];
-        const size_t off = ok ? (size_t)src * row_stride + (size_t)h * head_stride + (size_t)slot * D + prt * 8 : 0;
-        int q = head + p;
-        if (q >= planes) q -= planes;
-        __half* pb = kvs + (size_t)q * (2 * 64 * 64);
-        cp_async16(smem_u32(pb + (size_t)j * 64 + ((prt + j) & 7) * 8), a.kc + off, ok);
-        cp_async16(smem_u32(pb + (size_t)(64 + j) * 64 + prt * 8), a.vc + off, ok);
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      if (c == cl && !after_wait) newest_pending = true;
-      head += np;
-      if (head >= planes) head -= planes;
-      used += np;
-      ++next;
-    }
-  };
-  issue(false);
-  pdl_trigger();
-  pdl_wait();
-  if (threadIdx.x == 0) tr.mark(a.trace, 1);
-  if (n <= 0) {
-    for (int i = tid; i < R * D; i += kBmThreads)
-      a.out[(size_t)(beam0 + i / D) * a.ldo + (size_t)h * D + i % D] = __float2half_rn(0.0f);
-    return;
-  }
-  for (int i = tid; i < R * D; i += kBmThreads)
-    qs[i] = __half2float(a.q[(size_t)(beam0 + i / D) * a.ldq + (size_t)h * D + i % D]);
-  if (newest_pending) {  // the newest slot of a chunk staged before the wait
-    const int j = (hi - lo) % 64;
-    int plc = 0;
-#pragma unroll
-    for (int cc = 0; cc < kBmMaxCh; ++cc)
-      if (cc == cl) plc = pl[cc];
-    for (int i = tid; i < R * 16; i += kBmThreads) {
-      const int p = i >> 4, kv = (i >> 3) & 1, prt = i & 7;
-      const int src = beam0 + a.indir[(size_t)(beam0 + p) * a.cap + hi];
-      const size_t off = (size_t)src * row_stride + (size_t)h * head_stride + (size_t)hi * D + prt * 8;
-      int q = plc + p;
-      if (q >= planes) q -= planes;
-      __half* dst = kvs + (size_t)q * (2 * 64 * 64) + (size_t)(kv * 64 + j) * 64 + (kv ? prt : ((prt + j) & 7)) * 8;
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>((kv ? a.vc : a.kc) + off);
-    }
-  }
-  __syncthreads();  // qs complete
-  const int RT = (kBmThreads / R) * R;  // threads with a beam (QK^T: fixed beam, q in registers)
-  const int my_r = tid % R;
-  float qr[64];
-#pragma unroll
-  for (int e = 0; e < 64; e += 4) {
-    const float4 q4 = *reinterpret_cast<const float4*>(qs + (tid < RT ? my_r : 0) * 64 + e);
-    qr[e] = q4.x;
-    qr[e + 1] = q4.y;
-    qr[e + 2] = q4.z;
-    qr[e + 3] = q4.w;
-  }
-  auto plane_of = [&](int cc) {
-    int v = 0;
-#pragma unroll
-    for (int i = 0; i < kBmMaxCh; ++i)
-      if (i == cc) v = pl[i];
-    return v;
-  };
-  // one or two chunks per round: the second when it is already in the ring
-  // (fills the PV warps, halves the barriers per chunk)
-  for (int c = 0; c < nch;) {
-    issue(true);  // refill the ring (no-op when full or done)
-    const int k = c + 1 < next ? 2 : 1;
-    cp_async_wait_upto(next - c - k);
-    __syncthreads();
-    const int nk = min(k * 64, n - c * 64);
-    if (tid < RT) {
-      for (int key = tid / R; key < nk; key += kBmThreads / R) {
-        const int cc = c + (key >> 6), j = key & 63;
-        int q = plane_of(cc) + (s_sh[cc] ? 0 : my_r);
-        if (q >= planes) q -= planes;
-        const __half* kr = kvs + (size_t)q * (2 * 64 * 64) + (size_t)j * 64;
-        uint4 raw[8];
-#pragma unroll
-        for (int g = 0; g < 8; ++g) raw[g] = *reinterpret_cast<const uint4*>(kr + ((g + j) & 7) * 8);
-        float ps[8];
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          float kf[8];
-          unpack8(raw[g], kf);
-          float acc = __fmul_rn(qr[8 * g], kf[0]);
-#pragma unroll
-          for (int e = 1; e < 8; ++e) acc = __fmaf_rn(qr[8 * g + e], kf[e], acc);
-          ps[g] = acc;
-        }
-        const float d = __fadd_rn(__fadd_rn(__fadd_rn(ps[0], ps[1]), __fadd_rn(ps[2], ps[3])),
-                                  __fadd_rn(__fadd_rn(ps[4], ps[5]), __fadd_rn(ps[6], ps[7])));
-        sc[my_r * 128 + key] = __fmul_rn(d, a.scale);
-      }
-    }
-    __syncthreads();
-    // one warp per (beam, chunk): chunk softmax + PV (attn_decode_pf_kernel, WPC 1)
-    for (int u = warp; u < R * k; u += kBmThreads / 32) {
-      const int r = u % R, ci = u / R, cc = c + ci;
-      const int cnt = min(64, n - cc * 64);
-      float* sci = sc + r * 128 + ci * 64;
-      const float s0 = lane < cnt ? sci[lane] : -INFINITY;
-      const float s1 = lane + 32 < cnt ? sci[lane + 32] : -INFINITY;
-      const float m = warp_max(fmaxf(s0, s1));
-      const float e0 = lane < cnt ? expf(__fsub_rn(s0, m)) : 0.0f;
-      const float e1 = lane + 32 < cnt ? expf(__fsub_rn(s1, m)) : 0.0f;
-      const float z = warp_sum(__fadd_rn(e0, e1));
-      sci[lane] = e0;  // this warp alone reads / writes this row
-      sci[lane + 32] = e1;
-      __syncwarp();
-      int q = plane_of(cc) + (s_sh[cc] ? 0 : r);
-      if (q >= planes) q -= planes;
-      const __half* Vs = kvs + (size_t)q * (2 * 64 * 64) + 64 * 64;
-      float o0[4] = {0.f, 0.f, 0.f, 0.f}, o1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 4
-      for (int j = 0; j < 64; j += 4) {
-#pragma unroll
-        for (int uu = 0; uu < 4; ++uu) {
-          const float2 v = __half22float2(*reinterpret_cast<const __half2*>(Vs + (j + uu) * 64 + 2 * lane));
-          const float w = sci[j + uu];
-          o0[uu] = __fmaf_rn(w, v.x, o0[uu]);
-          o1[uu] = __fmaf_rn(w, v.y, o1[uu]);
-        }
-      }
-      float* dst = part + ((size_t)r * kBmMaxCh + cc) * 66;
-      dst[2 + 2 * lane] = __fadd_rn(__fadd_rn(o0[0], o0[1]), __fadd_rn(o0[2], o0[3]));
-      dst[3 + 2 * lane] = __fadd_rn(__fadd_rn(o1[0], o1[1]), __fadd_rn(o1[2], o1[3]));
-      if (lane == 0) {
-        dst[0] = m;
-        dst[1] = z;
-      }
-    }
-    __syncthreads();  // the round's planes and score rows are free
-    used -= (s_sh[c] ? 1 : R) + (k == 2 ? (s_sh[c + 1] ? 1 : R) : 0);
-    c += k;
-  }
-  if (threadIdx.x == 0) tr.mark(a.trace, 5);
-  for (int i = tid; i < R * D; i += kBmThreads) {
-    const int r = i / D, d = i % D;
-    const float* P = part + (size_t)r * kBmMaxCh * 66;
-    float M = -INFINITY;
-    for (int cc = 0; cc < nch; ++cc) M = fmaxf(M, P[(size_t)cc * 66]);
-    float Z = 0.0f, O = 0.0f;
-    for (int cc = 0; cc < nch; ++cc) {
-      const float f = expf(__fsub_rn(P[(size_t)cc * 66], M));
-      Z = __fadd_rn(Z, __fmul_rn(P[(size_t)cc * 66 + 1], f));
-      O = __fadd_rn(O, __fmul_rn(P[(size_t)cc * 66 + 2 + d], f));
-    }
-    a.out[(size_t)(beam0 + r) * a.ldo + (size_t)h * D + d] = f16_sat(__fdiv_rn(O, Z));
-  }
-  if (threadIdx.x == 0) {
-    tr.mark(a.trace, 7);
-    tr.flush(a.trace);
-  }
-}
-
 // ------------------------------------------------------------------ prefill, tensor cores
 // head_dim 64. One CTA = 64 query rows of one (head, sequence), 4 warps x 16 rows.
 // Key/value tiles of 64 slots (aligned to the row's first valid slot `start`, so
@@ -892,6 +644,253 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const AttnArgs a)
     if (row1 - t0 < rows)
       *reinterpret_cast<__half2*>(a.out + (size_t)(b * a.T + row1) * a.ldo + h * D + d) =
           __halves2half2(f16_sat(o[nd][2] * i1), f16_sat(o[nd][3] * i1));
+  }
+}
+
+// ------------------------------------------------------------------ decode, beam groups (tensor cores)
+// head_dim 64, beam search. One CTA (4 warps) per (head, request) over the whole
+// window. The window's 64-slot chunks (aligned to the request's first valid
+// slot) become work units: a chunk whose slots resolve to the same source row
+// for every beam (read off the indirection table: the prompt and any shared
+// ancestry) is ONE unit for all R beams, any other chunk is one unit per beam
+// (its own rows). A warp stages a unit's K and V rows (cp.async, 128-byte XOR
+// swizzle) and runs it on mma.sync m16n8k16 with the beams as the M rows:
+//   S[beams x 64] = Q K^T  (32 MMAs), scale, mask (slots past the newest,
+//                           beams the unit does not serve), online softmax per
+//                           beam in registers (flash form, running max / sum),
+//   O[beams x 64] += P V   (32 MMAs; P reused from the S fragments as f16).
+// Units are dealt round-robin to the 4 warps; each warp's first unit (all but
+// the newest slot) is staged before the PDL wait. The warps' partial states
+// are merged per beam in warp order (deterministic), output rounded once.
+constexpr int kBtThreads = 128, kBtMaxUnits = 64;  // <= 8 chunks x <= 8 beams
+__host__ __device__ constexpr size_t attn_beam_mma_smem() {
+  // q [16][72] f16 | s_ind [8][512] u8 | 4 warps x (K 8 KB + V 8 KB) | merge [4][8][66] f32 (aliases the K/V area)
+  return 16 * 72 * 2 + 8 * 512 + 4 * 16384 + 64;
+}
+
+__device__ __forceinline__ uint32_t xsw(int row, int chunk16) {  // 128-B rows, 16-B chunks XOR-swizzled
+  return (uint32_t)(row * 128 + ((chunk16 ^ (row & 7)) << 4));
+}
+
+__global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(const AttnArgs a) {
+  extern __shared__ __align__(128) uint8_t bt_smem[];
+  __half* qs = reinterpret_cast<__half*>(bt_smem);                 // [16][72]
+  uint8_t* s_ind = bt_smem + 16 * 72 * 2;                           // [R][512] source beam per slot
+  uint8_t* kv = s_ind + 8 * 512;                                    // [4 warps][K 8 KB | V 8 KB]
+  __shared__ int s_sh[8];
+  __shared__ int s_units, s_unit_c[kBtMaxUnits], s_unit_r[kBtMaxUnits];
+  constexpr int D = 64;
+  TF_TRACE_INIT(tr);
+  if (threadIdx.x == 0) tr.mark(a.trace, 0);
+  const int R = a.beam;
+  const int h = blockIdx.y, rq = blockIdx.z, beam0 = rq * R;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int qbase = *a.qbase_dev;
+  const int lo = a.start[beam0], hi = qbase;  // the beams of a request share the left pad
+  const int n = hi - lo + 1;
+  const int nch = n > 0 ? (n + 63) / 64 : 0;
+  const size_t row_stride = (size_t)a.NH * a.cap * D, head_stride = (size_t)a.cap * D;
+  // ---- before the wait: indirection rows, shared chunks, the unit list
+  for (int i = tid; i < R * nch * 64; i += kBtThreads) {
+    const int r = i / (nch * 64), k = i - r * (nch * 64), s = lo + k;
+    s_ind[r * 512 + k] = (uint8_t)(s < hi ? a.indir[(size_t)(beam0 + r) * a.cap + s] : r);
+  }
+  __syncthreads();
+  if (warp < nch) {
+    bool same = true;
+    for (int k = warp * 64 + lane; k < warp * 64 + 64; k += 32) {
+      const int s = lo + k;
+      if (s == hi) same = false;  // the newest slot: each beam's own row
+      for (int r = 1; r < R && s < hi; ++r) same = same && s_ind[r * 512 + k] == s_ind[k];
+    }
+    same = __all_sync(0xffffffffu, same);
+    if (lane == 0) s_sh[warp] = same;
+  }
+  if (warp + 4 < nch) {  // windows of up to 8 chunks
+    const int c = warp + 4;
+    bool same = true;
+    for (int k = c * 64 + lane; k < c * 64 + 64; k += 32) {
+      const int s = lo + k;
+      if (s == hi) same = false;
+      for (int r = 1; r < R && s < hi; ++r) same = same && s_ind[r * 512 + k] == s_ind[k];
+    }
+    same = __all_sync(0xffffffffu, same);
+    if (lane == 0) s_sh[c] = same;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int u = 0;
+    for (int c = 0; c < nch; ++c) {
+      if (s_sh[c]) {
+        s_unit_c[u] = c;
+        s_unit_r[u++] = -1;  // all beams
+      } else {
+        for (int r = 0; r < R; ++r) {
+          s_unit_c[u] = c;
+          s_unit_r[u++] = r;
+        }
+      }
+    }
+    s_units = u;
+  }
+  __syncthreads();
+  const int units = s_units;
+  uint8_t* kb = kv + warp * 16384;
+  uint8_t* vb = kb + 8192;
+  // stage unit u's rows (all but the newest slot when before the wait)
+  auto stage = [&](int u, bool after_wait) {
+    const int c = s_unit_c[u], ur = s_unit_r[u];
+    for (int i = lane; i < 64 * 8; i += 32) {
+      const int j = i >> 3, prt = i & 7, k = c * 64 + j, slot = lo + k;
+      if (slot == hi && !after_wait) continue;
+      const bool ok = slot <= hi;
+      const int rr = ur < 0 ? 0 : ur;
+      const int src = beam0 + (slot == hi ? a.indir[(size_t)(beam0 + rr) * a.cap + hi] : s_ind[rr * 512 + k]);
+      const size_t off = ok ? (size_t)src * row_stride + (size_t)h * head_stride + (size_t)slot * D + prt * 8 : 0;
+      cp_async16(smem_u32(kb + xsw(j, prt)), a.kc + off, ok);
+      cp_async16(smem_u32(vb + xsw(j, prt)), a.vc + off, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const bool pre = warp < units;
+  if (pre) stage(warp, false);
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) tr.mark(a.trace, 1);
+  // q rows (beams; rows >= R zero), f16 as stored by the QKV epilogue
+  for (int i = tid; i < 16 * 8; i += kBtThreads) {
+    const int r = i >> 3, prt = i & 7;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < R) v = *reinterpret_cast<const uint4*>(a.q + (size_t)(beam0 + r) * a.ldq + (size_t)h * D + prt * 8);
+    *reinterpret_cast<uint4*>(qs + r * 72 + prt * 8) = v;
+  }
+  __syncthreads();
+  uint32_t qa[4][4];  // A fragments of Q: rows g / g+8, 4 k-steps of 16 dims
+  {
+    const int r = (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+      ldsm_x4(smem_u32(qs + r * 72 + ks * 16 + (lane >> 4) * 8), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+  }
+  float m0 = -INFINITY, l0 = 0.0f;  // beam g (rows g + 8 are padding)
+  float o[8][4];
+#pragma unroll
+  for (int nd = 0; nd < 8; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.0f;
+  for (int u = warp; u < units; u += 4) {
+    if (u != warp) stage(u, true);  // later units: issued after the previous one was consumed
+    const int c = s_unit_c[u], ur = s_unit_r[u];
+    if (c * 64 + 63 >= hi - lo && u == warp) {  // the unit staged early holds the newest slot: fetch it now
+      const int j = hi - lo - c * 64;
+      if (lane < 8) {
+        const int rr = ur < 0 ? 0 : ur;
+        const int src = beam0 + a.indir[(size_t)(beam0 + rr) * a.cap + hi];
+        const size_t off = (size_t)src * row_stride + (size_t)h * head_stride + (size_t)hi * D + lane * 8;
+        cp_async16(smem_u32(kb + xsw(j, lane)), a.kc + off, true);
+        cp_async16(smem_u32(vb + xsw(j, lane)), a.vc + off, true);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    // S = Q K^T: 8 key n-tiles of 8
+    float sc[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.0f;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        uint32_t b0, b1;
+        ldsm_x2(smem_u32(kb + xsw(nt * 8 + (lane & 7), ks * 2 + ((lane >> 3) & 1))), b0, b1);
+        mma16816(sc[nt], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+      }
+    }
+    // scale + mask (rows: beam g; the unit serves beam ur, or all), chunk max
+    const bool row_in = g < R && (ur < 0 || ur == g);
+    float mx = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int slot = lo + c * 64 + nt * 8 + 2 * tq + e;
+        sc[nt][e] = (row_in && slot <= hi) ? __fmul_rn(sc[nt][e], a.scale) : -INFINITY;
+        mx = fmaxf(mx, sc[nt][e]);
+      }
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float mn = fmaxf(m0, mx);
+    const float al = (m0 == -INFINITY) ? 0.0f : expf(__fsub_rn(m0, mn));
+    float ps = 0.0f;
+    uint32_t pa[8][2];  // P as f16 pairs: row g (rows g+8 are zero)
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = sc[nt][0] == -INFINITY ? 0.0f : expf(__fsub_rn(sc[nt][0], mn));
+      const float p1 = sc[nt][1] == -INFINITY ? 0.0f : expf(__fsub_rn(sc[nt][1], mn));
+      ps = __fadd_rn(ps, __fadd_rn(p0, p1));
+      pa[nt][0] = pack_h2(p0, p1);
+      pa[nt][1] = 0u;
+    }
+    if (mx != -INFINITY) {  // this unit has visible keys for beam g
+      l0 = __fadd_rn(__fmul_rn(l0, al), ps);
+      m0 = mn;
+#pragma unroll
+      for (int nd = 0; nd < 8; ++nd) {
+        o[nd][0] = __fmul_rn(o[nd][0], al);
+        o[nd][1] = __fmul_rn(o[nd][1], al);
+      }
+    }
+    // O += P V: 4 key k-steps of 16, 8 dim n-tiles of 8
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+      for (int nd = 0; nd < 8; ++nd) {
+        uint32_t b0, b1;
+        const int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        ldsm_x2_t(smem_u32(vb + xsw(key, nd)), b0, b1);
+        mma16816(o[nd], pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1], b0, b1);
+      }
+    }
+    __syncwarp();  // every lane's ldmatrix done before the buffers are restaged
+  }
+  if (threadIdx.x == 0) tr.mark(a.trace, 5);
+  // per-beam merge of the 4 warps' states, in warp order
+  l0 = __fadd_rn(l0, __shfl_xor_sync(0xffffffffu, l0, 1));
+  l0 = __fadd_rn(l0, __shfl_xor_sync(0xffffffffu, l0, 2));
+  __syncthreads();  // all warps done with their K/V buffers (reused for the merge)
+  float* mrg = reinterpret_cast<float*>(kv);  // [4 warps][8 beams][66]: m, l, O[64]
+  if (g < R) {
+    float* dst = mrg + ((size_t)warp * 8 + g) * 66;
+    if (tq == 0) {
+      dst[0] = m0;
+      dst[1] = l0;
+    }
+#pragma unroll
+    for (int nd = 0; nd < 8; ++nd) {
+      dst[2 + nd * 8 + 2 * tq] = o[nd][0];
+      dst[2 + nd * 8 + 2 * tq + 1] = o[nd][1];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < R * D; i += kBtThreads) {
+    const int r = i / D, d = i - r * D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, mrg[((size_t)w * 8 + r) * 66]);
+    float Z = 0.0f, O = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float* P = mrg + ((size_t)w * 8 + r) * 66;
+      if (P[0] == -INFINITY) continue;
+      const float f = expf(__fsub_rn(P[0], M));
+      Z = __fadd_rn(Z, __fmul_rn(P[1], f));
+      O = __fadd_rn(O, __fmul_rn(P[2 + d], f));
+    }
+    a.out[(size_t)(beam0 + r) * a.ldo + (size_t)h * D + d] = f16_sat(Z > 0.0f ? __fdiv_rn(O, Z) : 0.0f);
+  }
+  if (threadIdx.x == 0) {
+    tr.mark(a.trace, 7);
+    tr.flush(a.trace);
   }
 }
 

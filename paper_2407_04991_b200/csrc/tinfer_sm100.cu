@@ -533,12 +533,12 @@ void run_ln(const LnArgs& a0, cudaStream_t st, bool pdl) {
 }
 
 // beam attention: TF_ATTN_BEAM=0 runs the per-row kernel through the
-// indirection table instead of the beam-grouped one (A/B; the bitwise
-// equality of the two is tests/test_gpu_beam_attention.py)
+// indirection table instead of the beam-grouped tensor-core one (A/B; both are
+// checked against a torch reference in tests/test_gpu_beam_attention_op.py)
 int beam_attn_mode() {
   static const int mode = [] {
     const char* e = getenv("TF_ATTN_BEAM");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 1;
   }();
   return mode;
 }
@@ -555,28 +555,15 @@ bool prefill_tc_on() {
 void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
   TF_REQUIRE(a.D >= 1 && a.D <= 128, TF_ERR_UNSUPPORTED, "head_dim must be in [1, 128]");
   const bool ws_ok = a.ws && a.cnt && a.max_chunks >= (a.cap + kPfKeysPerChunk - 1) / kPfKeysPerChunk;
-  if (a.T == 1 && a.D == 64 && a.indir && a.beam >= 2 && a.B % a.beam == 0 && a.cap <= kBmMaxCh * 64 &&
-      beam_attn_mode() != 0) {
-    // one CTA per (head, request): prompt chunks staged once for all beams;
-    // ring-pipelined, two CTAs per SM when a 6-plane ring fits
-    const int R = a.beam;
-    const size_t half = 115712 - 512;  // per-CTA share of the SM with two resident
-    const int p2 = (int)((half - attn_beam_ring_aux_bytes(R)) / kPfChunkBytes);
+  if (a.T == 1 && a.D == 64 && a.indir && a.beam >= 2 && a.beam <= 8 && a.B % a.beam == 0 &&
+      a.cap <= 512 && beam_attn_mode() != 0) {
+    // tensor-core beam attention: one CTA per (head, request), shared chunks
+    // once for all beams, mma.sync with the beams as M rows
     AttnArgs t = a;
     t.trace = trace_next("attn_decode_beam");
-    const dim3 grid(1, a.NH, a.B / a.beam);
-    if (p2 >= R) {
-      const int planes = std::min(p2, 6);
-      ensure_attr(attn_decode_beam_ring_kernel<2>, kMaxSmem - 2048);
-      launch(attn_decode_beam_ring_kernel<2>, grid, dim3(kBmThreads),
-             attn_beam_ring_aux_bytes(R) + (size_t)planes * kPfChunkBytes, st, pdl, t, planes);
-    } else {
-      const int planes = (int)std::min<size_t>(12, (kMaxSmem - 2048 - attn_beam_ring_aux_bytes(R)) / kPfChunkBytes);
-      TF_REQUIRE(planes >= R, TF_ERR_UNSUPPORTED, "beam attention: plane pool smaller than the beam");
-      ensure_attr(attn_decode_beam_ring_kernel<1>, kMaxSmem - 2048);
-      launch(attn_decode_beam_ring_kernel<1>, grid, dim3(kBmThreads),
-             attn_beam_ring_aux_bytes(R) + (size_t)planes * kPfChunkBytes, st, pdl, t, planes);
-    }
+    ensure_attr(attn_decode_beam_mma_kernel, attn_beam_mma_smem());
+    launch(attn_decode_beam_mma_kernel, dim3(1, a.NH, a.B / a.beam), dim3(kBtThreads), attn_beam_mma_smem(), st, pdl,
+           t);
   } else if (a.T == 1 && a.D == 64 && ws_ok) {
     // prefetching split-KV decode: chunks per CTA = the whole window when it is
     // <= 4 chunks (local merge), else groups of <= 4 (64 KB of K/V each)
@@ -1129,6 +1116,34 @@ int tf_attention(int batch, int heads, int head_dim, int cap, int seq_len, const
     a.out = static_cast<__half*>(out);
     a.ldo = ldo;
     if (batch > 0 && seq_len > 0) run_attention(a, static_cast<cudaStream_t>(stream), false);
+  });
+}
+
+int tf_attention_beam(int requests, int beam, int heads, int head_dim, int cap, const void* q, int ldq,
+                      const void* k_cache, const void* v_cache, const int* start, const int* qbase_dev,
+                      const int* indir, float scale, void* out, int ldo, void* stream) {
+  return guarded([&] {
+    TF_REQUIRE(q && k_cache && v_cache && start && indir && out && qbase_dev, TF_ERR_ARG,
+               "attention_beam: null pointer");
+    TF_REQUIRE(beam >= 1 && beam <= 8 && requests >= 0, TF_ERR_ARG, "attention_beam: beam must be in [1, 8]");
+    AttnArgs a{};
+    a.B = requests * beam;
+    a.NH = heads;
+    a.D = head_dim;
+    a.cap = cap;
+    a.T = 1;
+    a.q = static_cast<const __half*>(q);
+    a.ldq = ldq;
+    a.kc = static_cast<const __half*>(k_cache);
+    a.vc = static_cast<const __half*>(v_cache);
+    a.start = start;
+    a.qbase_dev = qbase_dev;
+    a.indir = indir;
+    a.beam = beam;
+    a.scale = scale;
+    a.out = static_cast<__half*>(out);
+    a.ldo = ldo;
+    if (requests > 0) run_attention(a, static_cast<cudaStream_t>(stream), false);
   });
 }
 

@@ -119,6 +119,16 @@ def attention(q, ldq_rows_view, k_cache, v_cache, start, qbase, scale, out, *, b
     return out
 
 
+def attention_beam(q, k_cache, v_cache, start, qbase, indir, scale, out, *, requests, beam, heads, head_dim,
+                   cap):
+    """Beam-search decode attention (tf_attention_beam): one query row per beam,
+    cache rows resolved through the indirection table ``indir`` [rows, cap]."""
+    N.check(N.lib().tf_attention_beam(requests, beam, heads, head_dim, cap, _ptr(q), q.stride(0), _ptr(k_cache),
+                                      _ptr(v_cache), _ptr(start), _ptr(qbase), _ptr(indir), C.c_float(scale),
+                                      _ptr(out), out.stride(0), _stream()), "tf_attention_beam")
+    return out
+
+
 def embed_ln(ids, pos, tok_emb, pos_emb, hidden, x, h=None, gamma=None, beta=None, *,
              remap=None, unk_id=0, type_ids=None, type_emb=None, type_const=0, ids_out=None):
     if ids.shape != pos.shape:
