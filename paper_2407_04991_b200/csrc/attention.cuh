@@ -650,33 +650,37 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const AttnArgs a)
 // ------------------------------------------------------------------ decode, beam groups (tensor cores)
 // head_dim 64, beam search. One CTA (4 warps) per (head, request) over the whole
 // window. The window's 64-slot chunks (aligned to the request's first valid
-// slot) become work units: a chunk whose slots resolve to the same source row
-// for every beam (read off the indirection table: the prompt and any shared
-// ancestry) is ONE unit for all R beams, any other chunk is one unit per beam
-// (its own rows). A warp stages a unit's K and V rows (cp.async, 128-byte XOR
-// swizzle) and runs it on mma.sync m16n8k16 with the beams as the M rows:
-//   S[beams x 64] = Q K^T  (32 MMAs), scale, mask (slots past the newest,
-//                           beams the unit does not serve), online softmax per
-//                           beam in registers (flash form, running max / sum),
-//   O[beams x 64] += P V   (32 MMAs; P reused from the S fragments as f16).
-// Units are dealt round-robin to the 4 warps; each warp's first unit (all but
-// the newest slot) is staged before the PDL wait. The warps' partial states
-// are merged per beam in warp order (deterministic), output rounded once.
-constexpr int kBtThreads = 128, kBtMaxUnits = 64;  // <= 8 chunks x <= 8 beams
-__host__ __device__ constexpr size_t attn_beam_mma_smem() {
-  // q [16][72] f16 | s_ind [8][512] u8 | 4 warps x (K 8 KB + V 8 KB) | merge [4][8][66] f32 (aliases the K/V area)
-  return 16 * 72 * 2 + 8 * 512 + 4 * 16384 + 64;
+// slot) are split into 32-slot work units: a chunk whose slots resolve to the
+// same source row for every beam (read off the indirection table: the prompt
+// and any shared ancestry) gives units serving all R beams, any other chunk
+// one unit per beam (its own rows). Units are dealt round-robin to the warps; a
+// warp streams its next unit's K and V rows (cp.async, 128-byte XOR swizzle,
+// two 8 KB buffers) while it runs the current one on mma.sync m16n8k16 with the
+// beams as the M rows:
+//   S[beams x 32] = Q K^T  (16 MMAs), scale, mask (slots past the newest, beams
+//                           the unit does not serve), online softmax per beam in
+//                           registers (flash form, running max / sum),
+//   O[beams x 64] += P V   (16 MMAs; P reused from the S fragments as f16).
+// Each warp's first unit (all but the newest slot) is staged before the PDL
+// wait. The warps' partial states are merged per beam in warp order
+// (deterministic), the output rounded once.
+constexpr int kBtThreads = 128, kBtMaxUnits = 128;  // <= 16 half-chunks x <= 8 beams
+__host__ __device__ constexpr size_t attn_beam_mma_smem(int R, int nbuf) {
+  // q [16][72] f16 | s_ind [R][512] u8 | 4 warps x nbuf x (K 4 KB + V 4 KB) | merge [4][8][66] f32 (aliases K/V)
+  return 16 * 72 * 2 + (size_t)R * 512 + (size_t)4 * nbuf * 8192 + 64;
 }
 
 __device__ __forceinline__ uint32_t xsw(int row, int chunk16) {  // 128-B rows, 16-B chunks XOR-swizzled
   return (uint32_t)(row * 128 + ((chunk16 ^ (row & 7)) << 4));
 }
 
+// (one buffer per warp at 6 CTAs per SM, one wave at C4, measured slower: 816 vs 789 us per beam step)
 __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(const AttnArgs a) {
+  constexpr int NBUF = 2;
   extern __shared__ __align__(128) uint8_t bt_smem[];
   __half* qs = reinterpret_cast<__half*>(bt_smem);                 // [16][72]
   uint8_t* s_ind = bt_smem + 16 * 72 * 2;                           // [R][512] source beam per slot
-  uint8_t* kv = s_ind + 8 * 512;                                    // [4 warps][K 8 KB | V 8 KB]
+  uint8_t* kv = s_ind + a.beam * 512;                               // [4 warps][NBUF][K 4 KB | V 4 KB]
   __shared__ int s_sh[8];
   __shared__ int s_units, s_unit_c[kBtMaxUnits], s_unit_r[kBtMaxUnits];
   constexpr int D = 64;
@@ -719,16 +723,19 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
     if (lane == 0) s_sh[c] = same;
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0) {  // units: 32-slot halves of the chunks (shared: all beams; else one per beam)
     int u = 0;
     for (int c = 0; c < nch; ++c) {
-      if (s_sh[c]) {
-        s_unit_c[u] = c;
-        s_unit_r[u++] = -1;  // all beams
-      } else {
-        for (int r = 0; r < R; ++r) {
-          s_unit_c[u] = c;
-          s_unit_r[u++] = r;
+      for (int hf = 0; hf < 2; ++hf) {
+        if (c * 64 + hf * 32 >= n) break;
+        if (s_sh[c]) {
+          s_unit_c[u] = 2 * c + hf;
+          s_unit_r[u++] = -1;  // all beams
+        } else {
+          for (int r = 0; r < R; ++r) {
+            s_unit_c[u] = 2 * c + hf;
+            s_unit_r[u++] = r;
+          }
         }
       }
     }
@@ -736,13 +743,16 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   }
   __syncthreads();
   const int units = s_units;
-  uint8_t* kb = kv + warp * 16384;
-  uint8_t* vb = kb + 8192;
-  // stage unit u's rows (all but the newest slot when before the wait)
-  auto stage = [&](int u, bool after_wait) {
-    const int c = s_unit_c[u], ur = s_unit_r[u];
-    for (int i = lane; i < 64 * 8; i += 32) {
-      const int j = i >> 3, prt = i & 7, k = c * 64 + j, slot = lo + k;
+  // two 8 KB unit buffers per warp (K 4 KB | V 4 KB): the next unit streams in
+  // while the current one is computed
+  uint8_t* wb = kv + warp * (NBUF * 8192);
+  // stage unit u's 32 slots into buffer `buf` (all but the newest slot before the wait)
+  auto stage = [&](int u, int buf, bool after_wait) {
+    const int hc = s_unit_c[u], ur = s_unit_r[u];
+    uint8_t* kb = wb + buf * 8192;
+    uint8_t* vb = kb + 4096;
+    for (int i = lane; i < 32 * 8; i += 32) {
+      const int j = i >> 3, prt = i & 7, k = hc * 32 + j, slot = lo + k;
       if (slot == hi && !after_wait) continue;
       const bool ok = slot <= hi;
       const int rr = ur < 0 ? 0 : ur;
@@ -751,13 +761,25 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
       cp_async16(smem_u32(kb + xsw(j, prt)), a.kc + off, ok);
       cp_async16(smem_u32(vb + xsw(j, prt)), a.vc + off, ok);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  const bool pre = warp < units;
-  if (pre) stage(warp, false);
+  if (warp < units) stage(warp, 0, false);
+  asm volatile("cp.async.commit_group;" ::: "memory");
   pdl_trigger();
   pdl_wait();
   if (threadIdx.x == 0) tr.mark(a.trace, 1);
+  // the unit staged early may hold the newest slot (written by this layer's QKV GEMM)
+  if (warp < units) {
+    const int hc = s_unit_c[warp], ur = s_unit_r[warp];
+    const int j = hi - lo - hc * 32;
+    if (j >= 0 && j < 32 && lane < 8) {
+      const int rr = ur < 0 ? 0 : ur;
+      const int src = beam0 + a.indir[(size_t)(beam0 + rr) * a.cap + hi];
+      const size_t off = (size_t)src * row_stride + (size_t)h * head_stride + (size_t)hi * D + lane * 8;
+      cp_async16(smem_u32(wb + xsw(j, lane)), a.kc + off, true);
+      cp_async16(smem_u32(wb + 4096 + xsw(j, lane)), a.vc + off, true);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   // q rows (beams; rows >= R zero), f16 as stored by the QKV epilogue
   for (int i = tid; i < 16 * 8; i += kBtThreads) {
     const int r = i >> 3, prt = i & 7;
@@ -777,26 +799,19 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   float o[8][4];
 #pragma unroll
   for (int nd = 0; nd < 8; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.0f;
-  for (int u = warp; u < units; u += 4) {
-    if (u != warp) stage(u, true);  // later units: issued after the previous one was consumed
-    const int c = s_unit_c[u], ur = s_unit_r[u];
-    if (c * 64 + 63 >= hi - lo && u == warp) {  // the unit staged early holds the newest slot: fetch it now
-      const int j = hi - lo - c * 64;
-      if (lane < 8) {
-        const int rr = ur < 0 ? 0 : ur;
-        const int src = beam0 + a.indir[(size_t)(beam0 + rr) * a.cap + hi];
-        const size_t off = (size_t)src * row_stride + (size_t)h * head_stride + (size_t)hi * D + lane * 8;
-        cp_async16(smem_u32(kb + xsw(j, lane)), a.kc + off, true);
-        cp_async16(smem_u32(vb + xsw(j, lane)), a.vc + off, true);
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  int buf = 0;
+  for (int u = warp; u < units; u += 4, buf ^= 1) {
+    if (u + 4 < units) stage(u + 4, buf ^ 1, true);  // the next unit streams in while this one computes
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
-    // S = Q K^T: 8 key n-tiles of 8
-    float sc[8][4];
+    const uint8_t* kb = wb + buf * 8192;
+    const uint8_t* vb = kb + 4096;
+    const int hc = s_unit_c[u], ur = s_unit_r[u];
+    // S = Q K^T: 4 key n-tiles of 8
+    float sc[4][4];
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
+    for (int nt = 0; nt < 4; ++nt) {
       sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.0f;
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
@@ -805,14 +820,14 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
         mma16816(sc[nt], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
       }
     }
-    // scale + mask (rows: beam g; the unit serves beam ur, or all), chunk max
+    // scale + mask (rows: beam g; the unit serves beam ur, or all), unit max
     const bool row_in = g < R && (ur < 0 || ur == g);
     float mx = -INFINITY;
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
+    for (int nt = 0; nt < 4; ++nt) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int slot = lo + c * 64 + nt * 8 + 2 * tq + e;
+        const int slot = lo + hc * 32 + nt * 8 + 2 * tq + e;
         sc[nt][e] = (row_in && slot <= hi) ? __fmul_rn(sc[nt][e], a.scale) : -INFINITY;
         mx = fmaxf(mx, sc[nt][e]);
       }
@@ -822,14 +837,13 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
     const float mn = fmaxf(m0, mx);
     const float al = (m0 == -INFINITY) ? 0.0f : expf(__fsub_rn(m0, mn));
     float ps = 0.0f;
-    uint32_t pa[8][2];  // P as f16 pairs: row g (rows g+8 are zero)
+    uint32_t pa[4];  // P as f16 pairs: row g (rows g+8 are zero)
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
+    for (int nt = 0; nt < 4; ++nt) {
       const float p0 = sc[nt][0] == -INFINITY ? 0.0f : expf(__fsub_rn(sc[nt][0], mn));
       const float p1 = sc[nt][1] == -INFINITY ? 0.0f : expf(__fsub_rn(sc[nt][1], mn));
       ps = __fadd_rn(ps, __fadd_rn(p0, p1));
-      pa[nt][0] = pack_h2(p0, p1);
-      pa[nt][1] = 0u;
+      pa[nt] = pack_h2(p0, p1);
     }
     if (mx != -INFINITY) {  // this unit has visible keys for beam g
       l0 = __fadd_rn(__fmul_rn(l0, al), ps);
@@ -840,18 +854,18 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
         o[nd][1] = __fmul_rn(o[nd][1], al);
       }
     }
-    // O += P V: 4 key k-steps of 16, 8 dim n-tiles of 8
+    // O += P V: 2 key k-steps of 16, 8 dim n-tiles of 8
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
+    for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
       for (int nd = 0; nd < 8; ++nd) {
         uint32_t b0, b1;
         const int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
         ldsm_x2_t(smem_u32(vb + xsw(key, nd)), b0, b1);
-        mma16816(o[nd], pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1], b0, b1);
+        mma16816(o[nd], pa[2 * kk], 0u, pa[2 * kk + 1], 0u, b0, b1);
       }
     }
-    __syncwarp();  // every lane's ldmatrix done before the buffers are restaged
+    __syncwarp();  // every lane's ldmatrix done before this buffer is restaged
   }
   if (threadIdx.x == 0) tr.mark(a.trace, 5);
   // per-beam merge of the 4 warps' states, in warp order

@@ -561,9 +561,9 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
     // once for all beams, mma.sync with the beams as M rows
     AttnArgs t = a;
     t.trace = trace_next("attn_decode_beam");
-    ensure_attr(attn_decode_beam_mma_kernel, attn_beam_mma_smem());
-    launch(attn_decode_beam_mma_kernel, dim3(1, a.NH, a.B / a.beam), dim3(kBtThreads), attn_beam_mma_smem(), st, pdl,
-           t);
+    ensure_attr(attn_decode_beam_mma_kernel, attn_beam_mma_smem(8, 2));
+    launch(attn_decode_beam_mma_kernel, dim3(1, a.NH, a.B / a.beam), dim3(kBtThreads), attn_beam_mma_smem(a.beam, 2),
+           st, pdl, t);
   } else if (a.T == 1 && a.D == 64 && ws_ok) {
     // prefetching split-KV decode: chunks per CTA = the whole window when it is
     // <= 4 chunks (local merge), else groups of <= 4 (64 KB of K/V each)
