@@ -406,6 +406,15 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
   if (tmem_free && row == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tmem_free) : "memory");
   const int cpr = bn * ESZ / 16;  // 16-byte chunks per row
   const int epc = 16 / ESZ;       // elements per chunk
+  // row / chunk of a linear chunk index: a shift when cpr is a power of two (every
+  // 128-wide tile); an integer division per 16-B chunk was ~15% of the kernel's
+  // stall samples (ncu source view, 4096x3072x768)
+  const bool cpr_pow2 = (cpr & (cpr - 1)) == 0;
+  const int cpr_sh = 31 - __clz(cpr);
+  auto split_idx = [&](int idx, int& r, int& ch) {
+    r = cpr_pow2 ? (idx >> cpr_sh) : idx / cpr;
+    ch = idx - r * cpr;
+  };
   if constexpr (MODE == EPI_BIAS_RESID) {
     // residual chunks are loaded 8 at a time before use (one exposed global
     // latency per 8 chunks instead of per chunk)
@@ -415,7 +424,8 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
 #pragma unroll
       for (int u = 0; u < BATCH; ++u) {
         const int idx = base + u * NT;
-        const int r = idx / cpr, ch = idx - r * cpr;
+        int r, ch;
+        split_idx(idx, r, ch);
         const int t = tile_a * kTileA + r, f0 = tile_b * bn + ch * 8;
         const bool fast = idx < kTileA * cpr && t < p.m_tok && f0 + 8 <= p.n_feat && (p.ldr % 8) == 0;
         rv[u] = fast ? *reinterpret_cast<const uint4*>(p.resid + (size_t)t * p.ldr + f0) : make_uint4(0, 0, 0, 0);
@@ -424,7 +434,8 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
       for (int u = 0; u < BATCH; ++u) {
         const int idx = base + u * NT;
         if (idx >= kTileA * cpr) break;
-        const int r = idx / cpr, ch = idx - r * cpr;
+        int r, ch;
+        split_idx(idx, r, ch);
         const int t = tile_a * kTileA + r, f0 = tile_b * bn + ch * 8;
         if (t >= p.m_tok || f0 >= p.n_feat) continue;
         const uint4 val = *reinterpret_cast<const uint4*>(stage + (size_t)r * pitch + ch * 16);
@@ -479,7 +490,8 @@ __device__ __forceinline__ void epi_tile_nonswap(const GemmArgs& p, int tile_a, 
     }
   }
   for (int idx = et; idx < kTileA * cpr; idx += NT) {
-    const int r = idx / cpr, ch = idx - r * cpr;
+    int r, ch;
+    split_idx(idx, r, ch);
     const int t = tile_a * kTileA + r;
     const int f0 = tile_b * bn + ch * epc;
     if (t >= p.m_tok || f0 >= p.n_feat) continue;
