@@ -177,13 +177,18 @@ class DeviceModel:
 
     def session(self, batch: int, capacity: int, max_tokens: int, max_new: int,
                 logits=False, beam: int = 0) -> "Session":
-        key = (batch, capacity, max_tokens, max_new, logits, beam)
+        """The calling thread's session of this shape. Sessions are owned per host
+        thread (its KV cache, scratch, step state and captured graphs), so
+        inference workers sharing one GPU run concurrently on their own streams
+        without touching each other's buffers; each thread keeps at most 16."""
+        tid = threading.get_ident()
+        key = (tid, batch, capacity, max_tokens, max_new, logits, beam)
         with self.lock:
             s = self._sessions.get(key)
             if s is None:
-                if len(self._sessions) >= 16:  # bound the cache; drop the oldest
-                    old = next(iter(self._sessions))
-                    self._sessions.pop(old).close()
+                mine = [k for k in self._sessions if k[0] == tid]
+                if len(mine) >= 16:  # bound this thread's cache; drop its oldest
+                    self._sessions.pop(mine[0]).close()
                 s = Session(self, batch, capacity, max_tokens, max_new, logits, beam=beam)
                 self._sessions[key] = s
             return s

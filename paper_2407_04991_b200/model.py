@@ -753,7 +753,9 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
     cap, max_tokens = _session_shape(c, L, max_new_tokens)
     dm = model.device_model()
     stats = GenerateStats()
-    with dm.lock, torch.cuda.device(dm.device):
+    # the session is this thread's own (DeviceModel.session), so concurrent
+    # generate calls from several host threads (each on its own stream) overlap
+    with torch.cuda.device(dm.device):
         s = dm.session(B, cap, max_tokens, max_new_tokens)
         s.set_remap(table)
         s.set_gen_type(gen_type_id)

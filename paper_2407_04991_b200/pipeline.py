@@ -445,6 +445,25 @@ class _on_device:
         return False
 
 
+class _own_stream:
+    """A private CUDA stream for this worker thread (workers sharing a GPU then
+    overlap: each runs its own sessions and graphs on its own stream)."""
+
+    def __init__(self, dev):
+        self.dev, self.ctx = dev, None
+
+    def __enter__(self):
+        if self.dev is not None and self.dev.type == "cuda":
+            import torch
+            self.ctx = torch.cuda.stream(torch.cuda.Stream(self.dev))
+            self.ctx.__enter__()
+
+    def __exit__(self, *exc):
+        if self.ctx is not None:
+            self.ctx.__exit__(*exc)
+        return False
+
+
 class _Stop:
     """First failure wins; every loop polls it (and the optional deadline), so
     no stage can block forever on a queue."""
@@ -563,7 +582,7 @@ def run_pipeline(items: Sequence[str], model, tokenizer, settings: PipelineSetti
     def inference_stage(dev):
         tm = timing["inference"]
         try:
-            with _on_device(dev):
+            with _on_device(dev), _own_stream(dev):
                 while True:
                     g = _get(q_grp, stop, None)
                     if g is _END:
