@@ -233,9 +233,8 @@ struct GemmPlan {
   int bn, tiles_a, tiles_b, k_blocks, splits, stages;
 };
 
-// Deterministic split count: a function of (features, K, row tiles), so
-// decode results are batch-invariant for batches <= 64 (one row tile); above
-// that the row-tile count can change the split (and summation) order. Splits form one cluster per
+// Deterministic split count: a function of (features, K) for batches of <= 2
+// row tiles (<= 128 rows; batch-invariant), of (features, K, row tiles) above. Splits form one cluster per
 // tile: up to 8 (portable) when there are many tiles, up to 16 (non-portable,
 // one cluster per GPC) when a few tiles must cover the machine.
 // The largest split count whose grid stays within 128 CTAs: every cluster is
@@ -286,7 +285,13 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
     TF_REQUIRE(d.splits <= 16, TF_ERR_ARG, "splits (cluster size) must be <= 16");
     p.splits = d.splits;
   } else {
-    p.splits = (p.swap && d.epilogue != TF_EPI_LOGITS) ? pick_splits(p.tiles_a * p.tiles_b, p.k_blocks) : 1;
+    // up to two 64-row batch tiles take the one-tile split count, so a row's
+    // f32 summation order is the same for every batch of <= 128 rows (batched ==
+    // single bitwise, model.py:8-13; C3 -2.7%); larger batches trade it for one
+    // wave of clusters (at 256 rows the one-tile count costs C4 18%)
+    p.splits = (p.swap && d.epilogue != TF_EPI_LOGITS)
+                   ? pick_splits(p.tiles_a * (p.tiles_b <= 2 ? 1 : p.tiles_b), p.k_blocks)
+                   : 1;
   }
   TF_REQUIRE(p.splits == 1 || d.epilogue != TF_EPI_LOGITS, TF_ERR_ARG,
              "argmax epilogue does not support split-K");

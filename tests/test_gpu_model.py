@@ -77,6 +77,22 @@ def test_batched_equals_single_bitwise(cuda_device, small_model):
     assert batched == single
 
 
+def test_batch_invariance_up_to_128_rows(cuda_device):
+    """A row's generation does not depend on its batch (reference model.py:8-13)
+    for every batch of <= 128 rows: 100 ragged prompts in one batch (two 64-row
+    tiles in the decode GEMMs) and the same prompts in batches of 10 give the
+    same tokens; the decode split-K counts, attention chunking and prefill tiles
+    are independent of the batch at these sizes."""
+    m = P.init_random(c1_cfg(P.DType.F16), 42)
+    prompts = O.synthetic_prompts(8192, 100, 40, seed=9)
+    prompts = [p[:8 + (7 * i) % 33] for i, p in enumerate(prompts)]
+    whole = P.batched_greedy_decode(m, prompts, 24)
+    parts = []
+    for i in range(0, 100, 10):
+        parts += P.batched_greedy_decode(m, prompts[i:i + 10], 24)
+    assert whole == parts
+
+
 def oracle_margins(args, seed, prompts, new):
     """Per-(step, row) top-1 margins of the oracle restatement's own greedy run
     (F16 numerics), for margin-gating token comparisons."""
