@@ -725,26 +725,6 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
   const bool l2pf = l2pf_on && T == 1;
   const unsigned long long lm_bytes = (unsigned long long)m.vocab * m.ldk_h * 2;
   const unsigned long long lm_q = ((lm_bytes / 4) + 255) & ~255ull;
-  auto pf_next = [&](int l, int which) {
-    GemmExtra ex;
-    if (!l2pf) return ex;
-    if (l + 1 < L) {
-      const tf_layer_weights& n = s.m->layers[l + 1];
-      switch (which) {
-        case 0: ex.l2pf = n.wqkv_t; ex.l2pf_bytes = 3ull * H * m.ldk_h * 2; break;
-        case 1: ex.l2pf = n.wo_t; ex.l2pf_bytes = (unsigned long long)H * m.ldk_h * 2; break;
-        case 2: ex.l2pf = n.w1_t; ex.l2pf_bytes = (unsigned long long)F * m.ldk_h * 2; break;
-        default: ex.l2pf = n.w2_t; ex.l2pf_bytes = (unsigned long long)H * m.ldk_f * 2; break;
-      }
-    } else {
-      const unsigned long long lo = which * lm_q;
-      if (lo >= lm_bytes) return ex;
-      ex.l2pf = static_cast<const uint8_t*>(m.lm_head_t) + lo;
-      ex.l2pf_bytes = std::min(lm_q, lm_bytes - lo);
-    }
-    return ex;
-  };
-
   // diagnostics: TF_SPLITS="q,o,f1,f2" forces the decode split counts (0 = auto)
   static const std::vector<int> force_splits = [] {
     std::vector<int> v(4, 0);
@@ -818,6 +798,27 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
           plan_emits_stats(plan_gemm(f2));
   // the lm_head reads the last position's rows: folded only when those are all rows
   const bool lm_fold = lnf && m.lm_head_ln_t && (T == 1 || mode == TF_FWD_LOGITS_ALL);
+  auto pf_next = [&](int l, int which) {
+    GemmExtra ex;
+    if (!l2pf) return ex;
+    if (l + 1 < L) {
+      const tf_layer_weights& n = s.m->layers[l + 1];
+      switch (which) {
+        // the copy the consumer will read: the LayerNorm-folded weights when folded
+        case 0: ex.l2pf = lnf ? n.wqkv_ln_t : n.wqkv_t; ex.l2pf_bytes = 3ull * H * m.ldk_h * 2; break;
+        case 1: ex.l2pf = n.wo_t; ex.l2pf_bytes = (unsigned long long)H * m.ldk_h * 2; break;
+        case 2: ex.l2pf = lnf ? n.w1_ln_t : n.w1_t; ex.l2pf_bytes = (unsigned long long)F * m.ldk_h * 2; break;
+        default: ex.l2pf = n.w2_t; ex.l2pf_bytes = (unsigned long long)H * m.ldk_f * 2; break;
+      }
+    } else {
+      const unsigned long long lo = which * lm_q;
+      if (lo >= lm_bytes) return ex;
+      ex.l2pf = static_cast<const uint8_t*>(lm_fold ? m.lm_head_ln_t : m.lm_head_t) + lo;
+      ex.l2pf_bytes = std::min(lm_q, lm_bytes - lo);
+    }
+    return ex;
+  };
+
   auto set_ln = [&](tf_gemm_desc& d, const float* stats, const void* wt_ln, const float* c, const float* dd) {
     d.act = x;
     d.wt = wt_ln;
