@@ -114,22 +114,28 @@ def make_prompts(V, w, rank):
     return out
 
 
+def _latest_profile(pattern):
+    import glob
+    hits = sorted(glob.glob(os.path.join(ROOT, "profiles", pattern)))
+    return hits[-1] if hits else None
+
+
 def ncu_step_traffic(wname):
-    """DRAM bytes (read + write) of one decode step from the committed ncu
-    per-launch capture (profiles/r1_ncu_step_<w>.json: tools/one_step.py under
+    """DRAM bytes (read + write) of one decode step from the newest committed ncu
+    per-launch capture (profiles/r<N>_ncu_step_<w>.json: tools/one_step.py under
     ncu --cache-control none, summed by tools/step_profile.py), or None."""
-    path = os.path.join(ROOT, "profiles", f"r1_ncu_step_{wname}.json")
-    if not os.path.exists(path):
+    path = _latest_profile(f"r*_ncu_step_{wname}.json")
+    if path is None:
         return None
     with open(path) as fh:
         return float(json.load(fh)["dram_bytes"])
 
 
 def ncu_traffic(kernel_tag="prof_lm_head"):
-    """dram__bytes_read + dram__bytes_write per launch of the dominant kernel from
-    the committed `ncu --set full` capture summary (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "r1_ncu_summary.md")
-    if not os.path.exists(path):
+    """dram read + write per launch of the dominant kernel from the newest
+    committed `ncu --set full` summary (profiles/r<N>_ncu_summary.md), or None."""
+    path = _latest_profile("r*_ncu_summary.md")
+    if path is None:
         return None
     text = open(path).read()
     at = text.find(kernel_tag)
@@ -138,7 +144,7 @@ def ncu_traffic(kernel_tag="prof_lm_head"):
     block = text[at:at + 2000]
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     total = 0.0
-    for key in ("dram__bytes_read.sum = ", "dram__bytes_write.sum = "):
+    for key in ("- dram read: ", "- dram write: "):
         i = block.find(key)
         if i < 0:
             return None

@@ -306,7 +306,11 @@ GemmPlan plan_gemm(const tf_gemm_desc& d) {
   if (st > 8) st = 8;
   // many independent full-K tiles (lm_head): a shallow ring lets 3 CTAs share
   // an SM so one CTA's epilogue overlaps the others' weight streaming
-  if (p.swap && p.splits == 1 && p.tiles_a * p.tiles_b > 148 && st > 3) st = 3;
+  static const int lm_st = [] {  // TF_LM_STAGES: ring depth of these many-tile full-K GEMMs (A/B)
+    const char* e = getenv("TF_LM_STAGES");
+    return e ? atoi(e) : 3;
+  }();
+  if (p.swap && p.splits == 1 && p.tiles_a * p.tiles_b > 148 && st > lm_st) st = lm_st;
   if (st > kb_per) st = kb_per;
   if (st < 1) st = 1;
   p.stages = st;
