@@ -252,9 +252,10 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
   return d;
 }
 // instruction descriptor for kind::f16: A,B f16 K-major, D f32, shape 128 x n
-__host__ __device__ constexpr uint32_t idesc_f16_m128(uint32_t n) {
-  return (1u << 4) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc_f16(uint32_t m, uint32_t n) {
+  return (1u << 4) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
+__host__ __device__ constexpr uint32_t idesc_f16_m128(uint32_t n) { return idesc_f16(128u, n); }
 
 // ---------------------------------------------------------------- clusters / DSMEM
 __device__ __forceinline__ uint32_t cluster_ctarank() {

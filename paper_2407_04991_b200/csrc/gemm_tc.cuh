@@ -1029,3 +1029,156 @@ __global__ void __launch_bounds__(gemm_threads(MODE, SWAP, RED, LNV), 1)
 }
 
 }  // namespace tf
+
+namespace tf {
+
+// ---------------------------------------------------------------- prefill, 2-CTA (cta_group::2)
+// Non-swap GEMM on CTA pairs: a 2-CTA cluster computes a 256-token x 256-feature
+// tile with tcgen05.mma.cta_group::2 (M = 256, N = 256). Each CTA stages its own
+// 128 token rows of A and HALF of the feature rows of B (128) per 64-wide K
+// block — 32 KB per CTA per k-block for 128x256x64 MACs, twice the MACs per
+// staged byte of the 128x128 single-CTA tiles, whose main loop is bound by the
+// per-SM TMA ingest. The leader CTA (rank 0) waits on its full barrier (both
+// CTAs' TMA bytes complete on it: the peer's loads carry the leader's barrier
+// address, the peer's producer arrives remotely) and issues the MMAs reading
+// both CTAs' shared memory at the same offsets; its commits are multicast to
+// both CTAs' empty / done barriers. Every CTA then drains its own TMEM rows
+// (128 tokens x 256 features) with the staged 8-warp epilogue of the
+// single-CTA kernel. Two such CTAs (of different pairs) share an SM: one's
+// epilogue overlaps the other's main loop.
+constexpr int kPf2BN = 256, kPf2Stages = 3;
+constexpr int kPf2StageBytes = 128 * kBK * 2 + 128 * kBK * 2;  // A 16 KB + B half 16 KB
+__host__ __device__ constexpr size_t gemm_pf2_smem_bytes() {
+  return 1024 + (size_t)kPf2Stages * kPf2StageBytes + (2 * kPf2Stages + 1) * 8 + 16;
+}
+
+__device__ __forceinline__ uint32_t peer0_addr(uint32_t smem_addr) {  // the leader CTA's copy of a barrier
+  return smem_addr & 0xFEFFFFFFu;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 1)
+    gemm_pf2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kPf2Stages * kPf2StageBytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kPf2Stages + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int tile_a = blockIdx.x;  // this CTA's 128-token block
+  const int tile_b = blockIdx.y;  // 256-feature block
+  const int nkb = p.k_blocks;
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kPf2Stages),
+                 done_bar = smem_u32(bars + 2 * kPf2Stages);
+  TF_TRACE_INIT(tr);
+  if (threadIdx.x == 0) tr.mark(p.trace, 0);
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kPf2Stages; ++s) {
+      mbar_init(full0 + 8 * s, 2);  // leader: both producers arrive (leader with the expected bytes)
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(done_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();  // both CTAs' barriers initialised and TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer (both CTAs): own A rows, own half of the B rows
+    pdl_wait();
+    if (threadIdx.x == 0) tr.mark(p.trace, 1);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kPf2Stages;
+      const uint32_t ph = (uint32_t)(i / kPf2Stages) & 1u;
+      mbar_wait(empty0 + 8 * s, ph ^ 1u);
+      const uint32_t sa = smem_u32(smem + (size_t)s * kPf2StageBytes);
+      const uint32_t sb = sa + 128 * kBK * 2;
+      const uint32_t fb = full0 + 8 * s;
+      if (leader) {
+        mbar_expect_tx(fb, (uint32_t)(2 * kPf2StageBytes));
+      } else {
+        asm volatile("{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, 0;\n\t"
+                     "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(fb)
+                     : "memory");
+      }
+      asm volatile(
+          "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3}], [%4];" ::"r"(sa),
+          "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(i * kBK), "r"(tile_a * 128), "r"(peer0_addr(fb))
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3}], [%4];" ::"r"(sb),
+          "l"(reinterpret_cast<uint64_t>(&tmB)), "r"(i * kBK), "r"(tile_b * kPf2BN + (int)rank * 128),
+          "r"(peer0_addr(fb))
+          : "memory");
+    }
+  } else if (warp == 1 && leader) {
+    // ---------------- MMA issue (leader only), M = 256 over both CTAs' rows
+    const uint32_t idesc = idesc_f16(256u, (uint32_t)kPf2BN);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kPf2Stages;
+      const uint32_t ph = (uint32_t)(i / kPf2Stages) & 1u;
+      mbar_wait(full0 + 8 * s, ph);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + (size_t)s * kPf2StageBytes);
+      const uint64_t da = umma_desc_sw128(sa);
+      const uint64_t db = umma_desc_sw128(sa + 128 * kBK * 2);
+      if (elect_lane0()) {
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k) {
+          asm volatile(
+              "{\n\t.reg .pred pp;\n\tsetp.ne.b32 pp, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, pp;\n\t}" ::"r"(tmem),
+              "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"((i | k) != 0 ? 1u : 0u)
+              : "memory");
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                empty0 + 8 * s),
+            "h"((unsigned short)3)
+            : "memory");
+      }
+      __syncwarp();
+    }
+    if (elect_lane0())
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+              done_bar),
+          "h"((unsigned short)3)
+          : "memory");
+  }
+  __syncwarp();
+
+  // ---------------- epilogue (all 8 warps, each CTA its own 128 token rows)
+  pdl_wait();
+  mbar_wait(done_bar, 0);
+  tc_fence_after();
+  if (threadIdx.x == 0) tr.mark(p.trace, 2);
+  GemmArgs q = p;
+  q.bn = kPf2BN;
+  epi_tile_nonswap<MODE, false, 256>(q, tile_a, tile_b, tmem + (uint32_t)((warp & 3) * 32 << 16), smem);
+  tc_fence_before();
+  cluster_sync();  // neither CTA frees TMEM / smem while the pair may still touch it
+  if (threadIdx.x == 0) {
+    tr.mark(p.trace, 7);
+    tr.flush(p.trace);
+  }
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+}
+
+}  // namespace tf

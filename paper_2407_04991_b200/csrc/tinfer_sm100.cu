@@ -460,6 +460,37 @@ void run_gemm(const tf_gemm_desc& d, cudaStream_t st, const GemmExtra& ex = Gemm
   const int ldp = p.swap ? d.ldw : d.lda, ldq = p.swap ? d.lda : d.ldw;
   const CUtensorMap ta = make_kmajor_map(P, a.rows_a, kext, ldp, kTileA);
   const CUtensorMap tb = make_kmajor_map(Q, a.rows_b, kext, ldq, p.bn);
+  // prefill on 2-CTA pairs (256 tokens x 256 features per cluster, tcgen05 cta_group::2)
+  static const bool pf2_on = [] {  // TF_PF2=0: single-CTA 128x128 prefill tiles (A/B)
+    const char* e = getenv("TF_PF2");
+    return !(e && e[0] == '0');
+  }();
+  // (only when the pair grid covers the SMs: N = 768 at 4096 tokens gives 96 CTAs,
+  // fewer than the 192 single-CTA tiles, and measured slower)
+  const int pf2_ctas = (p.tiles_a + 1) / 2 * 2 * ((d.n_feat + 255) / 256);
+  const bool pf2 = pf2_on && !p.swap && d.n_feat >= 256 && d.m_tok > 128 && pf2_ctas >= num_sms() &&
+                   (d.epilogue == TF_EPI_BIAS || d.epilogue == TF_EPI_BIAS_GELU || d.epilogue == TF_EPI_BIAS_RESID ||
+                    d.epilogue == TF_EPI_QKV || (d.epilogue == TF_EPI_LOGITS && d.argmax_keys == nullptr));
+  if (pf2) {
+    GemmArgs a2 = a;
+    a2.bn = kPf2BN;
+    a2.stages = kPf2Stages;
+    a2.splits = 1;
+    a2.kb_per_split = p.k_blocks;
+    const dim3 grid((p.tiles_a + 1) / 2 * 2, (d.n_feat + kPf2BN - 1) / kPf2BN, 1);
+    auto go = [&](auto kern) {
+      ensure_attr(kern, gemm_pf2_smem_bytes(), true);
+      launch_cluster3(kern, grid, dim3(256), gemm_pf2_smem_bytes(), st, d.pdl != 0, dim3(2, 1, 1), ta, tb, a2);
+    };
+    switch (d.epilogue) {
+      case TF_EPI_BIAS: go(gemm_pf2_kernel<EPI_BIAS>); break;
+      case TF_EPI_BIAS_GELU: go(gemm_pf2_kernel<EPI_BIAS_GELU>); break;
+      case TF_EPI_BIAS_RESID: go(gemm_pf2_kernel<EPI_BIAS_RESID>); break;
+      case TF_EPI_QKV: go(gemm_pf2_kernel<EPI_QKV>); break;
+      default: go(gemm_pf2_kernel<EPI_LOGITS>); break;
+    }
+    return;
+  }
   switch (d.epilogue) {
     case TF_EPI_F32: launch_gemm_mode<EPI_F32>(d, p, ta, tb, a, st); break;
     case TF_EPI_BIAS: launch_gemm_mode<EPI_BIAS>(d, p, ta, tb, a, st); break;

@@ -49,9 +49,11 @@ def test_gemm_f32_matches_torch(cuda_device, m, n, k, swap, splits):
     assert int(scr.counters.abs().sum().item()) == 0  # split-K counters self-reset
 
 
-@pytest.mark.parametrize("swap", [0, 1])
-def test_gemm_epilogues(cuda_device, swap):
-    m, n, k = 64, 384, 256
+@pytest.mark.parametrize("swap,m,n", [(0, 64, 384), (1, 64, 384), (0, 300, 640), (0, 4096, 2304)])
+def test_gemm_epilogues(cuda_device, swap, m, n):
+    """Bias / GELU / residual epilogues; (0, 300, 640) and (0, 4096, 2304) run the
+    2-CTA prefill kernel (odd 128-row tile count, partial 256-feature tile)."""
+    k = 256
     a = rand16(m, k, seed=3).to(cuda_device)
     w = rand16(n, k, scale=0.05, seed=4).to(cuda_device)
     bias = (torch.randn(n) * 0.1).half().float().to(cuda_device)
