@@ -666,8 +666,8 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const AttnArgs a)
 // (deterministic), the output rounded once.
 constexpr int kBtThreads = 128, kBtMaxUnits = 128;  // <= 16 half-chunks x <= 8 beams
 __host__ __device__ constexpr size_t attn_beam_mma_smem(int R, int nbuf) {
-  // q [16][72] f16 | s_ind [R][512] u8 | 4 warps x nbuf x (K 4 KB + V 4 KB) | merge [4][8][66] f32 (aliases K/V)
-  return 16 * 72 * 2 + (size_t)R * 512 + (size_t)4 * nbuf * 8192 + 64;
+  // q [16][72] f16 | s_ind [R][4096 / R] u8 | 4 warps x nbuf x (K 4 KB + V 4 KB) | merge [4][8][66] f32 (aliases K/V)
+  return 16 * 72 * 2 + 4096 + (size_t)4 * nbuf * 8192 + 64 + 0 * R;
 }
 
 __device__ __forceinline__ uint32_t xsw(int row, int chunk16) {  // 128-B rows, 16-B chunks XOR-swizzled
@@ -679,14 +679,15 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   constexpr int NBUF = 2;
   extern __shared__ __align__(128) uint8_t bt_smem[];
   __half* qs = reinterpret_cast<__half*>(bt_smem);                 // [16][72]
-  uint8_t* s_ind = bt_smem + 16 * 72 * 2;                           // [R][512] source beam per slot
-  uint8_t* kv = s_ind + a.beam * 512;                               // [4 warps][NBUF][K 4 KB | V 4 KB]
-  __shared__ int s_sh[8];
+  uint8_t* s_ind = bt_smem + 16 * 72 * 2;                           // [R][istr] source beam per slot
+  uint8_t* kv = s_ind + 4096;                                       // [4 warps][NBUF][K 4 KB | V 4 KB]
+  __shared__ int s_sh[16];
   __shared__ int s_units, s_unit_c[kBtMaxUnits], s_unit_r[kBtMaxUnits];
   constexpr int D = 64;
   TF_TRACE_INIT(tr);
   if (threadIdx.x == 0) tr.mark(a.trace, 0);
   const int R = a.beam;
+  const int istr = 4096 / R;  // slots per indirection row (window <= 4096 / R slots)
   const int h = blockIdx.y, rq = blockIdx.z, beam0 = rq * R;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
@@ -698,26 +699,15 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   // ---- before the wait: indirection rows, shared chunks, the unit list
   for (int i = tid; i < R * nch * 64; i += kBtThreads) {
     const int r = i / (nch * 64), k = i - r * (nch * 64), s = lo + k;
-    s_ind[r * 512 + k] = (uint8_t)(s < hi ? a.indir[(size_t)(beam0 + r) * a.cap + s] : r);
+    s_ind[r * istr + k] = (uint8_t)((s < hi && a.indir) ? a.indir[(size_t)(beam0 + r) * a.cap + s] : r);
   }
   __syncthreads();
-  if (warp < nch) {
+  for (int c = warp; c < nch; c += 4) {
     bool same = true;
-    for (int k = warp * 64 + lane; k < warp * 64 + 64; k += 32) {
-      const int s = lo + k;
+    for (int kk = c * 64 + lane; kk < c * 64 + 64; kk += 32) {
+      const int s = lo + kk;
       if (s == hi) same = false;  // the newest slot: each beam's own row
-      for (int r = 1; r < R && s < hi; ++r) same = same && s_ind[r * 512 + k] == s_ind[k];
-    }
-    same = __all_sync(0xffffffffu, same);
-    if (lane == 0) s_sh[warp] = same;
-  }
-  if (warp + 4 < nch) {  // windows of up to 8 chunks
-    const int c = warp + 4;
-    bool same = true;
-    for (int k = c * 64 + lane; k < c * 64 + 64; k += 32) {
-      const int s = lo + k;
-      if (s == hi) same = false;
-      for (int r = 1; r < R && s < hi; ++r) same = same && s_ind[r * 512 + k] == s_ind[k];
+      for (int r = 1; r < R && s < hi; ++r) same = same && s_ind[r * istr + kk] == s_ind[kk];
     }
     same = __all_sync(0xffffffffu, same);
     if (lane == 0) s_sh[c] = same;
@@ -756,7 +746,8 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
       if (slot == hi && !after_wait) continue;
       const bool ok = slot <= hi;
       const int rr = ur < 0 ? 0 : ur;
-      const int src = beam0 + (slot == hi ? a.indir[(size_t)(beam0 + rr) * a.cap + hi] : s_ind[rr * 512 + k]);
+      const int src = beam0 + (slot == hi ? (a.indir ? a.indir[(size_t)(beam0 + rr) * a.cap + hi] : rr)
+                                          : s_ind[rr * istr + k]);
       const size_t off = ok ? (size_t)src * row_stride + (size_t)h * head_stride + (size_t)slot * D + prt * 8 : 0;
       cp_async16(smem_u32(kb + xsw(j, prt)), a.kc + off, ok);
       cp_async16(smem_u32(vb + xsw(j, prt)), a.vc + off, ok);
@@ -773,7 +764,7 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
     const int j = hi - lo - hc * 32;
     if (j >= 0 && j < 32 && lane < 8) {
       const int rr = ur < 0 ? 0 : ur;
-      const int src = beam0 + a.indir[(size_t)(beam0 + rr) * a.cap + hi];
+      const int src = beam0 + (a.indir ? a.indir[(size_t)(beam0 + rr) * a.cap + hi] : rr);
       const size_t off = (size_t)src * row_stride + (size_t)h * head_stride + (size_t)hi * D + lane * 8;
       cp_async16(smem_u32(wb + xsw(j, lane)), a.kc + off, true);
       cp_async16(smem_u32(wb + 4096 + xsw(j, lane)), a.vc + off, true);

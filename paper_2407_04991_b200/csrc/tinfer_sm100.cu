@@ -583,6 +583,17 @@ int beam_attn_mode() {
   return mode;
 }
 
+// greedy decode attention kernel choice: -1 (default) the tensor-core unit
+// kernel for capacities > 256 slots, the per-row kernel below; TF_GREEDY_MMA=0 /
+// 1 forces the per-row / unit kernel (A/B)
+int greedy_mma_mode() {
+  static const int m = [] {
+    const char* e = getenv("TF_GREEDY_MMA");
+    return e ? atoi(e) : -1;
+  }();
+  return m;
+}
+
 // TF_PREFILL_TC=0: the mma.sync flash prefill instead of the tcgen05 kernel (A/B)
 bool prefill_tc_on() {
   static const bool on = [] {
@@ -596,7 +607,7 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
   TF_REQUIRE(a.D >= 1 && a.D <= 128, TF_ERR_UNSUPPORTED, "head_dim must be in [1, 128]");
   const bool ws_ok = a.ws && a.cnt && a.max_chunks >= (a.cap + kPfKeysPerChunk - 1) / kPfKeysPerChunk;
   if (a.T == 1 && a.D == 64 && a.indir && a.beam >= 2 && a.beam <= 8 && a.B % a.beam == 0 &&
-      a.cap <= 512 && beam_attn_mode() != 0) {
+      a.cap * a.beam <= 4096 && beam_attn_mode() != 0) {
     // tensor-core beam attention: one CTA per (head, request), shared chunks
     // once for all beams, mma.sync with the beams as M rows
     AttnArgs t = a;
@@ -604,6 +615,17 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
     ensure_attr(attn_decode_beam_mma_kernel, attn_beam_mma_smem(8, 2));
     launch(attn_decode_beam_mma_kernel, dim3(1, a.NH, a.B / a.beam), dim3(kBtThreads), attn_beam_mma_smem(a.beam, 2),
            st, pdl, t);
+  } else if (a.T == 1 && a.D == 64 && !a.indir && a.cap <= 4096 &&
+             (greedy_mma_mode() == 1 || (greedy_mma_mode() < 0 && a.cap > 256))) {
+    // long windows: greedy decode on the unit-streaming tensor-core kernel (one
+    // beam per request; each warp streams its next 32-slot unit while it computes
+    // the current one). Short windows keep the per-row kernel, which stages the
+    // whole window before the PDL wait (C5 buckets: faster from capacity ~320 on)
+    AttnArgs t = a;
+    t.beam = 1;
+    t.trace = trace_next("attn_decode_mma");
+    ensure_attr(attn_decode_beam_mma_kernel, attn_beam_mma_smem(8, 2));
+    launch(attn_decode_beam_mma_kernel, dim3(1, a.NH, a.B), dim3(kBtThreads), attn_beam_mma_smem(1, 2), st, pdl, t);
   } else if (a.T == 1 && a.D == 64 && ws_ok) {
     // prefetching split-KV decode: chunks per CTA = the whole window when it is
     // <= 4 chunks (local merge), else groups of <= 4 (64 KB of K/V each)

@@ -26,7 +26,7 @@ torch.manual_seed(0)
 dev = torch.device("cuda:0")
 fails = []
 for (req, R, hi, starts, share) in CASES:
-    NH, D, cap = 3, 64, 512
+    NH, D, cap = 3, 64, 1024 if hi >= 512 else 512
     rows = req * R
     q = (torch.randn(rows, NH * D) * 0.5).half()
     kc = (torch.randn(rows, NH, cap, D) * 0.5).half()
@@ -65,7 +65,7 @@ assert not fails
 '''
 
 CASES = [(3, 4, 300, [0, 5, 40], 256), (2, 3, 140, [0, 17], 130), (1, 8, 460, [3], 400), (4, 2, 66, [0, 1, 2, 64], 64),
-         (2, 4, 200, [0, 0], 0), (2, 4, 511, [0, 100], 448)]
+         (2, 4, 200, [0, 0], 0), (2, 4, 511, [0, 100], 448), (2, 2, 900, [0, 37], 700), (1, 4, 1000, [9], 512)]
 
 
 @pytest.mark.parametrize("mode", ["1", "0"])

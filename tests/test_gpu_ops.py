@@ -125,9 +125,11 @@ def _attn_ref(q, kc, vc, start, qbase, T, scale):
 
 
 @pytest.mark.parametrize("T,D,qbase", [(1, 64, 40), (1, 16, 5), (1, 4, 3), (16, 64, 0), (37, 64, 0),
-                                       (5, 32, 7), (130, 64, 0), (128, 64, 0), (200, 64, 60), (300, 64, 0)])
+                                       (5, 32, 7), (130, 64, 0), (128, 64, 0), (200, 64, 60), (300, 64, 0),
+                                       (1, 64, 700)])
 def test_attention(cuda_device, T, D, qbase):
-    """T > 1 with D = 64 runs the tcgen05 prefill kernel (S, O in TMEM)."""
+    """T > 1 with D = 64 runs the tcgen05 prefill kernel (S, O in TMEM); T = 1
+    with a capacity > 256 the tensor-core unit kernel (one beam per request)."""
     B, NH, cap = 3, 2, max(192, qbase + T + 8)
     H = NH * D
     q = rand16(B * T, H, seed=9).to(cuda_device)
