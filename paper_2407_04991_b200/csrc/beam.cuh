@@ -162,10 +162,23 @@ __global__ void __launch_bounds__(kSelThreads) beam_select_kernel(const BeamArgs
     if (sc == -INFINITY) continue;
     const float m = s_max[k], lz = s_lz[k];
     const __half* row = a.logits + (size_t)b * a.ldl;
-    for (int v = tid; v < V; v += kSelThreads) {
-      const float lp = __fsub_rn(__fsub_rn(__half2float(row[v]), m), lz);
-      const Cand c{__fadd_rn(sc, lp), k * V + v};
-      if (cand_better(c, worst)) topk_insert_reg(top, K, c, worst);
+    // 8 independent loads in flight per batch: the insert's dependency chain
+    // through `worst` otherwise serialises one L2 round trip per element
+    for (int v0 = tid; v0 < V; v0 += 8 * kSelThreads) {
+      float x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int v = v0 + u * kSelThreads;
+        x[u] = v < V ? __half2float(row[v]) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int v = v0 + u * kSelThreads;
+        if (v >= V) break;
+        const float lp = __fsub_rn(__fsub_rn(x[u], m), lz);
+        const Cand c{__fadd_rn(sc, lp), k * V + v};
+        if (cand_better(c, worst)) topk_insert_reg(top, K, c, worst);
+      }
     }
   }
   // ---- block merge: K rounds of arg-best over the per-thread list heads
