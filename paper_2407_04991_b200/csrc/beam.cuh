@@ -234,4 +234,157 @@ __global__ void __launch_bounds__(kSelThreads) beam_select_kernel(const BeamArgs
   pdl_trigger();
 }
 
+// Cluster form: one 2..8-CTA cluster per request, CTA k owns beam row k (the
+// K rows are scanned in parallel instead of by one CTA): per row the max, the
+// log-sum-exp and the row's own top-K candidates (8 logits in flight per
+// thread), then the leader CTA reads the K lists over DSMEM, picks the top K of
+// the K*K candidates (same total order: larger score, then lower flat index)
+// and rewrites the request's indirection rows, scores and histories.
+constexpr int kSelCThreads = 512, kSelCWarps = kSelCThreads / 32;
+
+__device__ __forceinline__ float sel_block_reduce(float v, bool is_max, float* s_red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  v = is_max ? warp_max(v) : warp_sum(v);
+  __syncthreads();  // s_red free
+  if (lane == 0) s_red[warp] = v;
+  __syncthreads();
+  float t = s_red[0];
+  for (int w = 1; w < kSelCWarps; ++w) t = is_max ? fmaxf(t, s_red[w]) : __fadd_rn(t, s_red[w]);
+  return t;
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kSelCThreads) beam_select_cluster_kernel(const BeamArgs a) {
+  pdl_wait();
+  constexpr int K = KB;
+  __shared__ float s_red[kSelCWarps];
+  __shared__ Cand s_cand[kSelCWarps];
+  __shared__ Cand s_list[kMaxBeam];
+  __shared__ int s_parent[kMaxBeam], s_tok[kMaxBeam];
+  __shared__ float s_best[kMaxBeam];
+  __shared__ unsigned char s_pfin[kMaxBeam];
+  extern __shared__ int s_indir[];  // [K][cap] (leader)
+  const int k = (int)cluster_ctarank(), r = blockIdx.y, V = a.V;
+  const int b = r * K + k;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int len = *a.len_dev;
+  const int step = len - a.prompt_len;
+  const float sc = a.scores[b];
+  const bool fin = a.finished[b] != 0;
+  Cand top[kMaxBeam];
+#pragma unroll
+  for (int j = 0; j < kMaxBeam; ++j) top[j] = Cand{-INFINITY, 0x7fffffff};
+  Cand worst = top[0];
+  if (fin) {  // frozen: proposes only itself, with eos
+    if (tid == 0) topk_insert_reg(top, K, Cand{sc, k * V + a.eos}, worst);
+  } else if (sc != -INFINITY) {
+    const __half* row = a.logits + (size_t)b * a.ldl;
+    float m = -INFINITY;
+    for (int v0 = tid; v0 < V; v0 += 8 * kSelCThreads) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int v = v0 + u * kSelCThreads;
+        if (v < V) m = fmaxf(m, __half2float(row[v]));
+      }
+    }
+    m = sel_block_reduce(m, true, s_red);
+    float z = 0.0f;
+    for (int v0 = tid; v0 < V; v0 += 8 * kSelCThreads) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int v = v0 + u * kSelCThreads;
+        if (v < V) z = __fadd_rn(z, expf(__fsub_rn(__half2float(row[v]), m)));
+      }
+    }
+    const float lz = logf(sel_block_reduce(z, false, s_red));
+    for (int v0 = tid; v0 < V; v0 += 8 * kSelCThreads) {
+      float x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int v = v0 + u * kSelCThreads;
+        x[u] = v < V ? __half2float(row[v]) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int v = v0 + u * kSelCThreads;
+        if (v >= V) break;
+        const Cand c{__fadd_rn(sc, __fsub_rn(__fsub_rn(x[u], m), lz)), k * V + v};
+        if (cand_better(c, worst)) topk_insert_reg(top, K, c, worst);
+      }
+    }
+  }
+  // ---- this row's top K: K rounds of arg-best over the per-thread list heads
+  int head = 0;
+  for (int round = 0; round < K; ++round) {
+    const Cand mine = head < K ? top[0] : Cand{-INFINITY, 0x7fffffff};
+    const Cand wb = cand_shfl_best(mine);
+    if (lane == 0) s_cand[warp] = wb;
+    __syncthreads();
+    if (warp == 0) {
+      const Cand c = cand_shfl_best(lane < kSelCWarps ? s_cand[lane] : Cand{-INFINITY, 0x7fffffff});
+      if (lane == 0) s_cand[0] = c;
+    }
+    __syncthreads();
+    const Cand best = s_cand[0];
+    if (head < K && mine.i == best.i && mine.v == best.v) {
+      ++head;
+#pragma unroll
+      for (int j = 0; j + 1 < kMaxBeam; ++j) top[j] = top[j + 1];
+      top[kMaxBeam - 1] = Cand{-INFINITY, 0x7fffffff};
+    }
+    if (tid == 0) s_list[round] = best;
+    __syncthreads();
+  }
+  cluster_sync();  // every row's list is in its CTA's shared memory
+  if (k == 0) {
+    if (tid == 0) {  // top K of the K x K candidates (unique flat indices)
+      Cand t[kMaxBeam];
+#pragma unroll
+      for (int j = 0; j < kMaxBeam; ++j) t[j] = Cand{-INFINITY, 0x7fffffff};
+      for (int q = 0; q < K; ++q) {
+        const uint32_t base = dsmem_addr(smem_u32(s_list), (uint32_t)q);
+        for (int j = 0; j < K; ++j) {
+          Cand c;
+          c.v = ld_dsmem_f32(base + 8u * j);
+          uint32_t ci;
+          asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(ci) : "r"(base + 8u * j + 4u));
+          c.i = (int)ci;
+          topk_insert(t, K, c);
+        }
+      }
+      for (int j = 0; j < K; ++j) {
+        const int pb = t[j].i / V;
+        s_parent[j] = pb;
+        s_tok[j] = t[j].i - pb * V;
+        s_best[j] = t[j].v;
+      }
+    }
+    __syncthreads();
+    // ---- read everything the children inherit before any row is rewritten
+    if (tid < K) s_pfin[tid] = a.finished[r * K + s_parent[tid]];
+    for (int i = tid; i < K * len; i += kSelCThreads) {
+      const int kk = i / len, sl = i - kk * len;
+      s_indir[kk * a.cap + sl] = a.indir[(size_t)(r * K + kk) * a.cap + sl];
+    }
+    __syncthreads();
+    const int span = min(len + 1, a.cap);
+    for (int i = tid; i < K * span; i += kSelCThreads) {
+      const int kk = i / span, sl = i - kk * span;
+      a.indir[(size_t)(r * K + kk) * a.cap + sl] = (sl < len) ? s_indir[s_parent[kk] * a.cap + sl] : kk;
+    }
+    if (tid < K) {
+      const int bb = r * K + tid, tok = s_tok[tid];
+      a.scores[bb] = s_best[tid];
+      a.finished[bb] = (s_pfin[tid] || tok == a.eos) ? 1 : 0;
+      a.tokens[bb] = tok;
+      if (step < a.max_new) {
+        a.tok_hist[(size_t)step * (a.R * K) + bb] = tok;
+        a.par_hist[(size_t)step * (a.R * K) + bb] = s_parent[tid];
+      }
+    }
+  }
+  cluster_sync();  // the peers' lists stay alive until the leader has read them
+  pdl_trigger();
+}
+
 }  // namespace tf

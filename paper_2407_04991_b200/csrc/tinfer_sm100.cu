@@ -1067,6 +1067,18 @@ BeamArgs beam_args(const Session& s, const tf_beam_desc& d) {
 
 template <int KB>
 void launch_select(const BeamArgs& a, size_t smem, cudaStream_t st, bool pdl) {
+  static const bool cl = [] {  // TF_SELECT_CLUSTER=0: one CTA per request (A/B)
+    const char* e = getenv("TF_SELECT_CLUSTER");
+    return !(e && e[0] == '0');
+  }();
+  if constexpr (KB >= 2) {
+    if (cl) {
+      ensure_attr(beam_select_cluster_kernel<KB>, kMaxSmem - 8192);
+      launch_cluster3(beam_select_cluster_kernel<KB>, dim3(KB, a.R), dim3(kSelCThreads), smem, st, pdl,
+                      dim3(KB, 1, 1), a);
+      return;
+    }
+  }
   ensure_attr(beam_select_kernel<KB>, kMaxSmem - 8192);
   launch(beam_select_kernel<KB>, dim3(a.R), dim3(kSelThreads), smem, st, pdl, a);
 }
