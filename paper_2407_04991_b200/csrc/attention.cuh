@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   __half* qs = reinterpret_cast<__half*>(bt_smem);                 // [16][72]
   uint8_t* s_ind = bt_smem + 16 * 72 * 2;                           // [R][istr] source beam per slot
   uint8_t* kv = s_ind + 4096;                                       // [4 warps][NBUF][K 4 KB | V 4 KB]
-  __shared__ unsigned char s_grp[2 * 64 * 8];  // [32-slot half][leader beam] -> mask of its group
+  __shared__ int s_sh[16];
   __shared__ int s_units, s_unit_c[kBtMaxUnits], s_unit_r[kBtMaxUnits];
   constexpr int D = 64;
   TF_TRACE_INIT(tr);
@@ -702,49 +702,33 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
     s_ind[r * istr + k] = (uint8_t)((s < hi && a.indir) ? a.indir[(size_t)(beam0 + r) * a.cap + s] : r);
   }
   __syncthreads();
-  // units: 32-slot halves of the chunks, one per group of beams whose source
-  // rows agree on every slot of the half (the shared prompt: one unit for all
-  // beams; generated slots: one per distinct ancestry). The newest slot is each
-  // beam's own row (s_ind = r), so its half is always per beam.
-  for (int hu = warp; hu < 2 * nch; hu += 4) {
-    const int k = hu * 32 + lane;
-    const bool valid = k < n;
-    int src[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) src[r] = (r < R && valid) ? s_ind[r * istr + k] : 0;
-    unsigned grp[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) grp[r] = 0u;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      if (r >= R) break;
-      int lead = r;
-#pragma unroll
-      for (int r2 = 0; r2 < 8; ++r2) {
-        if (r2 >= r) break;
-        if (__all_sync(0xffffffffu, src[r] == src[r2])) {
-          lead = r2;
-          break;
-        }
-      }
-#pragma unroll
-      for (int r2 = 0; r2 < 8; ++r2)
-        if (r2 == lead) grp[r2] |= 1u << r;
+  for (int c = warp; c < nch; c += 4) {
+    bool same = true;
+    for (int kk = c * 64 + lane; kk < c * 64 + 64; kk += 32) {
+      const int s = lo + kk;
+      if (s == hi) same = false;  // the newest slot: each beam's own row
+      for (int r = 1; r < R && s < hi; ++r) same = same && s_ind[r * istr + kk] == s_ind[kk];
     }
-    if (lane == 0) {
-#pragma unroll
-      for (int r = 0; r < 8; ++r) s_grp[hu * 8 + r] = (unsigned char)grp[r];
-    }
+    same = __all_sync(0xffffffffu, same);
+    if (lane == 0) s_sh[c] = same;
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0) {  // units: 32-slot halves of the chunks (shared: all beams; else one per beam)
     int u = 0;
-    for (int hu = 0; hu < 2 * nch && hu * 32 < n; ++hu)
-      for (int r = 0; r < R; ++r)
-        if (s_grp[hu * 8 + r] != 0) {
-          s_unit_c[u] = hu;
-          s_unit_r[u++] = s_grp[hu * 8 + r];  // mask of the beams the unit serves
+    for (int c = 0; c < nch; ++c) {
+      for (int hf = 0; hf < 2; ++hf) {
+        if (c * 64 + hf * 32 >= n) break;
+        if (s_sh[c]) {
+          s_unit_c[u] = 2 * c + hf;
+          s_unit_r[u++] = -1;  // all beams
+        } else {
+          for (int r = 0; r < R; ++r) {
+            s_unit_c[u] = 2 * c + hf;
+            s_unit_r[u++] = r;
+          }
         }
+      }
+    }
     s_units = u;
   }
   __syncthreads();
@@ -754,13 +738,14 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   uint8_t* wb = kv + warp * (NBUF * 8192);
   // stage unit u's 32 slots into buffer `buf` (all but the newest slot before the wait)
   auto stage = [&](int u, int buf, bool after_wait) {
-    const int hc = s_unit_c[u], rr = __ffs(s_unit_r[u]) - 1;  // the group's first beam
+    const int hc = s_unit_c[u], ur = s_unit_r[u];
     uint8_t* kb = wb + buf * 8192;
     uint8_t* vb = kb + 4096;
     for (int i = lane; i < 32 * 8; i += 32) {
       const int j = i >> 3, prt = i & 7, k = hc * 32 + j, slot = lo + k;
       if (slot == hi && !after_wait) continue;
       const bool ok = slot <= hi;
+      const int rr = ur < 0 ? 0 : ur;
       const int src = beam0 + (slot == hi ? (a.indir ? a.indir[(size_t)(beam0 + rr) * a.cap + hi] : rr)
                                           : s_ind[rr * istr + k]);
       const size_t off = ok ? (size_t)src * row_stride + (size_t)h * head_stride + (size_t)slot * D + prt * 8 : 0;
@@ -775,9 +760,10 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   if (threadIdx.x == 0) tr.mark(a.trace, 1);
   // the unit staged early may hold the newest slot (written by this layer's QKV GEMM)
   if (warp < units) {
-    const int hc = s_unit_c[warp], rr = __ffs(s_unit_r[warp]) - 1;
+    const int hc = s_unit_c[warp], ur = s_unit_r[warp];
     const int j = hi - lo - hc * 32;
     if (j >= 0 && j < 32 && lane < 8) {
+      const int rr = ur < 0 ? 0 : ur;
       const int src = beam0 + (a.indir ? a.indir[(size_t)(beam0 + rr) * a.cap + hi] : rr);
       const size_t off = (size_t)src * row_stride + (size_t)h * head_stride + (size_t)hi * D + lane * 8;
       cp_async16(smem_u32(wb + xsw(j, lane)), a.kc + off, true);
@@ -812,7 +798,7 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
     __syncwarp();
     const uint8_t* kb = wb + buf * 8192;
     const uint8_t* vb = kb + 4096;
-    const int hc = s_unit_c[u], umask = s_unit_r[u];
+    const int hc = s_unit_c[u], ur = s_unit_r[u];
     // S = Q K^T: 4 key n-tiles of 8
     float sc[4][4];
 #pragma unroll
@@ -825,8 +811,8 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
         mma16816(sc[nt], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
       }
     }
-    // scale + mask (rows: beam g; the unit serves the beams in umask), unit max
-    const bool row_in = g < R && ((umask >> g) & 1);
+    // scale + mask (rows: beam g; the unit serves beam ur, or all), unit max
+    const bool row_in = g < R && (ur < 0 || ur == g);
     float mx = -INFINITY;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
