@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   __half* qs = reinterpret_cast<__half*>(bt_smem);                 // [16][72]
   uint8_t* s_ind = bt_smem + 16 * 72 * 2;                           // [R][istr] source beam per slot
   uint8_t* kv = s_ind + 4096;                                       // [4 warps][NBUF][K 4 KB | V 4 KB]
-  __shared__ int s_sh[16];
+  __shared__ int s_sh[64];  // per 64-slot chunk: all beams share it (window <= 4096 / R slots)
   __shared__ int s_units, s_unit_c[kBtMaxUnits], s_unit_r[kBtMaxUnits];
   constexpr int D = 64;
   TF_TRACE_INIT(tr);
