@@ -28,6 +28,7 @@ import numpy as np
 import torch
 
 from . import _native as N
+from . import workspace
 from .ops import pad64
 from .tensor import round_to, DType
 
@@ -224,9 +225,14 @@ class Session:
         self.k_cache = k_cache if k_cache is not None else torch.zeros(shape, dtype=torch.float16, device=dev)
         self.v_cache = v_cache if v_cache is not None else torch.zeros(shape, dtype=torch.float16, device=dev)
         z16 = lambda n, ld: torch.zeros((n, ld), dtype=torch.float16, device=dev)  # noqa: E731
-        self.x, self.h = z16(rows, dm.ldk_h), z16(rows, dm.ldk_h)
-        self.q, self.attn = z16(rows, dm.ldk_h), z16(rows, dm.ldk_h)
-        self.ffn = z16(rows, dm.ldk_f)
+        # activation buffers: one zeroed arena, lifetime-disjoint buffers share
+        # storage (workspace.py: {ffn, q}, {h, attn}, {x})
+        self.plan = workspace.session_plan(rows, dm.H, dm.F, dm.ldk_h, dm.ldk_f, dm.L)
+        self.arena = torch.zeros(self.plan.arena_bytes(), dtype=torch.uint8, device=dev)
+        offs = self.plan.offsets()
+        for name, ld in (("x", dm.ldk_h), ("h", dm.ldk_h), ("q", dm.ldk_h), ("attn", dm.ldk_h), ("ffn", dm.ldk_f)):
+            o = offs[self.plan.assignment[name]]
+            setattr(self, name, self.arena[o:o + rows * ld * 2].view(torch.float16).view(rows, ld))
         logit_rows = batch if logits == "last" else rows
         self.logits = z16(logit_rows, dm.V) if logits else None
         self.keys = torch.zeros(batch, dtype=torch.int64, device=dev)
