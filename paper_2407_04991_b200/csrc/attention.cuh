@@ -674,6 +674,200 @@ __device__ __forceinline__ uint32_t xsw(int row, int chunk16) {  // 128-B rows, 
   return (uint32_t)(row * 128 + ((chunk16 ^ (row & 7)) << 4));
 }
 
+// ------------------------------------------------------------------ decode, prefetching, tensor cores
+// The per-row prefetching decode kernel (attn_decode_pf_kernel's staging, grid
+// and fixed chunk-order merge) with the per-chunk arithmetic on mma.sync:
+// warp w owns chunk w (G <= 4), q is the single nonzero row of the m16n8k16 A
+// operand (lanes 0-3 hold it, straight from the QKV output), S = q K^T is 32
+// MMAs per chunk, the chunk softmax runs on lanes 0-3 (quad shuffles), and
+// O = P V takes P rounded to f16 (as the beam kernel; 32 MMAs). K and V chunks
+// are staged with the 128-B XOR swizzle (xsw), conflict-free for ldmatrix.
+// Results depend only on the row's own window. Used for multi-wave grids: the
+// arithmetic is not faster than the CUDA-core form, but the 50 KB footprint and
+// shorter CTA lifetime let the next CTAs start sooner (C3 548 vs 560 us/step;
+// a single-wave batch-32 step is 316 vs 313 us, so it keeps the other kernel).
+__global__ void __launch_bounds__(128, 1) attn_decode_pfm_kernel(const AttnArgs a) {
+  extern __shared__ __align__(128) uint8_t pfm_smem[];
+  __shared__ int s_last;
+  constexpr int D = 64;
+  TF_TRACE_INIT(tr);
+  if (threadIdx.x == 0) tr.mark(a.trace, 0);
+  const int G = a.group;
+  uint8_t* kvs = pfm_smem;                                                    // [G][K 8 KB | V 8 KB]
+  float* part_s = reinterpret_cast<float*>(pfm_smem + (size_t)G * kPfChunkBytes);  // [G][66]
+  const int g = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int qbase = *a.qbase_dev;
+  const int lo = a.start[b], hi = qbase;  // window [lo, hi]
+  const int n = hi - lo + 1;
+  const int nch = n > 0 ? (n + 63) / 64 : 0;
+  const int ngr = (nch + G - 1) / G;
+  if (g >= (ngr > 0 ? ngr : 1)) {
+    pdl_trigger();
+    return;
+  }
+  const int c0 = g * G, nc = n > 0 ? min(G, nch - c0) : 0;
+  const size_t row_off = (size_t)b * a.NH * a.cap * D + (size_t)h * a.cap * D;
+  // ---- before the wait: K/V of every slot < hi in this CTA's chunks
+  for (int seg = tid; seg < nc * 64 * 8; seg += 128) {
+    const int i = seg >> 9, j = (seg >> 3) & 63, part = seg & 7;
+    const int slot = lo + (c0 + i) * 64 + j;
+    if (slot != hi) {  // slots past the window are zero-filled (src-size 0)
+      const bool ok = slot < hi;
+      const size_t off = ok ? row_off + (size_t)slot * D + part * 8 : 0;
+      uint8_t* kb = kvs + (size_t)i * kPfChunkBytes;
+      cp_async16(smem_u32(kb + xsw(j, part)), a.kc + off, ok);
+      cp_async16(smem_u32(kb + 8192 + xsw(j, part)), a.vc + off, ok);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  if (a.pf_kc != nullptr && tid < 2 && nc > 0) {
+    // next layer's copy of this CTA's window (contiguous slots of one (b, h))
+    const int s0 = lo + c0 * 64, s1 = min(lo + (c0 + nc) * 64, hi + 1);
+    l2_prefetch_bulk((tid == 0 ? a.pf_kc : a.pf_vc) + row_off + (size_t)s0 * D, (uint32_t)((s1 - s0) * D * 2));
+  }
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) tr.mark(a.trace, 1);
+  __half* orow = a.out + (size_t)b * a.ldo + (size_t)h * D;
+  if (n <= 0) {  // empty window: zeros
+    if (tid < D) orow[tid] = __float2half_rn(0.0f);
+    return;
+  }
+  // ---- after the wait: the newest slot, and q (A operand row 0: lanes 0-3)
+  {
+    const int i = (hi - lo) / 64 - c0, j = (hi - lo) % 64;
+    if (i >= 0 && i < nc && tid < 16) {
+      const int part = tid & 7;
+      const size_t off = row_off + (size_t)hi * D + part * 8;
+      uint8_t* dst = kvs + (size_t)i * kPfChunkBytes + (tid < 8 ? 0 : 8192) + xsw(j, part);
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>((tid < 8 ? a.kc : a.vc) + off);
+    }
+  }
+  const int gq = lane >> 2, tq = lane & 3;
+  uint32_t qa0[4], qa2[4];  // k-step ks: dims ks*16 + 2tq (+1) and ks*16 + 8 + 2tq (+1) of q, row 0 only
+  {
+    const uint32_t* q32 = reinterpret_cast<const uint32_t*>(a.q + (size_t)b * a.ldq + (size_t)h * D);
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      qa0[ks] = gq == 0 ? q32[ks * 8 + tq] : 0u;
+      qa2[ks] = gq == 0 ? q32[ks * 8 + 4 + tq] : 0u;
+    }
+  }
+  cp_async_commit_wait_all();
+  __syncthreads();
+  if (threadIdx.x == 0) tr.mark(a.trace, 2);
+  if (warp < nc) {
+    const int i = warp;
+    const uint8_t* kb = kvs + (size_t)i * kPfChunkBytes;
+    const uint8_t* vb = kb + 8192;
+    const int cnt_keys = min(64, n - (c0 + i) * 64);
+    // S = q K^T over the chunk's 64 keys: 8 n-tiles x 4 k-steps
+    float sc[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.0f;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        uint32_t b0, b1;
+        ldsm_x2(smem_u32(kb + xsw(nt * 8 + (lane & 7), ks * 2 + ((lane >> 3) & 1))), b0, b1);
+        mma16816(sc[nt], qa0[ks], 0u, qa2[ks], 0u, b0, b1);
+      }
+    }
+    // chunk softmax on row 0 (lanes 0-3 hold keys nt*8 + 2tq, +1)
+    float m = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int key = nt * 8 + 2 * tq + e;
+        sc[nt][e] = key < cnt_keys ? __fmul_rn(sc[nt][e], a.scale) : -INFINITY;
+        m = fmaxf(m, sc[nt][e]);
+      }
+    }
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    float z = 0.0f;
+    uint32_t ph[8];  // P as f16 pairs (z sums the f32 weights)
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = sc[nt][0] == -INFINITY ? 0.0f : expf(__fsub_rn(sc[nt][0], m));
+      const float p1 = sc[nt][1] == -INFINITY ? 0.0f : expf(__fsub_rn(sc[nt][1], m));
+      z = __fadd_rn(z, __fadd_rn(p0, p1));
+      ph[nt] = gq == 0 ? pack_h2(p0, p1) : 0u;
+    }
+    z = __fadd_rn(z, __shfl_xor_sync(0xffffffffu, z, 1));
+    z = __fadd_rn(z, __shfl_xor_sync(0xffffffffu, z, 2));
+    // O = P V: 4 key k-steps of 16, 8 dim n-tiles of 8
+    float o[8][4];
+#pragma unroll
+    for (int nd = 0; nd < 8; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.0f;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+      for (int nd = 0; nd < 8; ++nd) {
+        uint32_t b0, b1;
+        const int key = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        ldsm_x2_t(smem_u32(vb + xsw(key, nd)), b0, b1);
+        mma16816(o[nd], ph[2 * kk], 0u, ph[2 * kk + 1], 0u, b0, b1);
+      }
+    }
+    if (gq == 0) {
+      float* dst = part_s + i * 66;
+      if (tq == 0) {
+        dst[0] = m;
+        dst[1] = z;
+      }
+#pragma unroll
+      for (int nd = 0; nd < 8; ++nd) {
+        dst[2 + nd * 8 + 2 * tq] = o[nd][0];
+        dst[2 + nd * 8 + 2 * tq + 1] = o[nd][1];
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) tr.mark(a.trace, 5);
+  // merge in chunk order: M = max m_c, Z = sum z_c e^(m_c - M), O = sum o_c e^(m_c - M)
+  auto merge_into = [&](auto ld, int count) {
+    if (tid < D) {
+      float M = -INFINITY;
+      for (int cc = 0; cc < count; ++cc) M = fmaxf(M, ld(cc * 66));
+      float Z = 0.0f, O = 0.0f;
+      for (int cc = 0; cc < count; ++cc) {
+        const float f = expf(__fsub_rn(ld(cc * 66), M));
+        Z = __fadd_rn(Z, __fmul_rn(ld(cc * 66 + 1), f));
+        O = __fadd_rn(O, __fmul_rn(ld(cc * 66 + 2 + tid), f));
+      }
+      orow[tid] = f16_sat(__fdiv_rn(O, Z));
+    }
+  };
+  if (ngr == 1) {
+    merge_into([&](int e) { return part_s[e]; }, nch);
+  } else {
+    float* part = a.ws + (((size_t)b * a.NH + h) * a.max_chunks) * 66;
+    for (int e = tid; e < nc * 66; e += 128) __stcg(part + (size_t)c0 * 66 + e, part_s[e]);
+    fence_acq_rel_gpu();
+    __syncthreads();
+    if (tid == 0) {
+      const int prev = atomicAdd(a.cnt + (size_t)b * a.NH + h, 1);
+      s_last = (prev == ngr - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+      fence_acq_rel_gpu();
+      merge_into([&](int e) { return __ldcg(part + e); }, nch);
+      if (tid == 0) a.cnt[(size_t)b * a.NH + h] = 0;
+    }
+  }
+  if (threadIdx.x == 0) {
+    tr.mark(a.trace, 7);
+    tr.flush(a.trace);
+  }
+}
+__host__ __device__ inline size_t attn_pfm_smem_bytes(int G) {
+  return (size_t)G * kPfChunkBytes + (size_t)G * 66 * sizeof(float);
+}
+
 // (one buffer per warp at 6 CTAs per SM, one wave at C4, measured slower: 816 vs 789 us per beam step)
 __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(const AttnArgs a) {
   constexpr int NBUF = 2;

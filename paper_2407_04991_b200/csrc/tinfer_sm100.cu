@@ -639,6 +639,18 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
     const int ngr = (nch + gmax - 1) / gmax;
     AttnArgs t = a;
     t.group = (nch + ngr - 1) / ngr;
+    static const bool pfm = [] {  // TF_PF_MMA=0: CUDA-core per-chunk arithmetic everywhere (A/B)
+      const char* e = getenv("TF_PF_MMA");
+      return !(e && e[0] == '0');
+    }();
+    // multi-wave grids (more CTAs than ~4 per SM) take the tensor-core form
+    if (pfm && !a.indir && (long long)ngr * a.NH * a.B > 4ll * num_sms()) {
+      t.trace = trace_next("attn_decode_pfm");
+      const int grp = t.group;
+      ensure_attr(attn_decode_pfm_kernel, attn_pfm_smem_bytes(4));
+      launch(attn_decode_pfm_kernel, dim3(ngr, a.NH, a.B), dim3(128), attn_pfm_smem_bytes(grp), st, pdl, t);
+      return;
+    }
     t.trace = trace_next("attn_decode_pf");
     ensure_attr(attn_decode_pf_kernel<128>, attn_pf_smem_bytes(kPfMaxG));
     launch(attn_decode_pf_kernel<128>, dim3(ngr, a.NH, a.B), dim3(128), attn_pf_smem_bytes(t.group), st, pdl, t);
@@ -1194,7 +1206,24 @@ int tf_attention(int batch, int heads, int head_dim, int cap, int seq_len, const
     a.scale = scale;
     a.out = static_cast<__half*>(out);
     a.ldo = ldo;
-    if (batch > 0 && seq_len > 0) run_attention(a, static_cast<cudaStream_t>(stream), false);
+    if (batch <= 0 || seq_len <= 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    void* scratch = nullptr;
+    if (seq_len == 1 && head_dim == 64) {
+      // the split-KV decode kernels' partials + zeroed arrival counters, stream-
+      // ordered for this call (sessions own theirs), so the operator runs the
+      // same decode kernel as the generation path
+      const int chunks = (cap + kPfKeysPerChunk - 1) / kPfKeysPerChunk;
+      const size_t ws = (size_t)batch * heads * chunks * 66 * sizeof(float);
+      const size_t cnt = (size_t)batch * heads * sizeof(int);
+      TF_CHECK_CUDA(cudaMallocAsync(&scratch, ws + cnt, st));
+      TF_CHECK_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(scratch) + ws, 0, cnt, st));
+      a.ws = static_cast<float*>(scratch);
+      a.cnt = reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) + ws);
+      a.max_chunks = chunks;
+    }
+    run_attention(a, st, false);
+    if (scratch) TF_CHECK_CUDA(cudaFreeAsync(scratch, st));
   });
 }
 

@@ -146,6 +146,30 @@ def test_attention(cuda_device, T, D, qbase):
     assert (out.float().cpu() - ref).abs().max().item() <= 4e-3
 
 
+@pytest.mark.parametrize("B,NH,cap,qbase", [(64, 12, 192, 150), (128, 12, 256, 255), (8, 4, 192, 100),
+                                             (8, 4, 320, 300)])
+def test_decode_attention_per_row_kernels(cuda_device, B, NH, cap, qbase):
+    """T = 1, D = 64 through the operator runs the generation path's decode
+    kernels: multi-wave grids (B*NH > 4 CTAs per SM) the tensor-core per-row
+    kernel, (8, 4, 192) the CUDA-core per-row kernel, capacity 320 the unit
+    kernel; windows start at per-row left pads."""
+    D = 64
+    H = NH * D
+    q = rand16(B, H, seed=21).to(cuda_device)
+    kc = rand16(B, NH, cap, D, seed=22).to(cuda_device)
+    vc = rand16(B, NH, cap, D, seed=23).to(cuda_device)
+    start = torch.randint(0, qbase // 2, (B,), generator=torch.Generator().manual_seed(5), dtype=torch.int32)
+    start[0] = 0
+    qb = torch.tensor([qbase], dtype=torch.int32, device=cuda_device)
+    out = torch.full((B, H), float("nan"), dtype=torch.half, device=cuda_device)
+    scale = 1.0 / math.sqrt(D)
+    ops.attention(q, None, kc, vc, start.to(cuda_device), qb, scale, out, batch=B, heads=NH,
+                  head_dim=D, cap=cap, seq_len=1)
+    torch.cuda.synchronize()
+    ref = _attn_ref(q.cpu(), kc.cpu(), vc.cpu(), start, qbase, 1, scale)
+    assert (out.float().cpu() - ref).abs().max().item() <= 4e-3
+
+
 def test_embed_gather_sum_bit_exact_and_remap(cuda_device):
     V, P, H, n = 50, 20, 96, 13
     tok = rand16(V, H, seed=12, scale=0.05)
