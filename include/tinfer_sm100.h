@@ -160,7 +160,9 @@ int tf_convert(const void* src, int src_f32, long long n, void* dst, int dst_f32
 /* Masked attention over the KV cache (kernels.attend_f32, kernels.py:216-233).
  * q: [batch*seq_len, ldq] (head h at columns h*head_dim); caches [batch, heads,
  * cap, head_dim]; row t of sequence b attends slots [start[b], *qbase_dev + t].
- * seq_len == 1 selects the decode kernel. */
+ * seq_len == 1 selects the decode kernels of the generation path (for head_dim
+ * 64 with split-KV partials + arrival counters allocated stream-ordered on
+ * `stream` for the call: cudaMallocAsync / cudaFreeAsync). */
 int tf_attention(int batch, int heads, int head_dim, int cap, int seq_len, const void* q, int ldq,
                  const void* k_cache, const void* v_cache, const int* start, const int* qbase_dev,
                  float scale, void* out, int ldo, void* stream);
