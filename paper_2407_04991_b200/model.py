@@ -17,6 +17,7 @@ model's dtype tag. Argmax ties break to the lowest token id (model.py:594).
 
 from __future__ import annotations
 
+import itertools
 import json
 import math
 from dataclasses import dataclass, fields
@@ -367,6 +368,19 @@ def _count_forward(c: ModelConfig, B: int, T: int, qbase: int, start_sum: int, l
     COUNTERS.kernels += kernels
 
 
+def _count_decode_steps(c: ModelConfig, B: int, L: int, steps: int, start_sum: int, fused: bool = True) -> None:
+    """``steps`` single-token forwards at cache lengths L, L+1, ... in closed
+    form: the same totals as calling _count_forward once per step."""
+    if steps <= 0:
+        return
+    H, F = c.hidden_size, c.ffn_size
+    COUNTERS.gemm_macs += steps * (c.num_layers * B * (4 * H * H + 2 * H * F) + B * H * c.vocab_size)
+    # step k (qbase = L + k - 1, T = 1) attends qbase + 1 slots per row, minus its pad
+    slots = (L + 1 + L + steps) * steps // 2
+    COUNTERS.attn_macs += c.num_layers * 2 * c.num_heads * c.head_dim * (B * slots - start_sum * steps)
+    COUNTERS.launches += steps * _ref_launches(c, fused)
+
+
 # ---------------------------------------------------------------------------
 # KV cache (reference model.py:293-369), device-resident
 # ---------------------------------------------------------------------------
@@ -651,11 +665,13 @@ def _left_pad(c: ModelConfig, prompts):
         pos = np.broadcast_to(np.arange(L, dtype=np.int32), (B, L)).copy()
         return ids, pos, np.zeros(B, np.int32), lens
     pads = np.asarray([L - n for n in lens], np.int32)
+    flat = np.fromiter(itertools.chain.from_iterable(prompts), np.int32, count=sum(lens))
     ids = np.full((B, L), c.pad_token, np.int32)
-    pos = np.zeros((B, L), np.int32)
-    for i, p in enumerate(prompts):
-        ids[i, pads[i]:] = p
-        pos[i, pads[i]:] = np.arange(lens[i], dtype=np.int32)
+    # row i's tokens land in columns [pads[i], L): one scatter over the flat ids
+    cols = np.arange(L, dtype=np.int32)
+    live = cols[None, :] >= pads[:, None]
+    ids[live] = flat
+    pos = np.maximum(cols[None, :] - pads[:, None], 0).astype(np.int32)
     return ids, pos, pads, lens
 
 
@@ -766,8 +782,7 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
         stats.d2h_bytes = toks.nbytes
     stats.launches = n_pre + n_dec
     _count_forward(c, B, L, 0, int(pads.sum()), B, n_pre, fused)
-    for step in range(1, max_new_tokens):
-        _count_forward(c, B, 1, L + step - 1, int(pads.sum()), B, 0, fused)
+    _count_decode_steps(c, B, L, max_new_tokens - 1, int(pads.sum()), fused)
     COUNTERS.kernels += n_dec
     global LAST_STATS
     LAST_STATS = stats
