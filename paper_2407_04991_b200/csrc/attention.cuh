@@ -891,9 +891,30 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   const int nch = n > 0 ? (n + 63) / 64 : 0;
   const size_t row_stride = (size_t)a.NH * a.cap * D, head_stride = (size_t)a.cap * D;
   // ---- before the wait: indirection rows, shared chunks, the unit list
-  for (int i = tid; i < R * nch * 64; i += kBtThreads) {
-    const int r = i / (nch * 64), k = i - r * (nch * 64), s = lo + k;
-    s_ind[r * istr + k] = (uint8_t)((s < hi && a.indir) ? a.indir[(size_t)(beam0 + r) * a.cap + s] : r);
+  {
+    // indirection rows: the first 4 rows x 512 slots with 16 loads in flight per
+    // thread (late-wave CTAs start while the other CTAs saturate L2; a dependent
+    // load per slot made this staging ~4 us of their critical path), the rest
+    // (beam > 4 or windows > 512) by the plain loop
+    const int per = nch * 64;
+    int v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int r = e >> 2, k = tid + (e & 3) * kBtThreads;
+      v[e] = (r < R && k < per) ? ((lo + k < hi && a.indir) ? a.indir[(size_t)(beam0 + r) * a.cap + lo + k] : r) : 0;
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int r = e >> 2, k = tid + (e & 3) * kBtThreads;
+      if (r < R && k < per) s_ind[r * istr + k] = (uint8_t)v[e];
+    }
+    if (R > 4 || per > 4 * kBtThreads) {
+      for (int i = tid; i < R * per; i += kBtThreads) {
+        const int r = i / per, k = i - r * per;
+        if (r >= 4 || k >= 4 * kBtThreads)
+          s_ind[r * istr + k] = (uint8_t)((lo + k < hi && a.indir) ? a.indir[(size_t)(beam0 + r) * a.cap + lo + k] : r);
+      }
+    }
   }
   __syncthreads();
   for (int c = warp; c < nch; c += 4) {
@@ -907,23 +928,36 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
     if (lane == 0) s_sh[c] = same;
   }
   __syncthreads();
-  if (tid == 0) {  // units: 32-slot halves of the chunks (shared: all beams; else one per beam)
-    int u = 0;
-    for (int c = 0; c < nch; ++c) {
-      for (int hf = 0; hf < 2; ++hf) {
-        if (c * 64 + hf * 32 >= n) break;
-        if (s_sh[c]) {
-          s_unit_c[u] = 2 * c + hf;
-          s_unit_r[u++] = -1;  // all beams
+  if (warp == 0) {
+    // units: 32-slot halves of the chunks in order (shared: one unit for all
+    // beams; else one per beam), placed by a warp prefix sum over the halves
+    int base = 0;
+    for (int h0 = 0; h0 < 2 * nch; h0 += 32) {
+      const int h = h0 + lane;
+      const bool live = h < 2 * nch && h * 32 < n;
+      const bool sh = live && s_sh[h >> 1];
+      const int cnt = live ? (sh ? 1 : R) : 0;
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int u0 = base + incl - cnt;
+      if (live) {
+        if (sh) {
+          s_unit_c[u0] = h;
+          s_unit_r[u0] = -1;  // all beams
         } else {
           for (int r = 0; r < R; ++r) {
-            s_unit_c[u] = 2 * c + hf;
-            s_unit_r[u++] = r;
+            s_unit_c[u0 + r] = h;
+            s_unit_r[u0 + r] = r;
           }
         }
       }
+      base += __shfl_sync(0xffffffffu, incl, 31);
     }
-    s_units = u;
+    if (lane == 0) s_units = base;
   }
   __syncthreads();
   const int units = s_units;
