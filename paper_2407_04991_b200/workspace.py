@@ -62,6 +62,23 @@ def forward_ops(n_layers: int) -> list[Op]:
     return ops
 
 
+def forward_kernels(n_layers: int, folded: bool) -> list[str]:
+    """The kernels one native forward launches: a decode step (T = 1) folds
+    every LayerNorm into the consuming GEMM (5 per layer), a prefill runs the
+    stand-alone LayerNorm kernels (csrc/tinfer_sm100.cu forward)."""
+    names = ["embed"]
+    for layer in range(n_layers):
+        if layer > 0 and not folded:
+            names.append(f"ln1.{layer}")
+        names += [f"qkv.{layer}", f"attention.{layer}", f"wo.{layer}"]
+        if not folded:
+            names.append(f"ln2.{layer}")
+        names += [f"ffn1.{layer}", f"ffn2.{layer}"]
+    if not folded:
+        names.append("final_ln")
+    return names + ["lm_head", "collect"]
+
+
 def analyze_lifetimes(ops: list[Op], live_out: tuple[str, ...] = ()) -> dict[str, list[Interval]]:
     """Per buffer name, the (write index, last read index) interval of every
     value written to it, in order. A value never read spans its write only

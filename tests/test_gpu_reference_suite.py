@@ -12,8 +12,8 @@ is exact f32 arithmetic on the CPU, and a few of its tests assert bitwise or
 This path stores f16 and accumulates f32 on tensor cores for every model
 (DESIGN.md §4): those checks hold here within the north-star tolerance (they
 are restated with tolerances / margin gating in tests/test_gpu_model.py and
-tests/test_gpu_parity_tf.py), not bitwise. Out-of-scope modules (graphopt) are
-listed too. Everything else must pass as written.
+tests/test_gpu_parity_tf.py), not bitwise. Everything else must pass as written
+(``graph-opt`` reports the fused forward's plan, cli.py / workspace.py).
 """
 
 import json
@@ -42,8 +42,6 @@ EXPECTED: dict[str, str] = {
     "1e-5 bound on an f64 straight-line forward",
     "test_model.py::TestForwardFull::test_matches_straightline_oracle_multihead": _F16 + " — max-abs 3.2e-4 vs "
     "the 1e-5 bound",
-    "test_cli.py::TestGraphOptCommand::test_prints_summary": "graph-opt (the reference's operator-graph "
-    "optimiser) is outside the generation hot path (SURVEY §8f-4); the CLI does not provide it",
 }
 
 

@@ -116,3 +116,23 @@ def test_planner_matches_reference_first_fit():
         W.check_plan(plan)
         assert plan.buffer_sizes == ref_plan.buffer_sizes
         assert plan.assignment == ref_plan.assignment
+
+
+def test_graph_opt_cli_reports_the_forward_plan(tmp_path, capsys):
+    """`tinfer graph-opt` prints what the reference's does (cli.py:163-180:
+    nodes / launches / peak bytes, before -> after) for the fused forward, and
+    writes the kernel sequence and buffer plan."""
+    import json
+
+    from paper_2407_04991_b200 import cli
+    out = tmp_path / "plan.json"
+    assert cli.main(["graph-opt", "--out", str(out)]) == 0
+    text = capsys.readouterr().out
+    assert "nodes:" in text and "launches:" in text and "peak bytes:" in text
+    doc = json.loads(out.read_text())
+    L = doc["config"]["num_layers"]
+    assert len(doc["kernels"]) == 5 * L + 3  # decode step: LayerNorms folded into the GEMMs
+    assert doc["assignment"]["q"] == doc["assignment"]["ffn"]
+    assert cli.main(["graph-opt", "--tokens", "16"]) == 0
+    assert f"-> {7 * L + 3}" in capsys.readouterr().out  # prefill: stand-alone LayerNorm kernels
+    assert cli.main(["graph-opt", "--graph", "g.json"]) == 1
