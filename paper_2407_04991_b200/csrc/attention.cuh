@@ -43,6 +43,7 @@ struct AttnArgs {
   // streams its own window of them HBM -> L2 (null = off)
   const __half* pf_kc;
   const __half* pf_vc;
+  const uint8_t* plan;  // beam: per-request plans (kBeamPlanBytes each) from the select, or null
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
@@ -665,6 +666,13 @@ __global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const AttnArgs a)
 // wait. The warps' partial states are merged per beam in warp order
 // (deterministic), the output rounded once.
 constexpr int kBtThreads = 128, kBtMaxUnits = 128;  // <= 16 half-chunks x <= 8 beams
+// Per-request beam plan, written by the beam select of the previous step (which
+// has just rewritten the request's indirection rows) for the next step's
+// attention, so its 12 head CTAs read it instead of each re-deriving it:
+// [0, 4096) source beam per window slot, u8 [beam][4096 / beam] (slot lo + k at
+// k); [4096] unit count; [4112, +4 * kBtMaxUnits) units, (half-chunk << 8) |
+// (beam + 1), beam + 1 = 0 for a unit shared by all beams.
+constexpr int kBeamPlanBytes = 4096 + 16 + 4 * kBtMaxUnits;
 __host__ __device__ constexpr size_t attn_beam_mma_smem(int R, int nbuf) {
   // q [16][72] f16 | s_ind [R][4096 / R] u8 | 4 warps x nbuf x (K 4 KB + V 4 KB) | merge [4][8][66] f32 (aliases K/V)
   return 16 * 72 * 2 + 4096 + (size_t)4 * nbuf * 8192 + 64 + 0 * R;
@@ -890,7 +898,21 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   const int n = hi - lo + 1;
   const int nch = n > 0 ? (n + 63) / 64 : 0;
   const size_t row_stride = (size_t)a.NH * a.cap * D, head_stride = (size_t)a.cap * D;
-  // ---- before the wait: indirection rows, shared chunks, the unit list
+  // ---- before the wait: indirection rows, shared chunks, the unit list (from
+  // the select's plan when there is one)
+  if (a.plan != nullptr) {
+    const uint8_t* P = a.plan + (size_t)rq * kBeamPlanBytes;
+    for (int i = tid; i < 4096 / 16; i += kBtThreads)
+      reinterpret_cast<uint4*>(s_ind)[i] = reinterpret_cast<const uint4*>(P)[i];
+    const int cnt = *reinterpret_cast<const int*>(P + 4096);
+    for (int i = tid; i < kBtMaxUnits; i += kBtThreads) {
+      const int u = reinterpret_cast<const int*>(P + 4112)[i];
+      s_unit_c[i] = u >> 8;
+      s_unit_r[i] = (u & 255) - 1;
+    }
+    if (tid == 0) s_units = cnt;
+    __syncthreads();
+  } else {
   {
     // indirection rows: the first 4 rows x 512 slots with 16 loads in flight per
     // thread (late-wave CTAs start while the other CTAs saturate L2; a dependent
@@ -960,6 +982,7 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
     if (lane == 0) s_units = base;
   }
   __syncthreads();
+  }
   const int units = s_units;
   // two 8 KB unit buffers per warp (K 4 KB | V 4 KB): the next unit streams in
   // while the current one is computed

@@ -34,6 +34,8 @@ struct BeamArgs {
   int* indir;            // [R*K, cap]
   const int* len_dev;    // cache length = slot the fed token will occupy
   int prompt_len;        // step index = *len_dev - prompt_len
+  const int* pads;       // [R*K] left pads (the attention window of request r starts at pads[r*K])
+  uint8_t* plan;         // [R][kBeamPlanBytes] next step's attention plans (cluster select), or null
 };
 
 struct Cand {
@@ -380,6 +382,61 @@ __global__ void __launch_bounds__(kSelCThreads) beam_select_cluster_kernel(const
       if (step < a.max_new) {
         a.tok_hist[(size_t)step * (a.R * K) + bb] = tok;
         a.par_hist[(size_t)step * (a.R * K) + bb] = s_parent[tid];
+      }
+    }
+    if (a.plan != nullptr) {
+      // the next step's attention plan for this request (attention.cuh
+      // kBeamPlanBytes): window [lo, hi = len], the new rows' source per slot,
+      // per 64-slot chunk whether every beam reads the same rows (never the
+      // chunk holding the newest slot, which is each beam's own), and the units
+      uint8_t* P = a.plan + (size_t)r * kBeamPlanBytes;
+      __shared__ int s_shc[64];
+      const int lo = a.pads[r * K], hi = len, istr = 4096 / K;
+      const int n = hi - lo + 1, nch = n > 0 ? (n + 63) / 64 : 0;
+      auto nrow = [&](int kk, int sl) { return sl < len ? s_indir[s_parent[kk] * a.cap + sl] : kk; };
+      for (int i = tid; i < K * n; i += kSelCThreads) {
+        const int kk = i / n, k = i - kk * n;
+        P[kk * istr + k] = (uint8_t)nrow(kk, lo + k);
+      }
+      for (int c = warp; c < nch; c += kSelCWarps) {
+        bool same = true;
+        for (int kq = c * 64 + lane; kq < c * 64 + 64; kq += 32) {
+          const int sl = lo + kq;
+          if (sl == hi) same = false;
+          if (sl < hi) {
+            const int s0 = nrow(0, sl);
+            for (int q = 1; q < K; ++q) same = same && nrow(q, sl) == s0;
+          }
+        }
+        same = __all_sync(0xffffffffu, same);
+        if (lane == 0) s_shc[c] = same;
+      }
+      __syncthreads();
+      if (warp == 0) {  // units in (half-chunk, beam) order, placed by a warp prefix sum
+        int* U = reinterpret_cast<int*>(P + 4112);
+        int base = 0;
+        for (int h0 = 0; h0 < 2 * nch; h0 += 32) {
+          const int hh = h0 + lane;
+          const bool live = hh < 2 * nch && hh * 32 < n;
+          const bool sh = live && s_shc[hh >> 1];
+          const int cnt = live ? (sh ? 1 : K) : 0;
+          int incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int u0 = base + incl - cnt;
+          if (live) {
+            if (sh) {
+              U[u0] = hh << 8;
+            } else {
+              for (int q = 0; q < K; ++q) U[u0 + q] = (hh << 8) | (q + 1);
+            }
+          }
+          base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) *reinterpret_cast<int*>(P + 4096) = base;
       }
     }
   }

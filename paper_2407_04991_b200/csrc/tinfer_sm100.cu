@@ -688,6 +688,10 @@ struct Session {
   tf_beam_desc beam_key{};  // descriptor the beam graph was captured with
   int graph_launches = 0;
   int launches_last = 0;
+  // per-request beam attention plans written by the cluster select; valid for
+  // the next T = 1 forward only (the select sets it, every forward clears it)
+  uint8_t* beam_plan = nullptr;
+  bool plan_valid = false;
 };
 
 int* qbase_zero_ptr() {
@@ -941,6 +945,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     if (T == 1 && sd.beam_indir) {
       at.indir = sd.beam_indir;
       at.beam = sd.beam;
+      if (s.plan_valid) at.plan = s.beam_plan;
     }
     if (T == 1 && D == 64) {  // split-KV decode attention when the session provides scratch
       const int chunks = (sd.capacity + kPfKeysPerChunk - 1) / kPfKeysPerChunk;
@@ -1048,6 +1053,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
     launch_mc(collect_kernel, dim3(1), dim3(256), 0, st, pdl, c);
   }
   ++launches;
+  s.plan_valid = false;  // the cache length moved on: a plan is for one step
   return launches;
 }
 
@@ -1074,17 +1080,30 @@ BeamArgs beam_args(const Session& s, const tf_beam_desc& d) {
   a.indir = s.d.beam_indir;
   a.len_dev = s.d.len_dev;
   a.prompt_len = d.prompt_len;
+  a.pads = s.d.pads;
   return a;
 }
 
-template <int KB>
-void launch_select(const BeamArgs& a, size_t smem, cudaStream_t st, bool pdl) {
+bool select_cluster_on() {
   static const bool cl = [] {  // TF_SELECT_CLUSTER=0: one CTA per request (A/B)
     const char* e = getenv("TF_SELECT_CLUSTER");
     return !(e && e[0] == '0');
   }();
+  return cl;
+}
+
+bool beam_plan_on() {
+  static const bool on = [] {  // TF_BEAM_PLAN=0: every attention CTA derives its unit list (A/B)
+    const char* e = getenv("TF_BEAM_PLAN");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int KB>
+void launch_select(const BeamArgs& a, size_t smem, cudaStream_t st, bool pdl) {
   if constexpr (KB >= 2) {
-    if (cl) {
+    if (select_cluster_on()) {
       ensure_attr(beam_select_cluster_kernel<KB>, kMaxSmem - 8192);
       launch_cluster3(beam_select_cluster_kernel<KB>, dim3(KB, a.R), dim3(kSelCThreads), smem, st, pdl,
                       dim3(KB, 1, 1), a);
@@ -1095,8 +1114,11 @@ void launch_select(const BeamArgs& a, size_t smem, cudaStream_t st, bool pdl) {
   launch(beam_select_kernel<KB>, dim3(a.R), dim3(kSelThreads), smem, st, pdl, a);
 }
 
-void run_beam_select(const Session& s, const tf_beam_desc& d, cudaStream_t st, bool pdl) {
-  const BeamArgs a = beam_args(s, d);
+void run_beam_select(Session& s, const tf_beam_desc& d, cudaStream_t st, bool pdl) {
+  BeamArgs a = beam_args(s, d);
+  // the cluster select also writes the next step's attention plans
+  const bool plan = s.beam_plan && a.K >= 2 && select_cluster_on() && beam_plan_on();
+  if (plan) a.plan = s.beam_plan;
   const size_t smem = (size_t)a.K * a.cap * sizeof(int);
   TF_REQUIRE(smem <= kMaxSmem - 8192, TF_ERR_UNSUPPORTED, "beam: capacity too large");
   switch (a.K) {
@@ -1110,6 +1132,7 @@ void run_beam_select(const Session& s, const tf_beam_desc& d, cudaStream_t st, b
     case 8: launch_select<8>(a, smem, st, pdl); break;
     default: throw TfError{TF_ERR_UNSUPPORTED, "beam width must be in [1, 8]"};
   }
+  s.plan_valid = plan;
 }
 
 // one beam step: feed `tokens` (generated ids, no remap), last-row logits, select
@@ -1321,6 +1344,8 @@ int tf_session_create(void* model, const tf_session_desc* d, void** session) {
     Session* s = new Session();
     s->m = static_cast<Model*>(model);
     s->d = *d;
+    if (d->beam_indir && d->beam >= 2 && d->batch % d->beam == 0)
+      TF_CHECK_CUDA(cudaMalloc(&s->beam_plan, (size_t)(d->batch / d->beam) * kBeamPlanBytes));
     *session = s;
   });
 }
@@ -1331,6 +1356,7 @@ int tf_session_destroy(void* session) {
     if (s && s->graph) cudaGraphExecDestroy(s->graph);
     if (s && s->graph_multi) cudaGraphExecDestroy(s->graph_multi);
     if (s && s->beam_graph) cudaGraphExecDestroy(s->beam_graph);
+    if (s && s->beam_plan) cudaFree(s->beam_plan);
     delete s;
   });
 }
