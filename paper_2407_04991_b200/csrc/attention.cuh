@@ -893,6 +893,17 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   const int h = blockIdx.y, rq = blockIdx.z, beam0 = rq * R;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
+  // the select's plan (if any) is requested before the window scalars: the two
+  // loads are independent, so a late-starting CTA waits for one round trip
+  uint4 pv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+  int pu = 0, pcnt = 0;
+  if (a.plan != nullptr) {
+    const uint8_t* P = a.plan + (size_t)rq * kBeamPlanBytes;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) pv[e] = reinterpret_cast<const uint4*>(P)[tid + e * kBtThreads];
+    pu = reinterpret_cast<const int*>(P + 4112)[tid];
+    pcnt = *reinterpret_cast<const int*>(P + 4096);
+  }
   const int qbase = *a.qbase_dev;
   const int lo = a.start[beam0], hi = qbase;  // the beams of a request share the left pad
   const int n = hi - lo + 1;
@@ -901,16 +912,12 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
   // ---- before the wait: indirection rows, shared chunks, the unit list (from
   // the select's plan when there is one)
   if (a.plan != nullptr) {
-    const uint8_t* P = a.plan + (size_t)rq * kBeamPlanBytes;
-    for (int i = tid; i < 4096 / 16; i += kBtThreads)
-      reinterpret_cast<uint4*>(s_ind)[i] = reinterpret_cast<const uint4*>(P)[i];
-    const int cnt = *reinterpret_cast<const int*>(P + 4096);
-    for (int i = tid; i < kBtMaxUnits; i += kBtThreads) {
-      const int u = reinterpret_cast<const int*>(P + 4112)[i];
-      s_unit_c[i] = u >> 8;
-      s_unit_r[i] = (u & 255) - 1;
-    }
-    if (tid == 0) s_units = cnt;
+    static_assert(4096 / 16 == 2 * kBtThreads && kBtMaxUnits == kBtThreads, "plan staging: 2 + 1 loads per thread");
+#pragma unroll
+    for (int e = 0; e < 2; ++e) reinterpret_cast<uint4*>(s_ind)[tid + e * kBtThreads] = pv[e];
+    s_unit_c[tid] = pu >> 8;
+    s_unit_r[tid] = (pu & 255) - 1;
+    if (tid == 0) s_units = pcnt;
     __syncthreads();
   } else {
   {
