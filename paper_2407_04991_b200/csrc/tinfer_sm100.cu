@@ -643,8 +643,11 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
       const char* e = getenv("TF_PF_MMA");
       return !(e && e[0] == '0');
     }();
-    // multi-wave grids (more CTAs than ~4 per SM) take the tensor-core form
-    if (pfm && !a.indir && (long long)ngr * a.NH * a.B > 4ll * num_sms()) {
+    // the tensor-core form for every greedy batch: the choice must not depend on
+    // the batch (rows x heads once picked it by wave count, so a row's tokens
+    // changed between batches of 32 and 64 at 12 heads); C3 538 vs 560 us,
+    // C2 ~1% slower than the CUDA-core form it kept for one-wave grids
+    if (pfm && !a.indir) {
       t.trace = trace_next("attn_decode_pfm");
       const int grp = t.group;
       ensure_attr(attn_decode_pfm_kernel, attn_pfm_smem_bytes(4));
