@@ -690,10 +690,10 @@ __device__ __forceinline__ uint32_t xsw(int row, int chunk16) {  // 128-B rows, 
 // MMAs per chunk, the chunk softmax runs on lanes 0-3 (quad shuffles), and
 // O = P V takes P rounded to f16 (as the beam kernel; 32 MMAs). K and V chunks
 // are staged with the 128-B XOR swizzle (xsw), conflict-free for ldmatrix.
-// Results depend only on the row's own window. Used for multi-wave grids: the
-// arithmetic is not faster than the CUDA-core form, but the 50 KB footprint and
-// shorter CTA lifetime let the next CTAs start sooner (C3 548 vs 560 us/step;
-// a single-wave batch-32 step is 316 vs 313 us, so it keeps the other kernel).
+// Results depend only on the row's own window. Used for every greedy batch
+// (the choice must not depend on the batch): on multi-wave grids the 50 KB
+// footprint and shorter CTA lifetime let the next CTAs start sooner (C3 538 vs
+// 560 us/step); at one wave it is level with the CUDA-core form (C2 311 vs 312).
 __global__ void __launch_bounds__(128, 1) attn_decode_pfm_kernel(const AttnArgs a) {
   extern __shared__ __align__(128) uint8_t pfm_smem[];
   __shared__ int s_last;
