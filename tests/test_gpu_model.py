@@ -93,14 +93,14 @@ def test_batch_invariance_up_to_128_rows(cuda_device):
     assert whole == parts
 
 
-@pytest.mark.parametrize("lo,hi,new", [(20, 150, 40), (240, 400, 24)])
+@pytest.mark.parametrize("lo,hi,new", [(20, 150, 40), (240, 400, 24), (150, 300, 40)])
 def test_batch_invariance_ernie_heads(cuda_device, lo, hi, new):
     """Batch invariance at the Ernie-base head layout (12 heads x 64, H=768):
     128 ragged rows in one batch vs the same rows in batches of 64, 32, 8 and 1.
     The decode attention grid (rows x 12 heads) crosses from one wave to several
     between these batch sizes, so the kernel choice must not depend on it.
-    (20..150, +40): every window <= 256 slots (per-row kernel); (240..400, +24):
-    every window > 256 slots (unit kernel)."""
+    (20..150, +40): every window <= 256 slots; (240..400, +24): every window
+    > 256 slots; (150..300, +40): rows on both sides of 256 in one batch."""
     cfg = P.ModelConfig(2048, 768, 2, 12, 64, 1024, 512, P.DType.F16, 1, 2)
     m = P.init_random(cfg, 5)
     prompts = O.synthetic_prompts(2048, 128, hi, seed=3)

@@ -150,9 +150,9 @@ def test_attention(cuda_device, T, D, qbase):
                                              (8, 4, 320, 300)])
 def test_decode_attention_per_row_kernels(cuda_device, B, NH, cap, qbase):
     """T = 1, D = 64 through the operator runs the generation path's decode
-    kernels: multi-wave grids (B*NH > 4 CTAs per SM) the tensor-core per-row
-    kernel, (8, 4, 192) the CUDA-core per-row kernel, capacity 320 the unit
-    kernel; windows start at per-row left pads."""
+    kernels: capacities <= 256 the tensor-core per-row kernel (whatever the
+    grid: one wave at (8, 4, 192), several at (64, 12, 192)), capacity 320 the
+    unit kernel; windows start at per-row left pads."""
     D = 64
     H = NH * D
     q = rand16(B, H, seed=21).to(cuda_device)
@@ -168,6 +168,36 @@ def test_decode_attention_per_row_kernels(cuda_device, B, NH, cap, qbase):
     torch.cuda.synchronize()
     ref = _attn_ref(q.cpu(), kc.cpu(), vc.cpu(), start, qbase, 1, scale)
     assert (out.float().cpu() - ref).abs().max().item() <= 4e-3
+
+
+def test_decode_attention_capacity_invariant(cuda_device):
+    """A row's decode attention output does not depend on the capacity of the
+    cache it sits in (which the batch's longest prompt sets): the same windows
+    placed in caches of 192 ... 1024 slots give bitwise equal outputs within
+    each kernel class, and the per-row (<= 256 slots) and unit (> 256 slots)
+    kernels are reported against each other."""
+    B, NH, D, qbase = 16, 12, 64, 180
+    H = NH * D
+    q = rand16(B, H, seed=31).to(cuda_device)
+    k0 = rand16(B, NH, 192, D, seed=32)
+    v0 = rand16(B, NH, 192, D, seed=33)
+    start = torch.randint(0, 150, (B,), generator=torch.Generator().manual_seed(6), dtype=torch.int32).to(cuda_device)
+    qb = torch.tensor([qbase], dtype=torch.int32, device=cuda_device)
+    outs = {}
+    for cap in (192, 256, 320, 448, 1024):
+        kc = torch.zeros(B, NH, cap, D, dtype=torch.half)
+        vc = torch.zeros(B, NH, cap, D, dtype=torch.half)
+        kc[:, :, :192], vc[:, :, :192] = k0, v0
+        out = torch.empty(B, H, dtype=torch.half, device=cuda_device)
+        ops.attention(q, None, kc.to(cuda_device), vc.to(cuda_device), start, qb, 0.125, out, batch=B, heads=NH,
+                      head_dim=D, cap=cap, seq_len=1)
+        torch.cuda.synchronize()
+        outs[cap] = out.cpu()
+    assert torch.equal(outs[192], outs[256])
+    assert torch.equal(outs[320], outs[448]) and torch.equal(outs[320], outs[1024])
+    diff = (outs[192].float() - outs[320].float()).abs().max().item()
+    print(f"per-row vs unit kernel max-abs {diff:.3e}, bitwise {torch.equal(outs[192], outs[320])}")
+    assert diff <= 2e-3
 
 
 def test_embed_gather_sum_bit_exact_and_remap(cuda_device):
