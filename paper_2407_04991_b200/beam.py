@@ -31,29 +31,26 @@ from .model import ModelConfig, Model, _count_forward, _left_pad, _session_shape
 
 
 def _backtrack(c: ModelConfig, prompts, scores, tok_hist, par_hist, K: int):
-    out = []
-    steps = tok_hist.shape[0]
-    for r, prompt in enumerate(prompts):
-        row = scores[r * K:(r + 1) * K]
-        k = int(np.argmax(row))  # first max -> lowest beam index
-        rev = []
-        for t in range(steps - 1, -1, -1):
-            b = r * K + k
-            rev.append(int(tok_hist[t, b]))
-            k = int(par_hist[t, b])
-        gen = []
-        for tok in reversed(rev):
-            gen.append(tok)
-            if tok == c.eos_token:
-                break
-        out.append(list(prompt) + gen)
-    return out
+    """Best hypothesis per request (first max -> lowest beam index), followed back
+    through the parent history for every request at once (one vectorised gather
+    per step), cut after its first eos."""
+    R, steps = len(prompts), tok_hist.shape[0]
+    k = np.argmax(np.asarray(scores).reshape(R, K), axis=1)
+    base = np.arange(R) * K
+    toks = np.empty((R, steps), dtype=np.int64)
+    for t in range(steps - 1, -1, -1):
+        b = base + k
+        toks[:, t] = tok_hist[t, b]
+        k = par_hist[t, b]
+    hit = toks == c.eos_token
+    cut = np.where(hit.any(axis=1), hit.argmax(axis=1) + 1, steps)
+    return [list(p) + toks[r, :cut[r]].tolist() for r, p in enumerate(prompts)]
 
 
 class BeamRun:
     """Device state of one beam-search call (prepare -> run_device -> finish)."""
 
-    def __init__(self, model: Model, prompts, max_new_tokens: int, beam_width: int):
+    def __init__(self, model: Model, prompts, max_new_tokens: int, beam_width: int, validated: bool = False):
         import torch
 
         from .errors import ParameterError
@@ -64,10 +61,12 @@ class BeamRun:
         if beam_width > c.vocab_size:
             raise ParameterError("beam_width must not exceed vocab_size")
         self.model, self.c = model, c
-        self.prompts = _validate_prompts(c, prompts, max_new_tokens)
+        # validated: the caller already ran _validate_prompts on these prompts
+        self.prompts = prompts if validated else _validate_prompts(c, prompts, max_new_tokens)
         self.new, self.K, self.R = max_new_tokens, beam_width, len(self.prompts)
-        flat = [p for p in self.prompts for _ in range(self.K)]
-        self.ids, self.pos, self.pads, _ = _left_pad(c, flat)
+        # each request's padded row repeated for its K beams
+        ids, pos, pads, _ = _left_pad(c, self.prompts)
+        self.ids, self.pos, self.pads = (np.repeat(a, self.K, axis=0) for a in (ids, pos, pads))
         self.B, self.L = self.ids.shape
         cap, max_tokens = _session_shape(c, self.L, max_new_tokens)
         self.dm = model.device_model()
@@ -143,7 +142,7 @@ def beam_search_decode(model: Model, prompts: list[list[int]], max_new_tokens: i
         return [list(p) for p in checked]
     dm = model.device_model()
     with dm.lock, torch.cuda.device(dm.device):  # the session is created and used under the lock
-        run = BeamRun(model, checked, max_new_tokens, beam_width)
+        run = BeamRun(model, checked, max_new_tokens, beam_width, validated=True)
         h2d = run.stage_inputs()
         run.run_device(use_graph)
         seqs, d2h = run.finish()

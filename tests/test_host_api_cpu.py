@@ -122,3 +122,38 @@ def test_vocab_map_tsv(tmp_path):
     p.write_text("3\t0\n7\t2\n", encoding="utf-8")
     with pytest.raises(P.FormatError):
         PR.read_vocab_map(p)
+
+
+def test_beam_backtrack_vectorised_matches_per_request_walk():
+    """beam._backtrack follows every request's parents at once; the result equals
+    the per-request walk (first max score -> lowest beam index; cut after the
+    first eos) on random histories."""
+    from paper_2407_04991_b200.beam import _backtrack
+
+    class C:
+        eos_token = 1
+
+    def walk(prompts, scores, th, ph, K):
+        out = []
+        for r, p in enumerate(prompts):
+            k = int(np.argmax(scores[r * K:(r + 1) * K]))
+            rev = []
+            for t in range(th.shape[0] - 1, -1, -1):
+                rev.append(int(th[t, r * K + k]))
+                k = int(ph[t, r * K + k])
+            gen = []
+            for tok in reversed(rev):
+                gen.append(tok)
+                if tok == C.eos_token:
+                    break
+            out.append(list(p) + gen)
+        return out
+
+    g = np.random.default_rng(0)
+    for R, K, T in [(5, 4, 9), (64, 4, 128), (3, 1, 5), (7, 8, 1)]:
+        scores = g.standard_normal(R * K).astype(np.float32)
+        scores[:K] = 0.5  # tie inside request 0
+        th = g.integers(0, 6, (T, R * K)).astype(np.int32)
+        ph = g.integers(0, K, (T, R * K)).astype(np.int32)
+        prompts = [[9] * int(x) for x in g.integers(1, 4, R)]
+        assert _backtrack(C, prompts, scores, th, ph, K) == walk(prompts, scores, th, ph, K)
