@@ -686,6 +686,22 @@ def _session_shape(c: ModelConfig, L: int, max_new_tokens: int) -> tuple[int, in
     return max(cap, min(L + max_new_tokens, c.max_position)), r64(L)
 
 
+def _equal_length_ids(c: ModelConfig, prompts, max_new_tokens: int) -> np.ndarray | None:
+    """Fast path of _validate_prompts for a batch of equal-length integer prompts
+    (one array conversion and vectorised range checks). None whenever any check
+    would fail or the input is not such a batch: the caller then runs the
+    per-id validation, which raises the reference's errors."""
+    try:
+        arr = np.asarray(prompts)
+    except (ValueError, TypeError):
+        return None
+    if arr.ndim != 2 or arr.dtype.kind not in "iu" or arr.shape[1] < 1 or max_new_tokens < 0:
+        return None
+    if arr.shape[1] + max_new_tokens > c.max_position or arr.min() < 0 or arr.max() >= c.vocab_size:
+        return None
+    return arr
+
+
 def _validate_prompts(c: ModelConfig, prompts, max_new_tokens: int) -> list[list[int]]:
     checked = []
     for p in prompts:
@@ -741,7 +757,7 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
     c = model.config
     if not prompts:
         return []
-    table = None
+    table = arr = None
     if prompt_vocab_map is not None:
         table = prompt_vocab_map.remap_table()
         for p in prompts:  # original-vocabulary ids: only the sign/length checks apply
@@ -750,12 +766,22 @@ def batched_greedy_decode(model: Model, prompts: list[list[int]], max_new_tokens
             if len(p) + max_new_tokens > c.max_position:
                 raise PositionError("prompt + max_new_tokens exceeds max_position")
         checked = [[int(t) for t in p] for p in prompts]
+        seqs = [list(p) for p in checked]
     else:
-        checked = _validate_prompts(c, prompts, max_new_tokens)
-    seqs = [list(p) for p in checked]
+        arr = _equal_length_ids(c, prompts, max_new_tokens)
+        if arr is not None:  # every prompt valid, same length: no per-id Python work
+            checked = seqs = arr.tolist()
+        else:
+            checked = _validate_prompts(c, prompts, max_new_tokens)
+            seqs = [list(p) for p in checked]
     if max_new_tokens == 0:
         return seqs
-    ids, pos, pads, lens = _left_pad(c, checked)
+    if arr is not None:
+        B, L = arr.shape
+        ids, pads, lens = arr.astype(np.int32), np.zeros(B, np.int32), [L] * B
+        pos = np.broadcast_to(np.arange(L, dtype=np.int32), (B, L)).copy()
+    else:
+        ids, pos, pads, lens = _left_pad(c, checked)
     B, L = ids.shape
     types = None
     if type_ids is not None:
