@@ -376,7 +376,7 @@ def run_reference(args):
     v = float(base["value"])
     line = base_line(args, w, args.gpus, v, 1e3 * w["batch"] * w["new"] / v)
     line["impl"] = "reference"
-    line["config"]["parallelism"] = "cpu (rank 0 only)"
+    line["executor"] = "host CPU, rank 0 only (the reference path has no GPU code); config = our arm's workload"
     line["cpu_baseline"] = base
     line["e2e"] = {"value": v, "unit": "generated tokens/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}
