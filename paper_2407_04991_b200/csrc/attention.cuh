@@ -477,13 +477,10 @@ __global__ void __launch_bounds__(kPfThreads, 1) attn_decode_pf_kernel(const Att
   }
 }
 
-// ------------------------------------------------------------------ prefill, tensor cores
-// head_dim 64. One CTA = 64 query rows of one (head, sequence), 4 warps x 16 rows.
-// Key/value tiles of 64 slots (aligned to the row's first valid slot `start`, so
-// the arithmetic of a row never depends on how much padding its batch carries)
-// are staged with cp.async; S = Q K^T and O += P V run on mma.sync m16n8k16
-// (f16 in, f32 accumulate); the softmax is online (flash) in f32 registers.
-constexpr int kFaRows = 64, kFaKeys = 64, kFaPitch = 72;  // 144-byte smem rows
+// ------------------------------------------------------------------ mma.sync helpers
+// ldmatrix / m16n8k16 (f16 in, f32 accumulate) for the decode attention kernels,
+// whose per-row tiles (one query row, or the R beams of a request) are far below
+// the 64-128-row minimum of a tcgen05 MMA.
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -508,145 +505,6 @@ __device__ __forceinline__ uint32_t pack_h2(float x, float y) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-__global__ void __launch_bounds__(128) attn_prefill_mma_kernel(const AttnArgs a) {
-  __shared__ __align__(128) __half qsm[kFaRows * kFaPitch];
-  __shared__ __align__(128) __half ksm[kFaKeys * kFaPitch];
-  __shared__ __align__(128) __half vsm[kFaKeys * kFaPitch];
-  pdl_wait();
-  pdl_trigger();
-  constexpr int D = 64;
-  const int qblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, tq = lane & 3;
-  const int qbase = *a.qbase_dev;
-  const int lo = a.start[b];
-  const int t0 = qblk * kFaRows;
-  const int rows = min(kFaRows, a.T - t0);
-  const size_t head_off = ((size_t)b * a.NH + h) * a.cap * D;
-  const __half* K = a.kc + head_off;
-  const __half* V = a.vc + head_off;
-  // Q tile -> smem (rows beyond T zero)
-  for (int i = tid; i < kFaRows * 8; i += 128) {
-    const int r = i >> 3, c = (i & 7) * 8;
-    const bool ok = r < rows;
-    cp_async16(smem_u32(qsm + r * kFaPitch + c),
-               ok ? (const void*)(a.q + (size_t)(b * a.T + t0 + r) * a.ldq + h * D + c) : (const void*)a.q, ok);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  // Q fragments of this warp's 16 rows, 4 k-steps of 16 dims
-  uint32_t qa[4][4];
-  {
-    const int r = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      const int c = ks * 16 + (lane >> 4) * 8;
-      ldsm_x4(smem_u32(qsm + r * kFaPitch + c), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
-    }
-  }
-  const int row0 = t0 + warp * 16 + g, row1 = row0 + 8;  // query rows of this thread
-  const int hi0 = qbase + row0, hi1 = qbase + row1;       // last visible slot
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.0f, l1 = 0.0f;
-  float o[8][4];
-#pragma unroll
-  for (int nd = 0; nd < 8; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.0f;
-  const int hi_blk = qbase + t0 + rows - 1;
-  for (int k0 = lo; k0 <= hi_blk; k0 += kFaKeys) {
-    __syncthreads();
-    for (int i = tid; i < kFaKeys * 8; i += 128) {
-      const int r = i >> 3, c = (i & 7) * 8;
-      const int slot = k0 + r;
-      const bool ok = slot < a.cap;
-      cp_async16(smem_u32(ksm + r * kFaPitch + c), ok ? (const void*)(K + (size_t)slot * D + c) : (const void*)K, ok);
-      cp_async16(smem_u32(vsm + r * kFaPitch + c), ok ? (const void*)(V + (size_t)slot * D + c) : (const void*)V, ok);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-    // S = Q K^T: 8 key n-tiles of 8
-    float sc[8][4];
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.0f;
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        uint32_t b0, b1;
-        ldsm_x2(smem_u32(ksm + (nt * 8 + (lane & 7)) * kFaPitch + ks * 16 + ((lane >> 3) & 1) * 8), b0, b1);
-        mma16816(sc[nt], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
-      }
-    }
-    // scale + mask, row maxima
-    float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int slot = k0 + nt * 8 + 2 * tq + e;
-        sc[nt][e] = slot <= hi0 ? __fmul_rn(sc[nt][e], a.scale) : -INFINITY;
-        sc[nt][2 + e] = slot <= hi1 ? __fmul_rn(sc[nt][2 + e], a.scale) : -INFINITY;
-        mx0 = fmaxf(mx0, sc[nt][e]);
-        mx1 = fmaxf(mx1, sc[nt][2 + e]);
-      }
-    }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    const float al0 = (m0 == -INFINITY) ? 0.0f : expf(m0 - mn0);
-    const float al1 = (m1 == -INFINITY) ? 0.0f : expf(m1 - mn1);
-    m0 = mn0;
-    m1 = mn1;
-    float ps0 = 0.0f, ps1 = 0.0f;
-    uint32_t pa[8][2];  // P as f16 pairs: [n-tile][row g / row g+8]
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      const float p00 = sc[nt][0] == -INFINITY ? 0.0f : expf(sc[nt][0] - mn0);
-      const float p01 = sc[nt][1] == -INFINITY ? 0.0f : expf(sc[nt][1] - mn0);
-      const float p10 = sc[nt][2] == -INFINITY ? 0.0f : expf(sc[nt][2] - mn1);
-      const float p11 = sc[nt][3] == -INFINITY ? 0.0f : expf(sc[nt][3] - mn1);
-      ps0 += p00 + p01;
-      ps1 += p10 + p11;
-      pa[nt][0] = pack_h2(p00, p01);
-      pa[nt][1] = pack_h2(p10, p11);
-    }
-    l0 = l0 * al0 + ps0;
-    l1 = l1 * al1 + ps1;
-#pragma unroll
-    for (int nd = 0; nd < 8; ++nd) {
-      o[nd][0] *= al0;
-      o[nd][1] *= al0;
-      o[nd][2] *= al1;
-      o[nd][3] *= al1;
-    }
-    // O += P V: 4 key k-steps of 16, 8 dim n-tiles of 8
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-#pragma unroll
-      for (int nd = 0; nd < 8; ++nd) {
-        uint32_t b0, b1;
-        ldsm_x2_t(smem_u32(vsm + (kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * kFaPitch + nd * 8), b0, b1);
-        mma16816(o[nd], pa[2 * kk][0], pa[2 * kk][1], pa[2 * kk + 1][0], pa[2 * kk + 1][1], b0, b1);
-      }
-    }
-  }
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-  const float i0 = l0 > 0.0f ? 1.0f / l0 : 0.0f, i1 = l1 > 0.0f ? 1.0f / l1 : 0.0f;
-#pragma unroll
-  for (int nd = 0; nd < 8; ++nd) {
-    const int d = nd * 8 + 2 * tq;
-    if (row0 - t0 < rows)
-      *reinterpret_cast<__half2*>(a.out + (size_t)(b * a.T + row0) * a.ldo + h * D + d) =
-          __halves2half2(f16_sat(o[nd][0] * i0), f16_sat(o[nd][1] * i0));
-    if (row1 - t0 < rows)
-      *reinterpret_cast<__half2*>(a.out + (size_t)(b * a.T + row1) * a.ldo + h * D + d) =
-          __halves2half2(f16_sat(o[nd][2] * i1), f16_sat(o[nd][3] * i1));
-  }
-}
 
 // ------------------------------------------------------------------ decode, beam groups (tensor cores)
 // head_dim 64, beam search. One CTA (4 warps) per (head, request) over the whole
@@ -1161,8 +1019,7 @@ __global__ void __launch_bounds__(kBtThreads, 3) attn_decode_beam_mma_kernel(con
 // head_dim 64. One CTA = 128 query rows of one (head, sequence); query row r =
 // TMEM lane r. Key chunks of 64 slots aligned to start[b] (as in every other
 // attention kernel: a row's arithmetic never depends on its batch's padding).
-// One pass over the chunks (flash form, the tensor-core analogue of
-// attn_prefill_mma_kernel):
+// One pass over the chunks (flash form):
 //   S_j = Q K_j^T   tcgen05.mma kind::f16 M=128 N=64 K=64, f32 in TMEM (issued
 //                   as soon as every thread has read S_{j-1}, so it runs while
 //                   chunk j-1's P is computed; 128 TMEM columns per CTA keep

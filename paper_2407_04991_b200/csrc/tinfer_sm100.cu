@@ -598,15 +598,6 @@ int greedy_mma_mode() {
   return m;
 }
 
-// TF_PREFILL_TC=0: the mma.sync flash prefill instead of the tcgen05 kernel (A/B)
-bool prefill_tc_on() {
-  static const bool on = [] {
-    const char* e = getenv("TF_PREFILL_TC");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
   TF_REQUIRE(a.D >= 1 && a.D <= 128, TF_ERR_UNSUPPORTED, "head_dim must be in [1, 128]");
   const bool ws_ok = a.ws && a.cnt && a.max_chunks >= (a.cap + kPfKeysPerChunk - 1) / kPfKeysPerChunk;
@@ -662,13 +653,11 @@ void run_attention(const AttnArgs& a, cudaStream_t st, bool pdl) {
     TF_REQUIRE(smem <= kMaxSmem, TF_ERR_UNSUPPORTED, "cache capacity too large for decode kernel");
     ensure_attr(attn_decode_kernel, kMaxSmem);
     launch(attn_decode_kernel, dim3(a.NH, a.B), dim3(kDecThreads), smem, st, pdl, a);
-  } else if (a.D == 64 && a.ldq % 8 == 0 && a.ldo % 8 == 0 && prefill_tc_on()) {
+  } else if (a.D == 64 && a.ldq % 8 == 0 && a.ldo % 8 == 0) {
     // tcgen05 prefill attention: S and O in TMEM, softmax in registers
     ensure_attr(attn_prefill_tc_kernel, kTcSmem);
     launch(attn_prefill_tc_kernel, dim3((a.T + kTcRows - 1) / kTcRows, a.NH, a.B), dim3(kTcThreads), kTcSmem, st, pdl,
            a);
-  } else if (a.D == 64 && a.ldq % 8 == 0 && a.ldo % 2 == 0) {
-    launch(attn_prefill_mma_kernel, dim3((a.T + kFaRows - 1) / kFaRows, a.NH, a.B), dim3(128), 0, st, pdl, a);
   } else {
     const size_t smem = (size_t)kPfRows * a.D * sizeof(float) + (size_t)2 * kPfKeys * (a.D + 1) * 2;
     launch(attn_prefill_kernel, dim3((a.T + kPfRows - 1) / kPfRows, a.NH, a.B), dim3(128), smem, st,
