@@ -733,7 +733,8 @@ def run_sweep(args, w, model, dm, rank, world, dev):
     from paper_2407_04991_b200 import pipeline as PL
 
     reqs = make_prompts(model.config.vocab_size, w, 0)
-    settings = PL.PipelineSettings(max_batch_size=w["batch"], bucket_width=16, max_new_tokens=w["new"])
+    settings = PL.PipelineSettings(max_batch_size=args.c5_batch or w["batch"], bucket_width=16,
+                                   max_new_tokens=w["new"])
     plan = PL.plan_batches([len(r) for r in reqs], settings.max_batch_size, settings.bucket_width)
     mine = PL.rank_share(plan, world, rank, w["new"])
     # warm-up happens inside each worker thread (sessions are per thread), below
@@ -875,6 +876,7 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--c5-workers", type=int, default=2, help="inference worker threads per GPU (c5 sweep)")
+    ap.add_argument("--c5-batch", type=int, default=0, help="max rows per C5 batch (0: the workload's 128)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:

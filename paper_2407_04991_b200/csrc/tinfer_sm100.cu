@@ -780,7 +780,11 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
 
   tf_gemm_desc g{};
   g.m_tok = M;
-  g.force_swap = -1;
+  // prefill (T > 1): the layer GEMMs always take the full-K token-tile form, so a
+  // prompt's hidden states do not depend on how many tokens its batch has (the
+  // swap-AB split-K form, whose split count follows the token count, is for
+  // decode steps, where it is fixed for every batch of <= 128 rows)
+  g.force_swap = T > 1 ? 0 : -1;
   g.pdl = pdl ? 1 : 0;
 
   // decode: every kernel of layer l streams the next layer's copy of its own
@@ -997,6 +1001,7 @@ int forward(Session& s, const int* ids, const int* pos, int T, int mode, bool pd
   }
   // final_norm (model.py:497-498): only the last position feeds the lm_head
   tf_gemm_desc lg = g;
+  lg.force_swap = -1;  // full-K either way (no split-K for logits); swap-AB for <= 256 rows
   lg.m_tok = (mode == TF_FWD_LOGITS_ALL) ? M : B;
   lg.n_feat = m.vocab;
   lg.k = H;

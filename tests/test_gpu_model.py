@@ -115,6 +115,53 @@ def test_batch_invariance_ernie_heads(cuda_device, lo, hi, new):
         assert P.greedy_decode(m, prompts[i], new) == whole[i]
 
 
+def _teacher_forced_logits(model, prompts, forced, new):
+    """Last-position logits [steps][B, V] of prefill + (new - 1) decode steps fed
+    `forced` [B, new - 1] tokens, in the session shape batched_greedy_decode uses."""
+    import torch
+
+    from paper_2407_04991_b200 import _native as N
+    from paper_2407_04991_b200 import model as PM
+
+    c = model.config
+    ids, pos, pads, _ = PM._left_pad(c, prompts)
+    B, L = ids.shape
+    cap, mt = PM._session_shape(c, L, new)
+    dm = model.device_model()
+    out = []
+    with dm.lock, torch.cuda.device(dm.device):
+        s = dm.session(B, cap, mt, new, logits="last")
+        s.load_inputs(ids, pos, pads)
+        s.forward(L, N.FWD_LOGITS_LAST)
+        out.append(s.logits[:B].float().cpu().numpy())
+        for step in range(1, new):
+            slot = L + step - 1
+            s.load_inputs(forced[:, step - 1:step].astype(np.int32), (slot - pads).astype(np.int32).reshape(B, 1),
+                          pads, length=slot)
+            s.forward(1, N.FWD_LOGITS_LAST)
+            out.append(s.logits[:B].float().cpu().numpy())
+    return out
+
+
+def test_batch_invariance_logits_bitwise(cuda_device):
+    """The reference's contract (model.py:8-13) at the logit level, not only the
+    tokens: a row's prefill and decode-step logits are bitwise the same alone
+    and inside batches of 4, 32 and 128 ragged rows (12 heads x 64, H=768).
+    Prefill GEMMs take the full-K token-tile form for every batch; decode split
+    counts are fixed for <= 128 rows; attention chunks follow each row's start."""
+    cfg = P.ModelConfig(2048, 768, 2, 12, 64, 1024, 512, P.DType.F16, 1, 2)
+    m = P.init_random(cfg, 5)
+    prompts = O.synthetic_prompts(2048, 128, 60, seed=4)
+    prompts = [p[:20 + (13 * i) % 41] for i, p in enumerate(prompts)]
+    new = 6
+    forced = np.random.default_rng(2).integers(3, 2048, (128, new - 1))
+    whole = _teacher_forced_logits(m, prompts, forced, new)
+    for n in (1, 4, 32):
+        part = _teacher_forced_logits(m, prompts[:n], forced[:n], new)
+        for step in range(new):
+            assert np.array_equal(part[step], whole[step][:n]), (n, step)
+
+
 def oracle_margins(args, seed, prompts, new):
     """Per-(step, row) top-1 margins of the oracle restatement's own greedy run
     (F16 numerics), for margin-gating token comparisons."""
